@@ -1,0 +1,555 @@
+// ag_sm100.cu -- the bf16 All-Gather+GEMM path on 5th-generation tensor cores.
+//
+// One persistent, warp-specialised kernel per rank (ag_gemm.hpp:185-305
+// re-designed for sm_100a):
+//   warp 0      TMA producer.  Streams the A tile (128 x 64, SWIZZLE_128B)
+//               and four B boxes (64 x 64 each -> a 64 x 256 K x N panel,
+//               MN-major) into a STAGES-deep smem ring.  A k-block owned by
+//               this rank comes straight from its shard; a k-block owned by
+//               rank s comes from the local gathered buffer ("inbox", the
+//               reference's ag.inbox, m x k) once ready[m_blk][s] reaches
+//               this run's epoch (ld.acquire.sys spin, then
+//               fence.proxy.async so the TMA sees the generic-proxy bytes).
+//               The k loop starts at the rank's own shard, so the first
+//               16/W of every tile never waits.
+//   warp 1      MMA issuer (one thread): tcgen05.mma.cta_group::1.kind::f16,
+//               M=128 N=256 K=16, fp32 accumulators in TMEM (2 x 256
+//               columns, double-buffered so the epilogue of tile i overlaps
+//               the mainloop of tile i+1); tcgen05.commit frees smem stages.
+//   warps 2-5   epilogue: tcgen05.ld 32x32b -> bf16 -> global C.
+//   warps 6-7   gather (PULL): claim (m_blk, src) chunks from a global
+//               counter, copy them from the owner's shard over NVLink
+//               (128-bit peer loads) into the local inbox at column src*kw,
+//               then release ready[m_blk][src].  Each remote A byte crosses
+//               NVLink exactly once per rank (the reference re-pulls every
+//               A tile once per N tile, ag_gemm_test.cpp:134-143).
+// PUSH replaces the gather warps with a producer kernel on every rank that
+// stores its shard chunks into every peer's inbox and raises the peer's
+// ready cell (red.release.sys) -- the same consumer gate.
+// BASELINE gathers with copy engines between two world barriers and runs
+// the same kernel ungated.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "ag_internal.hpp"
+#include "sm100.cuh"
+
+namespace tfb {
+namespace {
+
+using namespace sm100;
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;           // 16 KB
+constexpr int B_BYTES = BK * BN * 2;           // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 48 KB
+constexpr int GROUP_M = 16;
+constexpr int NUM_THREADS = 256;
+constexpr int TMEM_COLS = 512;
+constexpr uint32_t IDESC = idesc_bf16(BM, BN, /*a MN-major*/ 0, /*b MN-major*/ 1);
+constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+struct AgTcParams {
+  int M, N, K, kw, W;
+  int own;          // rank whose shard map serves its own k-range; -1: all from inbox
+  int num_m, num_n, num_tiles, kb_total, kbw;
+  __nv_bfloat16* C;
+  const uint64_t* ready;  // [num_m][W] local board; nullptr: ungated
+  uint64_t epoch;
+  int gather;             // gather warps active (PULL)
+  __nv_bfloat16* inbox;   // local inbox, m x k
+  uint64_t* ready_w;      // writable view of `ready` (gather)
+  unsigned int* ctr;      // [0] gather chunk counter, [1] done counter
+  uint64_t watchdog_ns;
+  DevErr* err;
+  int board;
+  const __nv_bfloat16* peer_shard[64];
+};
+
+__device__ __forceinline__ void tile_coords(const AgTcParams& p, int t, int& mb, int& nb) {
+  const int per_group = GROUP_M * p.num_n;
+  const int group = t / per_group;
+  const int first_m = group * GROUP_M;
+  const int gsize = min(p.num_m - first_m, GROUP_M);
+  const int r = t % per_group;
+  mb = first_m + r % gsize;
+  nb = r / gsize;
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    ag_gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA_own,
+                         const __grid_constant__ CUtensorMap tmA_inbox,
+                         const __grid_constant__ CUtensorMap tmB, const AgTcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA_own);
+    tma_prefetch(&tmA_inbox);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===== TMA producer =====
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(p, t, mb, nb);
+        const int m0 = mb * BM, n0 = nb * BN;
+        uint64_t ready_mask = 0;
+        for (int i = 0; i < p.kb_total; ++i) {
+          const int kb = p.own >= 0 ? (i + p.own * p.kbw) % p.kb_total : i;
+          const int src = kb / p.kbw;
+          mbar_wait(&empty[stage], phase ^ 1);
+          const bool from_own = src == p.own;
+          if (!from_own && p.ready && !((ready_mask >> src) & 1ull)) {
+            wait_geq(p.ready + size_t(mb) * p.W + src, p.epoch, p.watchdog_ns, p.err, kWaitSignal,
+                     p.own, p.board, src, mb, 0);
+            fence_proxy_async_global();
+            ready_mask |= 1ull << src;
+          }
+          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          uint8_t* a_dst = smA + stage * A_BYTES;
+          if (from_own) tma_load_2d(a_dst, &tmA_own, &full[stage], kb * BK - p.own * p.kw, m0);
+          else tma_load_2d(a_dst, &tmA_inbox, &full[stage], kb * BK, m0);
+          uint8_t* b_dst = smB + stage * B_BYTES;
+#pragma unroll
+          for (int c = 0; c < BN / 64; ++c)
+            tma_load_2d(b_dst + c * (BK * 128), &tmB, &full[stage], n0 + 64 * c, kb * BK);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer =====
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+        for (int i = 0; i < p.kb_total; ++i) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smA + stage * A_BYTES);
+          const uint32_t b_addr = smem_u32(smB + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // A: K-major SW128, 8-row groups 1024 B apart; +32 B per K=16.
+            const uint64_t ad = smem_desc_sw128(a_addr + k * 32, 16, 1024);
+            // B: MN-major SW128, 64-col chunks 8 KB apart (LBO), 8-row K
+            // groups 1024 B apart (SBO); +16 rows (2 KB) per K=16.
+            const uint64_t bd = smem_desc_sw128(b_addr + k * 2048, BK * 128, 1024);
+            mma_bf16_ss(d_tmem, ad, bd, IDESC, (i | k) != 0);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+      }
+    }
+  } else if (warp < 6) {
+    // ===== epilogue: TMEM -> registers -> bf16 -> global =====
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      int mb, nb;
+      tile_coords(p, t, mb, nb);
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const int row = mb * BM + 32 * q + lane;
+      __nv_bfloat16* crow = p.C + size_t(row) * p.N;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + (uint32_t(32 * q) << 16) + uint32_t(acc * BN + 32 * c), r);
+        tmem_ld_wait();
+        const int col0 = nb * BN + 32 * c;
+        if (row < p.M) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            if (col0 + 8 * v < p.N) {
+              uint4 pk;
+              pk.x = pack_bf16x2(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1]));
+              pk.y = pack_bf16x2(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3]));
+              pk.z = pack_bf16x2(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5]));
+              pk.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
+              *reinterpret_cast<uint4*>(crow + col0 + 8 * v) = pk;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+  } else if (p.gather) {
+    // ===== gather (PULL): peer shard chunks -> local inbox + ready flags =====
+    const int gt = threadIdx.x - 6 * 32;  // 0..63
+    __shared__ unsigned int s_chunk;
+    const unsigned total = unsigned(p.num_m) * p.W;
+    const int vec_per_row = p.kw / 8;  // 16-byte vectors per shard row
+    for (;;) {
+      if (gt == 0) s_chunk = atomicAdd(&p.ctr[0], 1u);
+      named_bar(1, 64);
+      const unsigned c = s_chunk;
+      named_bar(1, 64);
+      if (c >= total) break;
+      const int mb = int(c / p.W);
+      const int src = (p.own + 1 + int(c % p.W)) % p.W;  // own shard last
+      const int r0 = mb * BM, rows = min(BM, p.M - r0);
+      const uint4* s = reinterpret_cast<const uint4*>(p.peer_shard[src] + size_t(r0) * p.kw);
+      const int nvec = rows * vec_per_row;
+      constexpr int U = 8;
+      for (int base = 0; base < nvec; base += 64 * U) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = base + u * 64 + gt;
+          if (e < nvec) v[u] = s[e];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = base + u * 64 + gt;
+          if (e < nvec) {
+            const int rr = e / vec_per_row, cv = e % vec_per_row;
+            *reinterpret_cast<uint4*>(p.inbox + size_t(r0 + rr) * p.K + size_t(src) * p.kw + 8 * cv) = v[u];
+          }
+        }
+      }
+      fence_proxy_async_global();
+      named_bar(1, 64);
+      if (gt == 0) {
+        __threadfence();
+        red_release_sys(p.ready_w + size_t(mb) * p.W + src, 1);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+  if (threadIdx.x == 0 && p.ctr) {
+    __threadfence();
+    if (atomicAdd(&p.ctr[1], 1u) == gridDim.x - 1) {
+      p.ctr[0] = 0;
+      p.ctr[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// PUSH producer (ag_gemm.hpp:241-260): claim (dst, m_blk) chunks, store this
+// rank's rows [m_blk*128, +128) x kw into dst's inbox at column self*kw, then
+// raise dst's ready[m_blk][self] with release semantics.  Never waits.
+struct PushParams {
+  const __nv_bfloat16* shard;
+  __nv_bfloat16* inbox[64];
+  uint64_t* ready[64];
+  int M, K, kw, W, self, num_m;
+  unsigned int* ctr;  // [0] chunk counter, [1] done
+};
+
+__global__ void __launch_bounds__(256) ag_push_kernel(const PushParams p) {
+  __shared__ unsigned int s_chunk;
+  const unsigned total = unsigned(p.num_m) * p.W;
+  const int vec_per_row = p.kw / 8;
+  for (;;) {
+    if (threadIdx.x == 0) s_chunk = atomicAdd(&p.ctr[0], 1u);
+    __syncthreads();
+    const unsigned c = s_chunk;
+    __syncthreads();
+    if (c >= total) break;
+    // m-block major so every consumer's first tiles are fed first; peers
+    // before self (the consumer reads its own shard directly).
+    const int mb = int(c / p.W);
+    const int dst = (p.self + 1 + int(c % p.W)) % p.W;
+    const int r0 = mb * BM, rows = min(BM, p.M - r0);
+    const uint4* s = reinterpret_cast<const uint4*>(p.shard + size_t(r0) * p.kw);
+    __nv_bfloat16* ib = p.inbox[dst];
+    const int nvec = rows * vec_per_row;
+    constexpr int U = 4;
+    for (int base = 0; base < nvec; base += 256 * U) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = base + u * 256 + threadIdx.x;
+        if (e < nvec) v[u] = s[e];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = base + u * 256 + threadIdx.x;
+        if (e < nvec) {
+          const int rr = e / vec_per_row, cv = e % vec_per_row;
+          *reinterpret_cast<uint4*>(ib + size_t(r0 + rr) * p.K + size_t(p.self) * p.kw + 8 * cv) = v[u];
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      fence_sys();
+      red_release_sys(p.ready[dst] + size_t(mb) * p.W + p.self, 1);
+    }
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&p.ctr[1], 1u) == gridDim.x - 1) {
+      p.ctr[0] = 0;
+      p.ctr[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// ---- host ------------------------------------------------------------------------
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 map: `inner` contiguous elements per row, `outer` rows, row pitch
+// `pitch_elems`; box {box_inner, box_outer}; 128-byte swizzle.
+tf_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                   uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {pitch_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return TF_OK;
+}
+
+}  // namespace
+
+// Launches the tensor-core GEMM for local rank r.  own: shard owner index
+// for the shard map (-1 => every k-block from `inbox`).
+static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void* shard,
+                             const void* inbox, const void* b, void* c, const uint64_t* ready,
+                             uint64_t epoch, int own, int gather, const AgTcParams& proto,
+                             cudaStream_t st, int board, unsigned grid_cap) {
+  const int W = w->W;
+  const size_t kw = sh.k / W;
+  CUtensorMap mOwn, mInbox, mB;
+  if (shard) TFB_CHECK(make_map(&mOwn, shard, kw, sh.m, kw, BK, BM));
+  if (inbox) TFB_CHECK(make_map(&mInbox, inbox, sh.k, sh.m, sh.k, BK, BM));
+  if (!shard) mOwn = mInbox;
+  if (!inbox) mInbox = mOwn;
+  TFB_CHECK(make_map(&mB, b, sh.n, sh.k, sh.n, 64, BK));
+  AgTcParams p = proto;
+  p.M = int(sh.m);
+  p.N = int(sh.n);
+  p.K = int(sh.k);
+  p.kw = int(kw);
+  p.W = W;
+  p.own = own;
+  p.num_m = int((sh.m + BM - 1) / BM);
+  p.num_n = int((sh.n + BN - 1) / BN);
+  p.num_tiles = p.num_m * p.num_n;
+  p.kb_total = int(sh.k / BK);
+  p.kbw = int(kw / BK);
+  p.C = static_cast<__nv_bfloat16*>(c);
+  p.ready = ready;
+  p.epoch = epoch;
+  p.gather = gather;
+  p.watchdog_ns = w->watchdog_ns;
+  p.err = w->err_dev;
+  p.board = board;
+  static bool attr_set[64] = {};
+  const int dev = w->ranks[r].device;
+  cudaSetDevice(dev);
+  if (!attr_set[dev & 63]) {
+    TFB_CUDA(cudaFuncSetAttribute(ag_gemm_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(SMEM_BYTES)));
+    attr_set[dev & 63] = true;
+  }
+  const unsigned grid = std::max(1u, std::min(unsigned(p.num_tiles), grid_cap));
+  ag_gemm_sm100_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(mOwn, mInbox, mB, p);
+  TFB_CUDA(cudaGetLastError());
+  ++w->launches;
+  return TF_OK;
+}
+
+tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, void* const* a_shard,
+                      const void* const* b, void* const* c, void* const* gathered,
+                      const std::vector<cudaStream_t>& streams) {
+  const int W = w->W;
+  const size_t m = sh.m, n = sh.n, k = sh.k, kw = k / W;
+  if (kw % BK != 0)
+    return set_error(TF_ERR_SHAPE, "ag_gemm(bf16): k / world_size = " + std::to_string(kw) +
+                                       " must be a multiple of 64");
+  if (n % 8 != 0) return set_error(TF_ERR_SHAPE, "ag_gemm(bf16): n must be a multiple of 8");
+  if (m > (size_t(1) << 31) || n > (size_t(1) << 31) || k > (size_t(1) << 31))
+    return set_error(TF_ERR_SHAPE, "ag_gemm(bf16): dimensions must fit in int32");
+  const int num_m = int((m + BM - 1) / BM);
+  const unsigned sms = unsigned(w->sm_count);
+
+  if (W == 1) {
+    // No exchange: the fused kernel degenerates to the GEMM over the shard.
+    if (!w->ranks[0].local) return TF_OK;
+    AgTcParams proto{};
+    TFB_CHECK(launch_gemm(w, 0, sh, a_shard[0], nullptr, b[0], c[0], nullptr, 0, 0, 0, proto,
+                          streams[0], -1, sms));
+    if (gathered && gathered[0])
+      TFB_CUDA(cudaMemcpyAsync(gathered[0], a_shard[0], m * k * 2, cudaMemcpyDefault, streams[0]));
+    return TF_OK;
+  }
+
+  // Gathered operand per rank: caller's buffer, else the heap inbox
+  // (double-buffered by epoch parity for PUSH, where peers write into it).
+  size_t inbox_off = 0, ctr_off = 0;
+  TFB_CHECK(heap_get(w, "ag.inbox.bf16[" + std::to_string(m * k) + "]", 2 * m * k * 2, &inbox_off));
+  TFB_CHECK(heap_get(w, "ag.ctr", 256, &ctr_off));
+  BoardEntry rb;
+  TFB_CHECK(board_next_epoch(w, "ag.ready", num_m, W, &rb));
+  w->ag_flags = FlagSnapshot{w->board_names[rb.id], size_t(num_m) * W, rb.epoch};
+  const int parity = int(rb.epoch & 1);
+  auto inbox_of = [&](int r) -> __nv_bfloat16* {
+    if (gathered && gathered[r]) return static_cast<__nv_bfloat16*>(gathered[r]);
+    return reinterpret_cast<__nv_bfloat16*>(w->ptr(r, inbox_off)) + size_t(parity) * m * k;
+  };
+  auto ready_of = [&](int r) { return reinterpret_cast<uint64_t*>(w->ptr(r, rb.offset)); };
+  auto ctr_of = [&](int r, int slot) { return reinterpret_cast<unsigned int*>(w->ptr(r, ctr_off)) + slot * 4; };
+
+  if (variant == TF_AG_BASELINE) {
+    TFB_CHECK(world_barrier(w, streams));
+    for (int r = 0; r < W; ++r) {
+      if (!w->ranks[r].local) continue;
+      cudaSetDevice(w->ranks[r].device);
+      for (int s = 0; s < W; ++s)
+        TFB_CUDA(cudaMemcpy2DAsync(inbox_of(r) + size_t(s) * kw, k * 2, a_shard[s], kw * 2, kw * 2, m,
+                                   cudaMemcpyDefault, streams[r]));
+    }
+    TFB_CHECK(world_barrier(w, streams));
+    for (int r = 0; r < W; ++r) {
+      if (!w->ranks[r].local) continue;
+      AgTcParams proto{};
+      TFB_CHECK(launch_gemm(w, r, sh, nullptr, inbox_of(r), b[r], c[r], nullptr, 0, -1, 0, proto,
+                            streams[r], -1, sms));
+    }
+    return TF_OK;
+  }
+
+  if (variant == TF_AG_PULL) {
+    for (int r = 0; r < W; ++r) {
+      if (!w->ranks[r].local) continue;
+      AgTcParams proto{};
+      for (int s = 0; s < W; ++s) proto.peer_shard[s] = static_cast<const __nv_bfloat16*>(a_shard[s]);
+      proto.inbox = inbox_of(r);
+      proto.ready_w = ready_of(r);
+      proto.ctr = ctr_of(r, 0);
+      TFB_CHECK(launch_gemm(w, r, sh, a_shard[r], inbox_of(r), b[r], c[r], ready_of(r), rb.epoch, r,
+                            1, proto, streams[r], rb.id, sms));
+    }
+    return TF_OK;
+  }
+
+  // PUSH: producers first on the side streams (they never wait), then the
+  // gated GEMMs with a few SMs left for the producers.
+  const unsigned push_ctas = 16;
+  for (int r = 0; r < W; ++r) {
+    if (!w->ranks[r].local) continue;
+    cudaSetDevice(w->ranks[r].device);
+    cudaEvent_t ev;
+    TFB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    TFB_CUDA(cudaEventRecord(ev, streams[r]));
+    TFB_CUDA(cudaStreamWaitEvent(w->ranks[r].side, ev, 0));
+    cudaEventDestroy(ev);
+    PushParams pp{};
+    pp.shard = static_cast<const __nv_bfloat16*>(a_shard[r]);
+    for (int d = 0; d < W; ++d) {
+      pp.inbox[d] = inbox_of(d);
+      pp.ready[d] = ready_of(d);
+    }
+    pp.M = int(m);
+    pp.K = int(k);
+    pp.kw = int(kw);
+    pp.W = W;
+    pp.self = r;
+    pp.num_m = num_m;
+    pp.ctr = ctr_of(r, 1);
+    ag_push_kernel<<<push_ctas, 256, 0, w->ranks[r].side>>>(pp);
+    TFB_CUDA(cudaGetLastError());
+    ++w->launches;
+  }
+  for (int r = 0; r < W; ++r) {
+    if (!w->ranks[r].local) continue;
+    AgTcParams proto{};
+    TFB_CHECK(launch_gemm(w, r, sh, a_shard[r], inbox_of(r), b[r], c[r], ready_of(r), rb.epoch, r, 0,
+                          proto, streams[r], rb.id, sms > push_ctas ? sms - push_ctas : 1));
+    cudaEvent_t ev;
+    TFB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    TFB_CUDA(cudaEventRecord(ev, w->ranks[r].side));
+    TFB_CUDA(cudaStreamWaitEvent(streams[r], ev, 0));
+    cudaEventDestroy(ev);
+  }
+  return TF_OK;
+}
+
+}  // namespace tfb

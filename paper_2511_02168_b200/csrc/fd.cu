@@ -1,0 +1,879 @@
+// fd.cu -- multi-GPU Flash Decode (flash_decode.hpp), all four schedules.
+//
+// Work decomposition (every schedule shares it, so every schedule folds the
+// same partial bits and outputs are bitwise identical across schedules and
+// across ranks, as flash_decode.hpp:35-36 promises):
+//   group  g = (b, kv_head): one KV stream [len][d] shared by gs = Hq/Hkv
+//          q-heads (GQA; gs = 1 is the reference's MHA).
+//   split  the rank's len = L/W positions are cut into S contiguous splits
+//          (S from the shape only).  A CTA computes one (group, split)
+//          attention partial for all gs heads (attention_partial,
+//          tilemath.hpp:145-181) and the LAST split to finish (ticket)
+//          folds the S split partials in ascending order into the rank's
+//          partial for the group.
+//   wire   the rank partial leaves as rows [m | l | o[d]] fp32
+//          (tilemath.hpp:244-258), one per (b, q-head):
+//          inbox[src][b][hq][d+2] (flash_decode.hpp:353-368).
+//   fold   ascending source order, combine_partials (tilemath.hpp:186-220),
+//          finalize (tilemath.hpp:225-239).
+//
+// Schedules:
+//   bsp            attention(publish) | barrier | gather | barrier | fold
+//   independent_ag attention(publish) | barrier | push+signal, wait-all |
+//                  barrier | fold
+//   fine_waits     attention(publish) | barrier | push+signal | fold with
+//                  per-source waits
+//   fused          ONE persistent launch: attention, split fold, push to
+//                  every peer + red.release.sys flag per (src, group), then
+//                  flag-gated ascending fold and finalize.  CTAs claim
+//                  compute items dynamically and only wait once no compute
+//                  item is left, so every push happens before any CTA
+//                  blocks: deadlock-free without co-residency assumptions.
+//
+// Attention kernels:
+//   fast     bf16 K/V, d = 128, gs = 8: register-only tensor-core decode.
+//            S^T = K.Q^T with mma.m16n8k16 (16 keys x 8 heads, no padding),
+//            P^T and V^T reach their MMA fragments through movmatrix
+//            transposes of plain 16-byte row loads -- no shared memory in
+//            the main loop, every KV byte read once with 128-bit
+//            L1::no_allocate loads.
+//   generic  any d <= 256, any gs <= 32, fp32 or bf16: one warp per q-head,
+//            ascending keys, lanes split d.  Runs the reference's own test
+//            shapes (d = 4, 8, 16; MHA).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <string>
+
+#include "world.hpp"
+
+namespace tfb {
+namespace {
+
+constexpr int kMaxLocal = 16;  // local ranks per launch (loopback worlds)
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+struct FdRank {
+  const void* q;
+  const void* k;
+  const void* v;
+  void* out;
+  float* pub;        // [B][Hq][d+2]: this rank's published partial (bsp/ag)
+  float* inbox;      // [W][B][Hq][d+2] local inbox (fold source)
+  uint64_t* flags;   // [W][G] local flag board
+  int rank;          // global rank id
+};
+
+struct FdParams {
+  int nlocal;
+  int W, B, Hq, Hkv, gs, d;
+  size_t len;        // positions per rank
+  int S;             // splits per group
+  size_t split_len;  // positions per split (last split may be shorter)
+  float scale;
+  int kv_bf16, out_bf16;
+  uint64_t epoch;       // ticket epoch (per ticket buffer)
+  uint64_t flag_epoch;  // flag-board epoch (per board geometry)
+  uint64_t watchdog_ns;
+  DevErr* err;
+  int board;
+  float* ws;                  // [nlocal][G][S][gs][d+2] split partials
+  unsigned long long* ticket; // [nlocal][G] epoch-valued tickets
+  unsigned int* ctr;          // [0] compute, [1] fold, [2] done
+  int push;                   // push rank partials to every inbox (+ signal)
+  int fold_inline;            // fused: fold after compute
+  float* inbox_all[64];       // every rank's inbox (this parity), this process' view
+  uint64_t* flags_all[64];    // every rank's flag board
+  FdRank r[kMaxLocal];
+};
+
+// ---- combine monoid on wire rows (tilemath.hpp:186-220) -------------------
+// One implementation for every fold so all schedules agree bit for bit.
+// __fmul_rn/__fadd_rn keep the compiler from contracting to FMA, matching
+// the reference's separately rounded arithmetic.
+struct Part {
+  float m, l;
+};
+__device__ __forceinline__ void combine_scalars(float am, float al, float bm, float bl,
+                                                float* m, float* l, float* ax, float* ay,
+                                                int* mode) {
+  if (al == 0.0f) {
+    *mode = 1;  // take b
+    *m = bm;
+    *l = bl;
+    return;
+  }
+  if (bl == 0.0f) {
+    *mode = 2;  // keep a
+    *m = am;
+    *l = al;
+    return;
+  }
+  *mode = 0;
+  const float mm = fmaxf(am, bm);
+  *ax = expf(am - mm);
+  *ay = expf(bm - mm);
+  *m = mm;
+  *l = __fadd_rn(__fmul_rn(al, *ax), __fmul_rn(bl, *ay));
+}
+
+__device__ __forceinline__ float combine_elem(int mode, float ao, float bo, float ax, float ay) {
+  if (mode == 1) return bo;
+  if (mode == 2) return ao;
+  return __fadd_rn(__fmul_rn(ao, ax), __fmul_rn(bo, ay));
+}
+
+// acc (one wire row, in smem or registers per thread) <- acc (+) row.
+// Cooperative over `nthreads` threads; each thread owns elements e = tid +
+// k*nthreads of o.  Caller provides m/l in shared memory.
+template <int MAXE>
+__device__ __forceinline__ void fold_row(float& am, float& al, float* ao, const float* row,
+                                         int d, int tid, int nthreads) {
+  const float bm = row[0], bl = row[1];
+  float m, l, ax = 0.f, ay = 0.f;
+  int mode;
+  combine_scalars(am, al, bm, bl, &m, &l, &ax, &ay, &mode);
+#pragma unroll
+  for (int i = 0; i < MAXE; ++i) {
+    const int e = tid + i * nthreads;
+    if (e < d) ao[i] = combine_elem(mode, ao[i], row[2 + e], ax, ay);
+  }
+  am = m;
+  al = l;
+}
+
+__device__ __forceinline__ float load_kv(const void* p, size_t idx, int bf16) {
+  return bf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(p)[idx])
+              : static_cast<const float*>(p)[idx];
+}
+
+__device__ __forceinline__ void store_out(void* p, size_t idx, float v, int bf16) {
+  if (bf16) static_cast<__nv_bfloat16*>(p)[idx] = __float2bfloat16_rn(v);
+  else static_cast<float*>(p)[idx] = v;
+}
+
+// ---- generic split partial: one warp per q-head ----------------------------
+// Writes ws rows [m | l | o] (natural-log m) for the gs heads of the group.
+__device__ void generic_split(const FdParams& P, int lr, int g, int sp, float* wsrow) {
+  const FdRank& R = P.r[lr];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = g / P.Hkv, kvh = g % P.Hkv;
+  const size_t k0 = size_t(sp) * P.split_len;
+  const size_t k1 = min(P.len, k0 + P.split_len);
+  const int d = P.d;
+  const size_t kvbase = (size_t(b) * P.Hkv + kvh) * P.len * d;
+  for (int h = warp; h < P.gs; h += blockDim.x >> 5) {
+    const int hq = kvh * P.gs + h;
+    const size_t qbase = (size_t(b) * P.Hq + hq) * d;
+    float q[8], o[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = lane + 32 * i;
+      q[i] = e < d ? load_kv(R.q, qbase + e, P.kv_bf16) : 0.0f;
+      o[i] = 0.0f;
+    }
+    float m = -INFINITY, l = 0.0f;
+    for (size_t j = k0; j < k1; ++j) {
+      float part = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int e = lane + 32 * i;
+        if (e < d) part = __fadd_rn(part, __fmul_rn(q[i], load_kv(R.k, kvbase + j * d + e, P.kv_bf16)));
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) part = __fadd_rn(part, __shfl_xor_sync(0xffffffffu, part, off));
+      const float s = __fmul_rn(part, P.scale);
+      if (!isfinite(s)) {
+        if (lane == 0)
+          raise_err(P.err, TF_ERR_NUMERIC, kNumeric, R.rank, -1, 0, 0, 0, 0,
+                    (uint64_t(hq) << 32) | uint64_t(size_t(R.rank) * P.len + j));
+        return;
+      }
+      const float mn = fmaxf(m, s);
+      const float alpha = expf(m - mn);
+      const float w = expf(s - mn);
+      l = __fadd_rn(__fmul_rn(l, alpha), w);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int e = lane + 32 * i;
+        if (e < d)
+          o[i] = __fadd_rn(__fmul_rn(o[i], alpha), __fmul_rn(w, load_kv(R.v, kvbase + j * d + e, P.kv_bf16)));
+      }
+      m = mn;
+    }
+    float* row = wsrow + size_t(h) * (d + 2);
+    if (lane == 0) {
+      row[0] = m;
+      row[1] = l;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = lane + 32 * i;
+      if (e < d) row[2 + e] = o[i];
+    }
+  }
+}
+
+// ---- fast split partial: bf16, d = 128, gs = 8 -----------------------------
+__device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t movtrans(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t w4(const uint4& v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
+constexpr int kFastWarps = 4;
+constexpr int kFastThreads = kFastWarps * 32;
+
+// d index held by O^T accumulator row r of PV tile (i, j) (see header).
+__device__ __forceinline__ int fast_d(int i, int j, int r) {
+  return 32 * i + 8 * (r >> 1) + 2 * j + (r & 1);
+}
+
+// One warp: keys [kb, ke) of the group's stream; leaves its log2-domain
+// partial for the 8 heads in smem (m2[8], l[8], o[8][128]).
+__device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
+                                const __nv_bfloat16* V, const __nv_bfloat16* Q, size_t kb,
+                                size_t ke, float* sm_m, float* sm_l, float* sm_o, int* bad) {
+  const int lane = threadIdx.x & 31;
+  const int gq = lane >> 2, t = lane & 3;
+  const float sl2 = P.scale * kLog2e;
+  // Q^T fragments: head gq, d positions 8(t+4i) .. +8.
+  uint4 qv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) qv[i] = *reinterpret_cast<const uint4*>(Q + size_t(gq) * 128 + 8 * (t + 4 * i));
+  float o[8][4];
+#pragma unroll
+  for (int x = 0; x < 8; ++x) o[x][0] = o[x][1] = o[x][2] = o[x][3] = 0.0f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
+  int badl = 0;
+  for (size_t j0 = kb; j0 < ke; j0 += 16) {
+    const size_t ka = j0 + gq, kb8 = j0 + gq + 8;
+    const bool va = ka < ke, vb = kb8 < ke;
+    uint4 k_a[4], k_b[4], v_a[4], v_b[4];
+    const uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      k_a[i] = va ? ldg_stream(K + ka * 128 + 8 * (t + 4 * i)) : z;
+      k_b[i] = vb ? ldg_stream(K + kb8 * 128 + 8 * (t + 4 * i)) : z;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v_a[i] = va ? ldg_stream(V + ka * 128 + 8 * (t + 4 * i)) : z;
+      v_b[i] = vb ? ldg_stream(V + kb8 * 128 + 8 * (t + 4 * i)) : z;
+    }
+    // S^T = K . Q^T over 8 k-steps of 16 d.
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int st = 0; st < 8; ++st) {
+      const int i = st >> 1, h = st & 1;
+      mma_bf16(s, w4(k_a[i], 2 * h), w4(k_b[i], 2 * h), w4(k_a[i], 2 * h + 1),
+               w4(k_b[i], 2 * h + 1), w4(qv[i], 2 * h), w4(qv[i], 2 * h + 1));
+    }
+    // log2-domain scores; rows g (key ka) and g+8 (key kb8); cols 2t, 2t+1.
+    float x0 = va ? s[0] * sl2 : -INFINITY, x1 = va ? s[1] * sl2 : -INFINITY;
+    float x2 = vb ? s[2] * sl2 : -INFINITY, x3 = vb ? s[3] * sl2 : -INFINITY;
+    badl |= (va && !(fabsf(x0) < INFINITY && fabsf(x1) < INFINITY)) ||
+            (vb && !(fabsf(x2) < INFINITY && fabsf(x3) < INFINITY));
+    float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+    }
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+    const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);
+    m0 = mn0;
+    m1 = mn1;
+    const __nv_bfloat162 p01 = __floats2bfloat162_rn(exp2f(x0 - mn0), exp2f(x1 - mn1));
+    const __nv_bfloat162 p23 = __floats2bfloat162_rn(exp2f(x2 - mn0), exp2f(x3 - mn1));
+    // Normalizer from the same rounded weights the PV product uses.
+    l0 = l0 * al0 + (__low2float(p01) + __low2float(p23));
+    l1 = l1 * al1 + (__high2float(p01) + __high2float(p23));
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      o[x][0] *= al0;
+      o[x][1] *= al1;
+      o[x][2] *= al0;
+      o[x][3] *= al1;
+    }
+    const uint32_t pb0 = movtrans(*reinterpret_cast<const uint32_t*>(&p01));
+    const uint32_t pb1 = movtrans(*reinterpret_cast<const uint32_t*>(&p23));
+    // O^T += V^T . P^T: tile (i, jp) covers d rows fast_d(i, 2jp, .) and
+    // fast_d(i, 2jp+1, .).
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+#pragma unroll
+      for (int jp = 0; jp < 2; ++jp) {
+        const uint32_t a0 = movtrans(w4(v_a[i], 2 * jp));
+        const uint32_t a1 = movtrans(w4(v_a[i], 2 * jp + 1));
+        const uint32_t a2 = movtrans(w4(v_b[i], 2 * jp));
+        const uint32_t a3 = movtrans(w4(v_b[i], 2 * jp + 1));
+        mma_bf16(o[2 * i + jp], a0, a1, a2, a3, pb0, pb1);
+      }
+    }
+  }
+  // Per-head normalizer: sum the per-lane partials over the 8 key rows.
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+  }
+  if (gq == 0) {
+    sm_m[2 * t] = m0;
+    sm_m[2 * t + 1] = m1;
+    sm_l[2 * t] = l0;
+    sm_l[2 * t + 1] = l1;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int jp = 0; jp < 2; ++jp) {
+      const float* c = o[2 * i + jp];
+      const int dA = fast_d(i, 2 * jp, gq), dB = fast_d(i, 2 * jp + 1, gq);
+      sm_o[(2 * t) * 128 + dA] = c[0];
+      sm_o[(2 * t + 1) * 128 + dA] = c[1];
+      sm_o[(2 * t) * 128 + dB] = c[2];
+      sm_o[(2 * t + 1) * 128 + dB] = c[3];
+    }
+  }
+  if (badl) *bad = 1;
+}
+
+struct FastSmem {
+  float m[kFastWarps][8];
+  float l[kFastWarps][8];
+  float o[kFastWarps][8 * 128];
+  int bad;
+};
+
+__device__ void fast_split(const FdParams& P, int lr, int g, int sp, float* wsrow,
+                           FastSmem& sm) {
+  const FdRank& R = P.r[lr];
+  const int warp = threadIdx.x >> 5;
+  const int b = g / P.Hkv, kvh = g % P.Hkv;
+  const size_t k0 = size_t(sp) * P.split_len;
+  const size_t k1 = min(P.len, k0 + P.split_len);
+  const size_t per = ((k1 - k0 + kFastWarps - 1) / kFastWarps + 15) / 16 * 16;
+  const size_t wb = min(k1, k0 + warp * per), we = min(k1, wb + per);
+  const __nv_bfloat16* K = static_cast<const __nv_bfloat16*>(R.k) + (size_t(b) * P.Hkv + kvh) * P.len * 128;
+  const __nv_bfloat16* V = static_cast<const __nv_bfloat16*>(R.v) + (size_t(b) * P.Hkv + kvh) * P.len * 128;
+  const __nv_bfloat16* Q = static_cast<const __nv_bfloat16*>(R.q) + (size_t(b) * P.Hq + kvh * 8) * 128;
+  if (threadIdx.x == 0) sm.bad = 0;
+  __syncthreads();
+  fast_warp_range(P, K, V, Q, wb, we, sm.m[warp], sm.l[warp], sm.o[warp], &sm.bad);
+  __syncthreads();
+  if (sm.bad) {
+    if (threadIdx.x == 0)
+      raise_err(P.err, TF_ERR_NUMERIC, kNumeric, R.rank, -1, 0, 0, 0, 0,
+                (uint64_t(kvh * 8) << 32) | uint64_t(size_t(R.rank) * P.len + k0));
+    return;
+  }
+  // Ascending fold of the warp partials (log2 domain), then natural m.
+  for (int e = threadIdx.x; e < 8 * 128; e += blockDim.x) {
+    const int h = e >> 7, dd = e & 127;
+    float m = -INFINITY, l = 0.0f, o = 0.0f;
+#pragma unroll
+    for (int w = 0; w < kFastWarps; ++w) {
+      const float bl = sm.l[w][h];
+      if (bl == 0.0f) continue;
+      const float bm = sm.m[w][h], bo = sm.o[w][h * 128 + dd];
+      if (l == 0.0f) {
+        m = bm;
+        l = bl;
+        o = bo;
+        continue;
+      }
+      const float mm = fmaxf(m, bm);
+      const float ax = exp2f(m - mm), ay = exp2f(bm - mm);
+      l = l * ax + bl * ay;
+      o = o * ax + bo * ay;
+      m = mm;
+    }
+    float* row = wsrow + size_t(h) * 130;
+    if (dd == 0) {
+      row[0] = m * kLn2;
+      row[1] = l;
+    }
+    row[2 + dd] = o;
+  }
+}
+
+// ---- the persistent kernel ------------------------------------------------
+template <bool FAST>
+__global__ void __launch_bounds__(kFastThreads) fd_attention_kernel(const FdParams P) {
+  __shared__ unsigned int s_item;
+  __shared__ int s_last;
+  __shared__ FastSmem fsm;
+  const int G = P.B * P.Hkv;
+  const unsigned total = unsigned(P.nlocal) * G * P.S;
+  const int d = P.d, row_len = d + 2;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(&P.ctr[0], 1u);
+    __syncthreads();
+    const unsigned item = s_item;
+    __syncthreads();
+    if (item >= total) break;
+    const int sp = item % P.S;
+    const int g = (item / P.S) % G;
+    const int lr = item / (unsigned(P.S) * G);
+    float* grp = P.ws + ((size_t(lr) * G + g) * P.S) * P.gs * row_len;
+    float* wsrow = grp + size_t(sp) * P.gs * row_len;
+    if (FAST) fast_split(P, lr, g, sp, wsrow, fsm);
+    else generic_split(P, lr, g, sp, wsrow);
+    if (err_raised(P.err)) break;
+    // Ticket: the last split of the group folds all S splits.
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const unsigned long long tk = atomicAdd(&P.ticket[size_t(lr) * G + g], 1ull);
+      s_last = (tk == P.epoch * P.S - 1) ? 1 : 0;
+      __threadfence();
+    }
+    __syncthreads();
+    if (!s_last) continue;
+    const FdRank& R = P.r[lr];
+    const int b = g / P.Hkv, kvh = g % P.Hkv;
+    // Rank partial rows for (b, kvh*gs + h): fold splits ascending.
+    for (int h = threadIdx.x >> 5; h < P.gs; h += blockDim.x >> 5) {
+      const int lane = threadIdx.x & 31;
+      float am = -INFINITY, al = 0.0f, ao[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ao[i] = 0.0f;
+      for (int s = 0; s < P.S; ++s) {
+        const volatile float* src = grp + (size_t(s) * P.gs + h) * row_len;
+        fold_row<8>(am, al, ao, const_cast<const float*>(src), d, lane, 32);
+      }
+      const int hq = kvh * P.gs + h;
+      const size_t roff = (size_t(b) * P.Hq + hq) * row_len;
+      auto emit = [&](float* dst) {
+        if (lane == 0) {
+          dst[0] = am;
+          dst[1] = al;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int e = lane + 32 * i;
+          if (e < d) dst[2 + e] = ao[i];
+        }
+      };
+      if (P.push) {
+        for (int dst = 0; dst < P.W; ++dst)
+          emit(P.inbox_all[dst] + size_t(R.rank) * P.B * P.Hq * row_len + roff);
+      } else {
+        emit(R.pub + roff);
+      }
+    }
+    if (P.push) {
+      __syncthreads();
+      if (threadIdx.x < P.W) {
+        fence_sys();
+        red_release_sys(P.flags_all[threadIdx.x] + size_t(R.rank) * G + g, 1);
+      }
+    }
+  }
+  if (P.fold_inline && !err_raised(P.err)) {
+    // Fold phase: every compute item has been claimed by a CTA that never
+    // blocks before pushing, so these waits always complete.
+    const unsigned nfold = unsigned(P.nlocal) * G;
+    for (;;) {
+      __syncthreads();
+      if (threadIdx.x == 0) s_item = atomicAdd(&P.ctr[1], 1u);
+      __syncthreads();
+      const unsigned item = s_item;
+      if (item >= nfold) break;
+      const int g = item % G, lr = item / G;
+      const FdRank& R = P.r[lr];
+      const int b = g / P.Hkv, kvh = g % P.Hkv;
+      if (threadIdx.x == 0) {
+        s_last = 1;
+        for (int s = 0; s < P.W; ++s)
+          if (!wait_geq(R.flags + size_t(s) * G + g, P.flag_epoch, P.watchdog_ns, P.err, kWaitSignal,
+                        R.rank, P.board, s, g, 0)) {
+            s_last = 0;
+            break;
+          }
+      }
+      __syncthreads();
+      if (!s_last) break;
+      for (int h = threadIdx.x >> 5; h < P.gs; h += blockDim.x >> 5) {
+        const int lane = threadIdx.x & 31;
+        const int hq = kvh * P.gs + h;
+        const size_t roff = (size_t(b) * P.Hq + hq) * row_len;
+        float am = -INFINITY, al = 0.0f, ao[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ao[i] = 0.0f;
+        for (int s = 0; s < P.W; ++s) {
+          const float* src = R.inbox + size_t(s) * P.B * P.Hq * row_len + roff;
+          fold_row<8>(am, al, ao, src, d, lane, 32);
+        }
+        if (al == 0.0f) {
+          if (lane == 0)
+            raise_err(P.err, TF_ERR_EMPTY_ATTENTION, kEmpty, R.rank, -1, 0, 0, 0, 0, uint64_t(hq));
+          continue;
+        }
+        const size_t ooff = (size_t(b) * P.Hq + hq) * d;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int e = lane + 32 * i;
+          if (e < d) store_out(R.out, ooff + e, ao[i] / al, P.out_bf16);
+        }
+      }
+    }
+  }
+  // Last CTA out resets the work counters for the next launch.
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&P.ctr[2], 1u) == gridDim.x - 1) {
+      P.ctr[0] = 0;
+      P.ctr[1] = 0;
+      P.ctr[2] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// Push this rank's published rows into every inbox slot `self` and signal
+// (dst, row=self, slot=0); block 0 then optionally waits for every source
+// (independent_ag's collective-internal wait-all, flash_decode.hpp:277-284).
+__global__ void fd_push_kernel(const float* pub, size_t row_floats, int self, int W,
+                               FdParams P, int wait_all) {
+  const int dst = blockIdx.x;
+  float* ib = P.inbox_all[dst] + size_t(self) * row_floats;
+  for (size_t e = threadIdx.x; e < row_floats; e += blockDim.x) ib[e] = pub[e];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fence_sys();
+    red_release_sys(P.flags_all[dst] + self, 1);
+  }
+  if (wait_all && dst == 0 && threadIdx.x == 0) {
+    for (int s = 0; s < W; ++s)
+      if (!wait_geq(P.r[0].flags + s, P.flag_epoch, P.watchdog_ns, P.err, kWaitSignal, self, P.board, s,
+                    0, 0))
+        return;
+  }
+}
+
+// BSP gather (flash_decode.hpp:234-241): copy every source's published row
+// into the local stage [W][B][Hq][d+2].
+__global__ void fd_gather_kernel(float* stage, size_t row_floats, FdParams P, int W) {
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < size_t(W) * row_floats;
+       e += size_t(gridDim.x) * blockDim.x) {
+    const int s = int(e / row_floats);
+    stage[e] = P.inbox_all[s][e % row_floats];  // inbox_all carries the pubs here
+  }
+}
+
+// Fold kernel (bsp / independent_ag / fine_waits): one CTA per (b, hq) row,
+// optional per-source waits right before each fold (fine_waits,
+// flash_decode.hpp:333-338).
+__global__ void fd_fold_kernel(const float* src_rows, void* out, FdParams P, int self,
+                               const uint64_t* flags, int wait) {
+  const int row = blockIdx.x;  // b * Hq + hq
+  const int d = P.d, row_len = d + 2;
+  __shared__ int ok;
+  if (threadIdx.x == 0) ok = 1;
+  __syncthreads();
+  float am = -INFINITY, al = 0.0f, ao[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ao[i] = 0.0f;
+  const size_t stride = size_t(P.B) * P.Hq * row_len;
+  for (int s = 0; s < P.W; ++s) {
+    if (wait) {
+      if (threadIdx.x == 0 &&
+          !wait_geq(flags + s, P.flag_epoch, P.watchdog_ns, P.err, kWaitSignal, self, P.board, s, 0, 0))
+        ok = 0;
+      __syncthreads();
+      if (!ok) return;
+    }
+    fold_row<8>(am, al, ao, src_rows + size_t(s) * stride + size_t(row) * row_len, d,
+                threadIdx.x, 32);
+  }
+  if (al == 0.0f) {
+    if (threadIdx.x == 0)
+      raise_err(P.err, TF_ERR_EMPTY_ATTENTION, kEmpty, self, -1, 0, 0, 0, 0, uint64_t(row % P.Hq));
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int e = threadIdx.x + 32 * i;
+    if (e < d) store_out(out, size_t(row) * d + e, ao[i] / al, P.out_bf16);
+  }
+}
+
+}  // namespace
+
+static bool fast_ok(const tf_fd_shape& s) {
+  return s.kv_dtype == TF_BF16 && s.head_dim == 128 && s.q_heads / s.kv_heads == 8;
+}
+
+// Split count: enough (group, split) items to cover the SMs a few times,
+// never fewer than 64 positions per split.  Shape-only, so every schedule
+// and every rank cuts identically.
+static int choose_splits(const tf_fd_shape& s, size_t len, int sms) {
+  const long groups = long(s.batch) * s.kv_heads;
+  long want = (long(sms) * 4 + groups - 1) / groups;
+  long maxs = long((len + 63) / 64);
+  long S = std::max(1L, std::min(want, maxs));
+  return int(S);
+}
+
+static tf_status fd_validate(World* w, const tf_fd_shape* s, const void* const* q,
+                             const void* const* k, const void* const* v, void* const* out) {
+  if (!s || !q || !k || !v || !out) return set_error(TF_ERR_CONFIG, "tf_flash_decode: NULL argument");
+  if (s->q_heads < 1 || s->head_dim < 1 || s->kv_len < 1 || s->batch < 1 || s->kv_heads < 1)
+    return set_error(TF_ERR_CONFIG, "flash_decode: heads, head_dim, kv_len must be >= 1");
+  if (s->kv_len % size_t(w->W) != 0)
+    return set_error(TF_ERR_CONFIG, "flash_decode: kv_len = " + std::to_string(s->kv_len) +
+                                        " must be divisible by world_size = " +
+                                        std::to_string(w->W));
+  if (!std::isfinite(s->scale)) return set_error(TF_ERR_CONFIG, "flash_decode: scale must be finite");
+  if (s->q_heads % s->kv_heads != 0)
+    return set_error(TF_ERR_CONFIG, "flash_decode: q_heads must be a multiple of kv_heads");
+  if (s->head_dim > 256 || s->q_heads / s->kv_heads > 32)
+    return set_error(TF_ERR_SHAPE, "flash_decode: head_dim <= 256 and q_heads/kv_heads <= 32");
+  for (int r = 0; r < w->W; ++r)
+    if (w->ranks[r].local && (!q[r] || !k[r] || !v[r] || !out[r]))
+      return set_error(TF_ERR_CONFIG, "flash_decode: NULL tensor for rank " + std::to_string(r));
+  return TF_OK;
+}
+
+}  // namespace tfb
+
+using namespace tfb;
+
+extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
+                                           const tf_fd_shape* shape, const void* const* q,
+                                           const void* const* k_shard,
+                                           const void* const* v_shard, void* const* out,
+                                           void* const* inbox_opt, void* const* streams) {
+  if (!tw) return set_error(TF_ERR_CONFIG, "tf_flash_decode: NULL world");
+  World* w = &tw->impl;
+  TFB_CHECK(fd_validate(w, shape, q, k_shard, v_shard, out));
+  if (variant < TF_FD_BSP || variant > TF_FD_FUSED)
+    return set_error(TF_ERR_CONFIG, "run_fd: unknown variant");
+  const tf_fd_shape& sh = *shape;
+  auto st = resolve_streams(w, streams);
+  const int W = w->W, d = sh.head_dim, G = sh.batch * sh.kv_heads, gs = sh.q_heads / sh.kv_heads;
+  const size_t len = sh.kv_len / W;
+  const size_t row_floats = size_t(sh.batch) * sh.q_heads * (d + 2);
+  const bool fast = fast_ok(sh);
+  const int S = choose_splits(sh, len, w->sm_count);
+  const size_t split_len = (len + S - 1) / S;
+  const int S_eff = int((len + split_len - 1) / split_len);
+
+  // Boards: per (src, group) for fused, per src otherwise (fd.flags is
+  // W x 1 in the reference, flash_decode.hpp:357).
+  const bool fused = variant == TF_FD_FUSED;
+  BoardEntry fb;
+  TFB_CHECK(board_next_epoch(w, "fd.flags", W, fused ? G : 1, &fb));
+  w->fd_flags = FlagSnapshot{w->board_names[fb.id], size_t(W) * (fused ? G : 1), fb.epoch};
+  // Inbox / pubs / stage in the symmetric heap.  The internal inbox is
+  // double-buffered by epoch parity: a fast peer's next push can never land
+  // in the buffer a slow rank is still folding.
+  size_t inbox_off = 0, pub_off = 0, ws_off = 0, tick_off = 0, ctr_off = 0;
+  const std::string geo = "[" + std::to_string(row_floats) + "]";
+  TFB_CHECK(heap_get(w, "fd.inbox" + geo, sizeof(float) * W * row_floats * 2, &inbox_off));
+  TFB_CHECK(heap_get(w, "fd.partials" + geo, sizeof(float) * row_floats, &pub_off));
+  const int nlocal_max = std::min(w->n_local, kMaxLocal);
+  const size_t ws_floats = size_t(nlocal_max) * G * S_eff * gs * (d + 2);
+  TFB_CHECK(heap_get(w, "fd.ws[" + std::to_string(ws_floats) + "]", sizeof(float) * ws_floats, &ws_off));
+  TFB_CHECK(heap_get(w, "fd.tickets[" + std::to_string(G) + "x" + std::to_string(S_eff) + "]",
+                     sizeof(unsigned long long) * nlocal_max * G, &tick_off));
+  TFB_CHECK(heap_get(w, "fd.ctr", 64, &ctr_off));
+  // Tickets are epoch-valued per (group, split-count) geometry.
+  const uint64_t tepoch = ++w->epochs["fd.tickets@" + std::to_string(tick_off)];
+  const int parity = int(fb.epoch & 1);
+
+  auto inbox_of = [&](int r) -> float* {
+    if (inbox_opt && inbox_opt[r]) return static_cast<float*>(inbox_opt[r]);
+    return reinterpret_cast<float*>(w->ptr(r, inbox_off)) + size_t(parity) * W * row_floats;
+  };
+
+  FdParams P{};
+  P.W = W;
+  P.B = sh.batch;
+  P.Hq = sh.q_heads;
+  P.Hkv = sh.kv_heads;
+  P.gs = gs;
+  P.d = d;
+  P.len = len;
+  P.S = S_eff;
+  P.split_len = split_len;
+  P.scale = sh.scale;
+  P.kv_bf16 = sh.kv_dtype == TF_BF16;
+  P.out_bf16 = sh.out_dtype == TF_BF16;
+  P.watchdog_ns = w->watchdog_ns;
+  P.err = w->err_dev;
+  P.board = fb.id;
+  for (int r = 0; r < W; ++r) {
+    P.inbox_all[r] = inbox_of(r);
+    P.flags_all[r] = reinterpret_cast<uint64_t*>(w->ptr(r, fb.offset));
+  }
+
+  // Group local ranks by device: one attention launch per device.
+  std::map<int, std::vector<int>> by_dev;
+  for (int r = 0; r < W; ++r)
+    if (w->ranks[r].local) by_dev[w->ranks[r].device].push_back(r);
+
+  P.epoch = tepoch;
+  P.flag_epoch = fb.epoch;
+  // One attention launch per device (a loopback device runs all its ranks
+  // in one persistent grid, so the fused waits can never starve a producer).
+  auto launch_attention = [&](int push, int fold_inline) -> tf_status {
+    for (auto& kv : by_dev) {
+      const std::vector<int>& rs = kv.second;
+      for (size_t c0 = 0; c0 < rs.size(); c0 += kMaxLocal) {
+        FdParams Q = P;
+        Q.nlocal = int(std::min(rs.size() - c0, size_t(kMaxLocal)));
+        const int lead = rs[c0];
+        for (int i = 0; i < Q.nlocal; ++i) {
+          const int r = rs[c0 + i];
+          Q.r[i] = FdRank{q[r], k_shard[r], v_shard[r], out[r],
+                          reinterpret_cast<float*>(w->ptr(r, pub_off)), inbox_of(r),
+                          reinterpret_cast<uint64_t*>(w->ptr(r, fb.offset)), r};
+        }
+        Q.ws = reinterpret_cast<float*>(w->ptr(lead, ws_off));
+        Q.ticket = reinterpret_cast<unsigned long long*>(w->ptr(lead, tick_off));
+        Q.ctr = reinterpret_cast<unsigned int*>(w->ptr(lead, ctr_off));
+        Q.push = push;
+        Q.fold_inline = fold_inline;
+        cudaSetDevice(kv.first);
+        const unsigned items = unsigned(Q.nlocal) * G * S_eff;
+        int per_sm = 1;
+        if (fast)
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fd_attention_kernel<true>,
+                                                        kFastThreads, 0);
+        else
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fd_attention_kernel<false>,
+                                                        kFastThreads, 0);
+        const unsigned grid =
+            std::max(1u, std::min(items, unsigned(std::max(per_sm, 1) * w->sm_count)));
+        if (fast) fd_attention_kernel<true><<<grid, kFastThreads, 0, st[lead]>>>(Q);
+        else fd_attention_kernel<false><<<grid, kFastThreads, 0, st[lead]>>>(Q);
+        TFB_CUDA(cudaGetLastError());
+        ++w->launches;
+        // Ranks sharing the launch are complete when it is: order their streams.
+        for (int i = 1; i < Q.nlocal; ++i) {
+          const int r = rs[c0 + i];
+          if (st[r] == st[lead]) continue;
+          cudaEvent_t ev;
+          TFB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+          TFB_CUDA(cudaEventRecord(ev, st[lead]));
+          TFB_CUDA(cudaStreamWaitEvent(st[r], ev, 0));
+          cudaEventDestroy(ev);
+        }
+      }
+    }
+    return TF_OK;
+  };
+
+  if (fused) return launch_attention(/*push=*/1, /*fold_inline=*/1);
+  TFB_CHECK(launch_attention(0, 0));
+  TFB_CHECK(world_barrier(w, st));
+  const FdParams PP = P;
+  if (variant == TF_FD_BSP) {
+    size_t stage_off;
+    TFB_CHECK(heap_get(w, "fd.stage" + geo, sizeof(float) * W * row_floats, &stage_off));
+    FdParams G2 = PP;
+    for (int r = 0; r < W; ++r) G2.inbox_all[r] = reinterpret_cast<float*>(w->ptr(r, pub_off));
+    for (int r = 0; r < W; ++r) {
+      if (!w->ranks[r].local) continue;
+      cudaSetDevice(w->ranks[r].device);
+      float* stage = (inbox_opt && inbox_opt[r]) ? static_cast<float*>(inbox_opt[r])
+                                                 : reinterpret_cast<float*>(w->ptr(r, stage_off));
+      const unsigned blocks = unsigned(std::min<size_t>((W * row_floats + 255) / 256, 1024));
+      fd_gather_kernel<<<blocks, 256, 0, st[r]>>>(stage, row_floats, G2, W);
+      TFB_CUDA(cudaGetLastError());
+      ++w->launches;
+    }
+    TFB_CHECK(world_barrier(w, st));
+    for (int r = 0; r < W; ++r) {
+      if (!w->ranks[r].local) continue;
+      cudaSetDevice(w->ranks[r].device);
+      float* stage = (inbox_opt && inbox_opt[r]) ? static_cast<float*>(inbox_opt[r])
+                                                 : reinterpret_cast<float*>(w->ptr(r, stage_off));
+      fd_fold_kernel<<<sh.batch * sh.q_heads, 32, 0, st[r]>>>(stage, out[r], PP, r, nullptr, 0);
+      TFB_CUDA(cudaGetLastError());
+      ++w->launches;
+    }
+    return TF_OK;
+  }
+  // independent_ag / fine_waits: push kernel per rank.
+  const int wait_all = variant == TF_FD_INDEPENDENT_AG;
+  for (int r = 0; r < W; ++r) {
+    if (!w->ranks[r].local) continue;
+    cudaSetDevice(w->ranks[r].device);
+    FdParams Q = PP;
+    Q.r[0].flags = reinterpret_cast<uint64_t*>(w->ptr(r, fb.offset));
+    fd_push_kernel<<<W, 256, 0, st[r]>>>(reinterpret_cast<float*>(w->ptr(r, pub_off)), row_floats,
+                                         r, W, Q, wait_all);
+    TFB_CUDA(cudaGetLastError());
+    ++w->launches;
+  }
+  if (wait_all) TFB_CHECK(world_barrier(w, st));
+  for (int r = 0; r < W; ++r) {
+    if (!w->ranks[r].local) continue;
+    cudaSetDevice(w->ranks[r].device);
+    fd_fold_kernel<<<sh.batch * sh.q_heads, 32, 0, st[r]>>>(
+        inbox_of(r), out[r], PP, r, reinterpret_cast<uint64_t*>(w->ptr(r, fb.offset)),
+        wait_all ? 0 : 1);
+    TFB_CUDA(cudaGetLastError());
+    ++w->launches;
+  }
+  return TF_OK;
+}
+
+extern "C" tf_status tf_flash_decode(tf_world* tw, tf_fd_variant variant,
+                                     const tf_fd_shape* shape, const void* const* q,
+                                     const void* const* k_shard, const void* const* v_shard,
+                                     void* const* out, void* const* inbox_opt,
+                                     void* const* streams) {
+  TFB_CHECK(tf_flash_decode_async(tw, variant, shape, q, k_shard, v_shard, out, inbox_opt, streams));
+  return sync_and_check(&tw->impl, resolve_streams(&tw->impl, streams));
+}
+
+extern "C" tf_status tf_fd_flag_counts(tf_world* tw, int rank, uint64_t* out, size_t cap,
+                                       size_t* count) {
+  if (!tw) return set_error(TF_ERR_CONFIG, "NULL world");
+  World* w = &tw->impl;
+  const FlagSnapshot& f = w->fd_flags;
+  if (count) *count = f.cells ? size_t(w->W) : 0;
+  if (f.cells == 0 || !out) return TF_OK;
+  if (rank < 0 || rank >= w->W) return set_error(TF_ERR_BOUNDS, "fd_flag_counts: bad rank");
+  auto it = w->boards.find(f.board);
+  if (it == w->boards.end()) return TF_OK;
+  std::vector<uint64_t> v(f.cells);
+  TFB_CUDA(cudaMemcpy(v.data(), w->ptr(rank, it->second.offset), sizeof(uint64_t) * f.cells,
+                      cudaMemcpyDefault));
+  const size_t per = f.cells / size_t(w->W);
+  for (int s = 0; s < w->W && size_t(s) < cap; ++s) {
+    uint64_t mn = UINT64_MAX;
+    for (size_t g = 0; g < per; ++g) mn = std::min(mn, v[size_t(s) * per + g]);
+    out[s] = mn - (f.epoch - 1);
+  }
+  return TF_OK;
+}

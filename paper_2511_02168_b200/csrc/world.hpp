@@ -1,0 +1,118 @@
+// world.hpp -- host-side world: ranks, per-rank streams, the symmetric heap
+// registry, signal boards, epochs and the error record.  This is the B200
+// form of the reference's World/RankCtx (fabric.hpp:253-692): a "rank" is a
+// GPU (or, in a loopback world, a slice of one GPU's memory), a symmetric
+// tensor is one bump allocation at the same offset in every rank's heap, and
+// a signal board is a heap region of u64 counters.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "tilefabric_b200/tf_abi.h"
+
+namespace tfb {
+
+struct RankRes {
+  int device = 0;
+  char* heap = nullptr;       // base of this rank's heap, valid in this process
+  bool local = false;         // launched by this process
+  bool owns_heap = false;     // allocated (vs IPC-opened) here
+  cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // producer stream (push variants)
+};
+
+struct HeapEntry {
+  size_t offset = 0;
+  size_t bytes = 0;
+};
+
+struct BoardEntry {
+  int id = 0;
+  int rows = 0;
+  int slots = 0;
+  size_t offset = 0;  // heap offset of the rows x slots u64 grid
+  uint64_t epoch = 0; // completed-run count: a run waits for cells >= epoch
+};
+
+// Records the last push-style run's flag geometry for *_flag_counts.
+struct FlagSnapshot {
+  std::string board;
+  size_t cells = 0;     // per rank
+  uint64_t epoch = 0;   // value a completed run leaves in every cell
+};
+
+struct World {
+  int W = 0;
+  bool ipc = false;
+  int first_local = 0;
+  int n_local = 0;
+  double watchdog_secs = 10.0;
+  uint64_t watchdog_ns = 10000000000ull;
+  size_t heap_bytes = 0;
+  size_t heap_used = 0;
+  std::vector<RankRes> ranks;
+  std::map<std::string, HeapEntry> heap;
+  std::map<std::string, BoardEntry> boards;
+  std::vector<std::string> board_names;  // id -> name
+  DevErr* err_host = nullptr;
+  DevErr* err_dev = nullptr;
+  uint64_t launches = 0;
+  uint64_t barrier_epoch = 0;
+  uint64_t ag_epoch = 0;
+  uint64_t fd_epoch = 0;
+  FlagSnapshot ag_flags, fd_flags;
+  // Named monotonic epochs for counters that live in the heap (tickets,
+  // soak boards); cleared with the heap.
+  std::map<std::string, uint64_t> epochs;
+  int sm_count = 148;
+  // Loopback: several ranks share one device.
+  bool loopback = false;
+
+  char* ptr(int rank, size_t offset) const { return ranks[rank].heap + offset; }
+  bool is_local(int r) const { return r >= first_local && r < first_local + n_local; }
+};
+
+// ---- status plumbing -----------------------------------------------------
+tf_status set_error(tf_status s, const std::string& msg);
+tf_status cuda_status(cudaError_t e, const char* what);
+#define TFB_CUDA(call)                                              \
+  do {                                                              \
+    cudaError_t _e = (call);                                        \
+    if (_e != cudaSuccess) return ::tfb::cuda_status(_e, #call);    \
+  } while (0)
+#define TFB_CHECK(call)                      \
+  do {                                       \
+    tf_status _s = (call);                   \
+    if (_s != TF_OK) return _s;              \
+  } while (0)
+
+// Heap/board helpers used by the pattern implementations.
+tf_status heap_get(World* w, const std::string& name, size_t bytes, size_t* offset);
+tf_status board_get(World* w, const std::string& name, int rows, int slots, BoardEntry* out);
+// Geometry-keyed board for a pattern run; returns it with its epoch bumped
+// (monotonic counters: run e waits for >= e, fabric.hpp:515-517).
+tf_status board_next_epoch(World* w, const std::string& base, int rows, int slots,
+                           BoardEntry* out);
+// Device-side world barrier over every rank (fabric.hpp:574-584): one tiny
+// kernel per local rank, red.release.sys onto every rank's barrier cell,
+// then an acquire spin on its own.
+tf_status world_barrier(World* w, const std::vector<cudaStream_t>& streams);
+// Resolve caller streams (NULL -> world streams).
+std::vector<cudaStream_t> resolve_streams(World* w, void* const* streams);
+// Wait for local streams and turn the device error record into a status.
+tf_status sync_and_check(World* w, const std::vector<cudaStream_t>& streams);
+tf_status check_record(World* w);
+
+// Checks that [p, p+bytes) lies inside rank r's heap.
+bool in_heap(const World* w, int r, const void* p, size_t bytes);
+
+}  // namespace tfb
+
+struct tf_world {
+  tfb::World impl;
+};

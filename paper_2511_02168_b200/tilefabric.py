@@ -1,0 +1,394 @@
+"""Python mirror of the reference's operator API over the C ABI.
+
+Same names, argument meaning and error behaviour as
+proj/include/tilefabric/{ag_gemm,flash_decode,fabric,tilemath}.hpp, so the
+parity tests read like the reference's own GTest suites:
+
+    p = ag.make_problem(seed, m, n, k, TileSpec(...))
+    run = ag.run_pull(p, WorldConfig(world_size=2))   # run.c[rank] == C
+    run = fd.run_fd(p, fd.Variant.kFused, cfg)         # run.out[rank]
+
+Every call drives the sm_100a kernels of libtilefabric_b200.so (no CPU
+path).  A world of W ranks uses W GPUs when that many are visible and a
+loopback world (all ranks on GPU 0, each with its own symmetric heap) when
+not -- the GPU analogue of the reference's oversubscribed thread worlds.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+from ._abi import (BoundsError, ConfigError, CudaError, DeadlockError,  # noqa: F401
+                   EmptyAttentionError, Error, NumericError, ShapeError, WorldError)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+# ---- common.hpp ---------------------------------------------------------------
+
+def uniform_reals(seed: int, n: int) -> np.ndarray:
+    """common.hpp:132-140 (bit-exact: libstdc++ mt19937_64 + uniform_real_distribution)."""
+    out = np.empty(n, np.float32)
+    _abi.check(_abi.lib().tf_uniform_reals(seed, n, out.ctypes.data_as(C.POINTER(C.c_float))))
+    return out
+
+
+@dataclass
+class TileSpec:
+    """tilemath.hpp:78-88"""
+    bm: int = 16
+    bn: int = 16
+    bk: int = 16
+
+    def validate(self) -> None:
+        if self.bm < 1 or self.bn < 1 or self.bk < 1:
+            raise ConfigError("tile extents must be >= 1")
+
+
+@dataclass
+class WorldConfig:
+    """fabric.hpp:46-96 (the fields that mean something on a GPU)."""
+    world_size: int = 1
+    watchdog: float = 0.0            # seconds; 0 -> TILEFABRIC_WATCHDOG_SECS or 10 s
+    devices: Optional[Sequence[int]] = None  # None -> distinct GPUs if available, else loopback
+    heap_bytes: int = 0              # 0 -> sized from the problem
+
+    def validate(self) -> None:
+        if self.world_size < 1 or self.world_size > 64:
+            raise ConfigError(f"world_size must be in [1, 64], got {self.world_size}")
+
+    def device_list(self) -> List[int]:
+        if self.devices is not None:
+            return list(self.devices)
+        n = _torch().cuda.device_count()
+        loop = os.environ.get("TILEFABRIC_LOOPBACK", "0") == "1"
+        if n >= self.world_size and not loop:
+            return list(range(self.world_size))
+        return [0] * self.world_size
+
+
+class World:
+    """A tf_world: ranks, per-rank symmetric heaps, boards (fabric.hpp:253-378)."""
+
+    def __init__(self, world_size: int, devices: Sequence[int], heap_bytes: int,
+                 watchdog: float = 0.0) -> None:
+        self.lib = _abi.lib()
+        self.W = world_size
+        self.devices = list(devices)
+        h = C.c_void_p()
+        devs = (C.c_int * world_size)(*self.devices)
+        _abi.check(self.lib.tf_world_create(world_size, devs, heap_bytes, watchdog, C.byref(h)))
+        self.handle = h
+
+    @classmethod
+    def from_config(cls, cfg: WorldConfig, heap_bytes: int) -> "World":
+        cfg.validate()
+        return cls(cfg.world_size, cfg.device_list(), cfg.heap_bytes or heap_bytes, cfg.watchdog)
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.tf_world_destroy(self.handle)
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- heap / boards --
+    def alloc(self, name: str, nbytes: int) -> List[int]:
+        ptrs = (C.c_void_p * self.W)()
+        _abi.check(self.lib.tf_heap_alloc(self.handle, name.encode(), nbytes, ptrs))
+        return [p or 0 for p in ptrs]
+
+    def board(self, name: str, rows: int, slots: int) -> List[int]:
+        ptrs = (C.c_void_p * self.W)()
+        _abi.check(self.lib.tf_board_alloc(self.handle, name.encode(), rows, slots, ptrs))
+        return [p or 0 for p in ptrs]
+
+    def signal(self, board: str, src: int, dst: int, row: int, slot: int) -> None:
+        _abi.check(self.lib.tf_signal(self.handle, board.encode(), src, dst, row, slot))
+
+    def wait_signal(self, board: str, rank: int, row: int, slot: int, expected: int) -> None:
+        _abi.check(self.lib.tf_wait_signal(self.handle, board.encode(), rank, row, slot, expected))
+
+    def read_signal(self, board: str, rank: int, row: int, slot: int) -> int:
+        v = C.c_uint64()
+        _abi.check(self.lib.tf_read_signal(self.handle, board.encode(), rank, row, slot, C.byref(v)))
+        return v.value
+
+    def soak(self, seed: int, rounds: int) -> int:
+        v = C.c_uint64()
+        _abi.check(self.lib.tf_signal_soak(self.handle, seed, rounds, C.byref(v)))
+        return v.value
+
+    def memcpy(self, dst: int, src: int, nbytes: int) -> None:
+        _abi.check(self.lib.tf_memcpy(self.handle, dst, src, nbytes))
+
+    def sync(self) -> None:
+        _abi.check(self.lib.tf_world_sync(self.handle))
+
+    def launches(self) -> int:
+        return int(self.lib.tf_launch_count(self.handle))
+
+    def stream(self, rank: int) -> int:
+        return self.lib.tf_world_stream(self.handle, rank) or 0
+
+    # -- host <-> heap helpers (input placement, never timed) --
+    def put(self, dst: int, arr: np.ndarray) -> None:
+        arr = np.ascontiguousarray(arr)
+        self.memcpy(dst, arr.ctypes.data, arr.nbytes)
+
+    def get(self, src: int, shape, dtype) -> np.ndarray:
+        out = np.empty(shape, dtype)
+        self.memcpy(out.ctypes.data, src, out.nbytes)
+        return out
+
+
+# ---- ag_gemm.hpp ----------------------------------------------------------------
+
+class ag:  # namespace tilefabric::ag
+    @dataclass
+    class AgGemmProblem:
+        """ag_gemm.hpp:47-66"""
+        m: int = 0
+        n: int = 0
+        k: int = 0
+        tiles: TileSpec = field(default_factory=TileSpec)
+        a: np.ndarray = None  # m x k
+        b: np.ndarray = None  # k x n
+
+        def validate(self, world_size: int) -> None:
+            if self.m < 1 or self.n < 1 or self.k < 1:
+                raise ConfigError("ag_gemm: m, n, k must be >= 1")
+            if self.k % world_size != 0:
+                raise ConfigError(f"ag_gemm: k = {self.k} must be divisible by world_size = {world_size}")
+            self.tiles.validate()
+
+    @dataclass
+    class AgGemmRun:
+        """ag_gemm.hpp:85-92 (+ the gathered operand per rank and the launch count)."""
+        c: List[np.ndarray]
+        flag_counts: List[List[int]]
+        gathered: List[np.ndarray]
+        launches: int
+
+    @staticmethod
+    def make_problem(seed: int, m: int, n: int, k: int, tiles: Optional[TileSpec] = None):
+        """ag_gemm.hpp:71-83: one stream, A first then B."""
+        v = uniform_reals(seed, m * k + k * n)
+        return ag.AgGemmProblem(m, n, k, tiles or TileSpec(), v[: m * k].reshape(m, k).copy(),
+                                v[m * k:].reshape(k, n).copy())
+
+    @staticmethod
+    def _run(variant: int, p: "ag.AgGemmProblem", cfg: WorldConfig, dtype: int = _abi.TF_F32):
+        cfg.validate()
+        p.validate(cfg.world_size)
+        torch = _torch()
+        W = cfg.world_size
+        kw = p.k // W
+        esz = 4 if dtype == _abi.TF_F32 else 2
+        tdt = torch.float32 if dtype == _abi.TF_F32 else torch.bfloat16
+        heap = esz * p.m * kw + 2 * esz * p.m * p.k + (8 << 20)
+        with World.from_config(cfg, heap) as w:
+            shards = w.alloc("ag.a", esz * p.m * kw)
+            gathered = w.alloc("ag.gathered", esz * p.m * p.k)
+            A = torch.from_numpy(np.ascontiguousarray(p.a, np.float32))
+            bufs_b, bufs_c = [], []
+            for r in range(W):
+                dev = torch.device("cuda", w.devices[r])
+                shard = A[:, r * kw:(r + 1) * kw].contiguous().to(tdt)  # fill_shard :103-112
+                shard_d = shard.to(dev)
+                w.memcpy(shards[r], shard_d.data_ptr(), shard_d.numel() * esz)
+                bufs_b.append(torch.from_numpy(np.ascontiguousarray(p.b, np.float32)).to(tdt).to(dev))
+                bufs_c.append(torch.empty((p.m, p.n), dtype=tdt, device=dev))
+            torch.cuda.synchronize()
+            shape = _abi.AgShape(p.m, p.n, p.k, p.tiles.bm, p.tiles.bn, p.tiles.bk, dtype)
+            before = w.launches()
+            _abi.check(w.lib.tf_ag_gemm(
+                w.handle, variant, C.byref(shape), _abi.ptr_array(shards),
+                _abi.ptr_array([b.data_ptr() for b in bufs_b]),
+                _abi.ptr_array([c.data_ptr() for c in bufs_c]),
+                _abi.ptr_array(gathered) if variant != _abi.TF_AG_PULL else None, None))
+            launches = w.launches() - before
+            cs = [c.float().cpu().numpy() for c in bufs_c]
+            gath = []
+            if variant != _abi.TF_AG_PULL:
+                for r in range(W):
+                    g = torch.empty((p.m, p.k), dtype=tdt, device=torch.device("cuda", w.devices[r]))
+                    w.memcpy(g.data_ptr(), gathered[r], g.numel() * esz)
+                    gath.append(g.float().cpu().numpy())
+            flags = []
+            if variant == _abi.TF_AG_PUSH:
+                for r in range(W):
+                    cnt = C.c_size_t()
+                    _abi.check(w.lib.tf_ag_flag_counts(w.handle, r, None, 0, C.byref(cnt)))
+                    buf = (C.c_uint64 * max(1, cnt.value))()
+                    _abi.check(w.lib.tf_ag_flag_counts(w.handle, r, buf, cnt.value, C.byref(cnt)))
+                    flags.append([int(x) for x in buf[: cnt.value]])
+            return ag.AgGemmRun(cs, flags, gath, launches)
+
+    @staticmethod
+    def run_baseline(p, cfg, dtype=_abi.TF_F32):
+        """ag_gemm.hpp:134-180"""
+        return ag._run(_abi.TF_AG_BASELINE, p, cfg, dtype)
+
+    @staticmethod
+    def run_pull(p, cfg, dtype=_abi.TF_F32):
+        """ag_gemm.hpp:185-222"""
+        return ag._run(_abi.TF_AG_PULL, p, cfg, dtype)
+
+    @staticmethod
+    def run_push(p, cfg, dtype=_abi.TF_F32):
+        """ag_gemm.hpp:228-305"""
+        return ag._run(_abi.TF_AG_PUSH, p, cfg, dtype)
+
+
+# ---- flash_decode.hpp -------------------------------------------------------------
+
+class fd:  # namespace tilefabric::fd
+    class Variant(enum.IntEnum):
+        """flash_decode.hpp:50"""
+        kBsp = _abi.TF_FD_BSP
+        kIndependentAg = _abi.TF_FD_INDEPENDENT_AG
+        kFineWaits = _abi.TF_FD_FINE_WAITS
+        kFused = _abi.TF_FD_FUSED
+
+    @staticmethod
+    def to_string(v) -> str:
+        return {0: "bsp", 1: "independent_ag", 2: "fine_waits", 3: "fused"}.get(int(v), "unknown")
+
+    @dataclass
+    class DecodeProblem:
+        """flash_decode.hpp:66-88, extended with batch and kv_heads (GQA).
+        q: [batch][heads][d]; k, v: [batch][kv_heads][kv_len][d]."""
+        heads: int = 0
+        head_dim: int = 0
+        kv_len: int = 0
+        scale: float = 0.0
+        q: np.ndarray = None
+        k: np.ndarray = None
+        v: np.ndarray = None
+        batch: int = 1
+        kv_heads: int = 0  # 0 -> heads (MHA, the reference)
+
+        def kvh(self) -> int:
+            return self.kv_heads or self.heads
+
+        def validate(self, world_size: int) -> None:
+            if self.heads < 1 or self.head_dim < 1 or self.kv_len < 1:
+                raise ConfigError("flash_decode: heads, head_dim, kv_len must be >= 1")
+            if self.kv_len % world_size != 0:
+                raise ConfigError(f"flash_decode: kv_len = {self.kv_len} must be divisible by "
+                                  f"world_size = {world_size}")
+            if not math.isfinite(self.scale):
+                raise ConfigError("flash_decode: scale must be finite")
+
+    @dataclass
+    class FdOptions:
+        """flash_decode.hpp:108-114"""
+        fold_by_arrival: bool = False
+
+    @dataclass
+    class FdRun:
+        """flash_decode.hpp:116-123 (+ each rank's inbox and the launch count)."""
+        out: List[np.ndarray]
+        flag_counts: List[List[int]]
+        inbox: List[np.ndarray]
+        launches: int
+
+    @staticmethod
+    def make_problem(seed: int, heads: int, head_dim: int, kv_len: int):
+        """flash_decode.hpp:90-106: scale 1/sqrt(d); q, then K, then V."""
+        hd = heads * head_dim
+        v = uniform_reals(seed, hd + 2 * hd * kv_len)
+        q = v[:hd].reshape(1, heads, head_dim).copy()
+        k = v[hd: hd + hd * kv_len].reshape(1, heads, kv_len, head_dim).copy()
+        vv = v[hd + hd * kv_len:].reshape(1, heads, kv_len, head_dim).copy()
+        return fd.DecodeProblem(heads, head_dim, kv_len,
+                                float(np.float32(1.0) / np.sqrt(np.float32(head_dim))), q, k, vv)
+
+    @staticmethod
+    def run_fd(p: "fd.DecodeProblem", variant, cfg: WorldConfig, opts: Optional["fd.FdOptions"] = None,
+               dtype: int = _abi.TF_F32, out_dtype: Optional[int] = None):
+        """flash_decode.hpp:425-438"""
+        if opts is not None and opts.fold_by_arrival:
+            raise ConfigError("fold_by_arrival is not supported: the B200 fold is always "
+                              "ascending-source (bitwise reproducible)")
+        cfg.validate()
+        p.validate(cfg.world_size)
+        torch = _torch()
+        W = cfg.world_size
+        B, H, Hkv, d, L = p.batch, p.heads, p.kvh(), p.head_dim, p.kv_len
+        ln = L // W
+        tdt = torch.float32 if dtype == _abi.TF_F32 else torch.bfloat16
+        odt = dtype if out_dtype is None else out_dtype
+        tod = torch.float32 if odt == _abi.TF_F32 else torch.bfloat16
+        row = B * H * (d + 2)
+        esz = 4 if dtype == _abi.TF_F32 else 2
+        heap = 4 * W * row * 6 + 4 * B * Hkv * 4096 * (d + 2) * 8 + (16 << 20)
+        with World.from_config(cfg, heap) as w:
+            inbox = w.alloc("fd.inbox.user", 4 * W * row)
+            q = torch.from_numpy(np.ascontiguousarray(p.q, np.float32)).reshape(B, H, d).to(tdt)
+            k = torch.from_numpy(np.ascontiguousarray(p.k, np.float32)).reshape(B, Hkv, L, d).to(tdt)
+            v = torch.from_numpy(np.ascontiguousarray(p.v, np.float32)).reshape(B, Hkv, L, d).to(tdt)
+            qs, ks, vs, outs = [], [], [], []
+            for r in range(W):
+                dev = torch.device("cuda", w.devices[r])
+                qs.append(q.to(dev))
+                ks.append(k[:, :, r * ln:(r + 1) * ln].contiguous().to(dev))  # slice_shard :140-160
+                vs.append(v[:, :, r * ln:(r + 1) * ln].contiguous().to(dev))
+                outs.append(torch.empty((B, H, d), dtype=tod, device=dev))
+            torch.cuda.synchronize()
+            shape = _abi.FdShape(B, H, Hkv, d, L, p.scale, dtype, odt)
+            before = w.launches()
+            _abi.check(w.lib.tf_flash_decode(
+                w.handle, int(variant), C.byref(shape),
+                _abi.ptr_array([t.data_ptr() for t in qs]), _abi.ptr_array([t.data_ptr() for t in ks]),
+                _abi.ptr_array([t.data_ptr() for t in vs]), _abi.ptr_array([t.data_ptr() for t in outs]),
+                _abi.ptr_array(inbox), None))
+            launches = w.launches() - before
+            out = [o.float().cpu().numpy().reshape(B * H, d) if B > 1 else
+                   o.float().cpu().numpy().reshape(H, d) for o in outs]
+            boxes = [w.get(inbox[r], (W, B, H, d + 2), np.float32) for r in range(W)]
+            flags = []
+            if int(variant) != _abi.TF_FD_BSP:
+                for r in range(W):
+                    buf = (C.c_uint64 * W)()
+                    cnt = C.c_size_t()
+                    _abi.check(w.lib.tf_fd_flag_counts(w.handle, r, buf, W, C.byref(cnt)))
+                    flags.append([int(x) for x in buf[: cnt.value]])
+            return fd.FdRun(out, flags, boxes, launches)
+
+    @staticmethod
+    def run_bsp(p, cfg, **kw):
+        return fd.run_fd(p, fd.Variant.kBsp, cfg, **kw)
+
+    @staticmethod
+    def run_independent_ag(p, cfg, **kw):
+        return fd.run_fd(p, fd.Variant.kIndependentAg, cfg, **kw)
+
+    @staticmethod
+    def run_fine_waits(p, cfg, **kw):
+        return fd.run_fd(p, fd.Variant.kFineWaits, cfg, **kw)
+
+    @staticmethod
+    def run_fused(p, cfg, opts=None, **kw):
+        return fd.run_fd(p, fd.Variant.kFused, cfg, opts, **kw)
