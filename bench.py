@@ -1,0 +1,471 @@
+#!/usr/bin/env python
+"""bench.py -- AG+GEMM & Flash Decode latency on B200 (BASELINE.json metric).
+
+Headline (one JSON line on rank 0): the fused All-Gather+GEMM step of
+BASELINE.json configs[1] -- bf16, M=8192 gathered rows, K=8192 (A sharded
+along K), N=28672/W per GPU -- timed with CUDA events over K back-to-back
+steps after W warm-ups, max over ranks.  Every input is larger than L2
+(A 128 MiB, B 448 MiB at W=1), so no flush is needed between steps.
+
+Beside it, in the same line: the roofline of the dominant kernel, the
+NCCL+cuBLAS BSP baseline, the reference's CPU path (oracle/_ref, timed on
+this host), an end-to-end number through the C ABI with host buffers, and
+the Flash Decode configs (configs[2], configs[3]) as secondary results.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M_, K_, N_TOTAL = 8192, 8192, 28672
+FD3 = dict(batch=1, q_heads=64, kv_heads=8, head_dim=128, kv_len=131072)
+FD4 = dict(batch=32, q_heads=64, kv_heads=8, head_dim=128, kv_len=32768)
+METRIC = "AG+GEMM & Flash Decode latency (µs) at 1/2/4/8 B200 vs BSP; % of roofline"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return dict(hbm=p["hbm_gbs"], bf16=p["bf16_tflops"], bf16_sus=p["bf16_tflops_sustained"],
+                    src="measured")
+    except Exception:
+        return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+
+
+def ncu_traffic(key):
+    """dram bytes per launch of the dominant kernel from the committed
+    ncu --set full summary (profiles/ncu_summary.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f).get(key, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock/throttle sampling (NVML) during the timed region."""
+
+    def __init__(self, dev=0):
+        self.samples, self.reasons, self.stop = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(dev)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception:
+            self.N = None
+
+    def _run(self):
+        N = self.N
+        names = {getattr(N, k): k for k in dir(N) if k.startswith("nvmlClocksEventReason") or
+                 k.startswith("nvmlClocksThrottleReason")}
+        while not self.stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                mask = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit in (0x2, 0x4, 0x8, 0x20, 0x40, 0x80, 0x100):
+                    if mask & bit:
+                        self.reasons.add({0x2: "applications_clocks", 0x4: "sw_power_cap",
+                                          0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+                                          0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake",
+                                          0x100: "display_clocks"}.get(bit, names.get(bit, hex(bit))))
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.N:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        if self.N:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------------
+# distributed plumbing (torchrun) -- one process per GPU, IPC symmetric heap
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Ctx:
+    def __init__(self, n_gpus):
+        import torch
+        self.torch = torch
+        self.ws, self.rank, self.local = dist_env()
+        if self.ws != n_gpus and self.ws > 1:
+            raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={self.ws}")
+        self.W = max(self.ws, 1)
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        self.pg = None
+        if self.ws > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("nccl", device_id=self.dev)
+            self.dist = dist
+
+    def barrier(self):
+        if self.ws > 1:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if self.ws == 1:
+            return x
+        t = self.torch.tensor([x], device=self.dev, dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def world(self, heap_bytes):
+        import paper_2511_02168_b200 as tf
+        from paper_2511_02168_b200 import _abi
+        L = _abi.lib()
+        h = C.c_void_p()
+        if self.ws == 1:
+            devs = (C.c_int * 1)(self.local)
+            _abi.check(L.tf_world_create(1, devs, heap_bytes, 0.0, C.byref(h)))
+        else:
+            _abi.check(L.tf_world_create_ipc(self.rank, self.ws, self.local, heap_bytes, 0.0, C.byref(h)))
+            mine = (C.c_char * _abi.IPC_HANDLE_BYTES)()
+            _abi.check(L.tf_world_ipc_export(h, mine))
+            allh = [None] * self.ws
+            self.dist.all_gather_object(allh, bytes(mine))
+            buf = (C.c_char * (_abi.IPC_HANDLE_BYTES * self.ws)).from_buffer_copy(b"".join(allh))
+            _abi.check(L.tf_world_ipc_import(h, buf))
+        w = tf.World.__new__(tf.World)
+        w.lib, w.W, w.devices, w.handle = L, self.W, [self.local] * self.W, h
+        return w
+
+
+def ptrs_for(ctx, local_ptr):
+    """Per-rank pointer array with only this process' rank filled."""
+    arr = [0] * ctx.W
+    arr[ctx.rank] = local_ptr
+    return arr
+
+
+def time_steps(ctx, stream, fn, steps, warmup):
+    torch = ctx.torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ctx.barrier()
+    torch.cuda.synchronize()
+    s = torch.cuda.ExternalStream(stream) if isinstance(stream, int) else stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        fn()
+    e1.record(s)
+    torch.cuda.synchronize()
+    ctx.barrier()
+    torch.cuda.synchronize()
+    return ctx.max(e0.elapsed_time(e1) / steps)  # ms per step, max over ranks
+
+
+# ---------------------------------------------------------------------------------
+# AG+GEMM (headline)
+
+def bench_ag(ctx, steps, warmup, variant_name="pull"):
+    from paper_2511_02168_b200 import _abi
+    torch = ctx.torch
+    W = ctx.W
+    M, K, N = M_, K_, N_TOTAL // W
+    kw = K // W
+    variant = {"pull": _abi.TF_AG_PULL, "push": _abi.TF_AG_PUSH, "baseline": _abi.TF_AG_BASELINE}[variant_name]
+    w = ctx.world(M * kw * 2 + 2 * 2 * M * K * 2 + (64 << 20))
+    try:
+        g = torch.Generator(device=ctx.dev).manual_seed(1 + ctx.rank)
+        shard_ptrs = w.alloc("ag.a", M * kw * 2)
+        A_local = (torch.rand(M, kw, device=ctx.dev, generator=g) * 2 - 1).bfloat16()
+        w.memcpy(shard_ptrs[ctx.rank], A_local.data_ptr(), M * kw * 2)
+        B = (torch.rand(K, N, device=ctx.dev, generator=g) * 2 - 1).bfloat16()
+        Cm = torch.empty(M, N, device=ctx.dev, dtype=torch.bfloat16)
+        torch.cuda.synchronize()
+        ctx.barrier()
+        shape = _abi.AgShape(M, N, K, 0, 0, 0, _abi.TF_BF16)
+        st = w.stream(ctx.rank)
+        args = (w.handle, variant, C.byref(shape), _abi.ptr_array(shard_ptrs),
+                _abi.ptr_array(ptrs_for(ctx, B.data_ptr())), _abi.ptr_array(ptrs_for(ctx, Cm.data_ptr())),
+                None, None)
+        step = lambda: _abi.check(w.lib.tf_ag_gemm_async(*args))  # noqa: E731
+        l0 = w.launches()
+        with ClockSampler(ctx.local) as clk:
+            ms = time_steps(ctx, st, step, steps, warmup)
+        launches = (w.launches() - l0) // (steps + warmup) * steps
+        _abi.check(w.lib.tf_world_sync(w.handle))
+        # Correctness on the benchmarked buffers: rank 0 checks sampled rows
+        # of C against an fp32 product (W=1: the full operand is local).
+        err = None
+        if W == 1:
+            rows = torch.arange(0, M, M // 64, device=ctx.dev)
+            ref = A_local[rows].float() @ B.float()
+            err = float(((Cm[rows].float() - ref).abs().max() / ref.abs().max()).item())
+        # BSP baseline: NCCL all-gather (W > 1) + relayout + cuBLAS.
+        bsp_ms = bench_bsp_ag(ctx, A_local, B, steps, warmup)
+        # End to end through the C ABI with host buffers: H2D of the shard and
+        # B from pinned memory, the fused step, D2H of C -- every step.
+        e2e = bench_ag_e2e(ctx, w, A_local, B, Cm, shard_ptrs, shape, variant, max(3, steps // 5))
+        return dict(ms=ms, launches=launches, clocks=clk.summary(), err=err, bsp_ms=bsp_ms,
+                    e2e=e2e, M=M, N=N, K=K)
+    finally:
+        w.close()
+
+
+def bench_bsp_ag(ctx, A_local, B, steps, warmup):
+    torch = ctx.torch
+    W = ctx.W
+    M, kw = A_local.shape
+    gathered = torch.empty(W, M, kw, device=ctx.dev, dtype=torch.bfloat16)
+    out = torch.empty(M, B.shape[1], device=ctx.dev, dtype=torch.bfloat16)
+
+    def step():
+        if W > 1:
+            ctx.dist.all_gather_into_tensor(gathered, A_local)
+            A = gathered.permute(1, 0, 2).reshape(M, W * kw)  # relayout [W][M][kw] -> M x K
+        else:
+            A = A_local
+        torch.matmul(A, B, out=out)
+
+    return time_steps(ctx, torch.cuda.current_stream(), step, steps, warmup)
+
+
+def bench_ag_e2e(ctx, w, A_local, B, Cm, shard_ptrs, shape, variant, steps):
+    from paper_2511_02168_b200 import _abi
+    torch = ctx.torch
+    hA = A_local.cpu().pin_memory()
+    hB = B.cpu().pin_memory()
+    hC = torch.empty(Cm.shape, dtype=Cm.dtype).pin_memory()
+    st = torch.cuda.ExternalStream(w.stream(ctx.rank))
+    dA = torch.empty_like(A_local)  # staging for the shard (heap copy below)
+    cudart = torch.cuda.cudart()
+
+    def step():
+        with torch.cuda.stream(st):
+            dA.copy_(hA, non_blocking=True)
+            B.copy_(hB, non_blocking=True)
+        # shard placement into the symmetric heap (device to device, same stream)
+        cudart.cudaMemcpyAsync(shard_ptrs[ctx.rank], dA.data_ptr(), dA.numel() * 2, 3, st.cuda_stream)
+        _abi.check(w.lib.tf_ag_gemm_async(w.handle, variant, C.byref(shape), _abi.ptr_array(shard_ptrs),
+                                          _abi.ptr_array(ptrs_for(ctx, B.data_ptr())),
+                                          _abi.ptr_array(ptrs_for(ctx, Cm.data_ptr())), None, None))
+        with torch.cuda.stream(st):
+            hC.copy_(Cm, non_blocking=True)
+
+    ms = time_steps(ctx, st, step, steps, 1)
+    h2d = hA.numel() * 2 + hB.numel() * 2
+    d2h = hC.numel() * 2
+    return dict(ms=ms, h2d=h2d, d2h=d2h)
+
+
+# ---------------------------------------------------------------------------------
+# Flash Decode (secondary)
+
+def bench_fd(ctx, cfg, steps, warmup):
+    from paper_2511_02168_b200 import _abi
+    torch = ctx.torch
+    W = ctx.W
+    B, Hq, Hkv, d, L = cfg["batch"], cfg["q_heads"], cfg["kv_heads"], cfg["head_dim"], cfg["kv_len"]
+    ln = L // W
+    row = B * Hq * (d + 2)
+    w = ctx.world(4 * W * row * 4 + 4 * B * Hkv * 1024 * (d + 2) * 8 * 4 + (64 << 20))
+    try:
+        g = torch.Generator(device=ctx.dev).manual_seed(7 + ctx.rank)
+        q = (torch.rand(B, Hq, d, device=ctx.dev, generator=g) * 2 - 1).bfloat16()
+        k = (torch.rand(B, Hkv, ln, d, device=ctx.dev, generator=g) * 2 - 1).bfloat16()
+        v = (torch.rand(B, Hkv, ln, d, device=ctx.dev, generator=g) * 2 - 1).bfloat16()
+        out = torch.empty(B, Hq, d, device=ctx.dev, dtype=torch.bfloat16)
+        torch.cuda.synchronize()
+        ctx.barrier()
+        shape = _abi.FdShape(B, Hq, Hkv, d, L, float(d ** -0.5), _abi.TF_BF16, _abi.TF_BF16)
+        res = {}
+        for name, var in (("fused", _abi.TF_FD_FUSED), ("bsp", _abi.TF_FD_BSP)):
+            args = (w.handle, var, C.byref(shape), _abi.ptr_array(ptrs_for(ctx, q.data_ptr())),
+                    _abi.ptr_array(ptrs_for(ctx, k.data_ptr())), _abi.ptr_array(ptrs_for(ctx, v.data_ptr())),
+                    _abi.ptr_array(ptrs_for(ctx, out.data_ptr())), None, None)
+            step = lambda: _abi.check(w.lib.tf_flash_decode_async(*args))  # noqa: E731
+            res[name] = time_steps(ctx, w.stream(ctx.rank), step, steps, warmup)
+        _abi.check(w.lib.tf_world_sync(w.handle))
+        # numerics spot check (W=1): torch fp32 attention on the same bf16 data
+        err = None
+        if W == 1:
+            gs = Hq // Hkv
+            bb = 0
+            qf = q[bb].float().view(Hkv, gs, d)
+            s = torch.einsum("hgd,hld->hgl", qf, k[bb].float()) * (d ** -0.5)
+            ref = torch.einsum("hgl,hld->hgd", torch.softmax(s, -1), v[bb].float()).reshape(Hq, d)
+            err = float(((out[bb].float() - ref).abs().amax(-1) / ref.abs().amax(-1)).max().item())
+        kv_bytes = 2 * B * Hkv * ln * d * 2
+        return dict(fused_ms=res["fused"], bsp_ms=res["bsp"], kv_bytes=kv_bytes, err=err)
+    finally:
+        w.close()
+
+
+# ---------------------------------------------------------------------------------
+# the reference's CPU path (oracle/_ref: proj/include/tilefabric compiled as-is)
+
+def cpu_reference_ag(W, sample_rows=32, n_slice=1792):
+    """ag::run_pull (ag_gemm.hpp:185-222) on bounded M x N slices of config 2,
+    one independent call per host core, extrapolated linearly in M*N (the
+    loops are exactly linear there, ag_gemm.hpp:200-217)."""
+    import numpy as np
+    from oracle.oracle import Reference
+    if not Reference.available():
+        return None
+    R = Reference()
+    cores = os.cpu_count() or 1
+    K, N = K_, N_TOTAL // W
+    n_slice = min(n_slice, N)
+    rng = np.random.default_rng(0)
+    A = rng.uniform(-1, 1, (sample_rows, K)).astype(np.float32)
+    Bs = rng.uniform(-1, 1, (K, n_slice)).astype(np.float32)
+    times = [None] * cores
+
+    def work(i):
+        t0 = time.perf_counter()
+        R.ag_run_inputs(1, A, Bs, W)
+        times[i] = time.perf_counter() - t0
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(cores)]
+    t0 = time.perf_counter()
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    wall = time.perf_counter() - t0
+    sample_mn = cores * sample_rows * n_slice
+    full_mn = M_ * N
+    est_s = wall * full_mn / sample_mn
+    return dict(value=est_s * 1e6, unit="us", cores=cores, kind="reference",
+                sample=f"{cores} concurrent ag::run_pull(W={W}) calls on {sample_rows}x{n_slice} slices "
+                       f"of the M x N output at K={K} (wall {wall:.2f}s), extrapolated x{full_mn / sample_mn:.0f} "
+                       f"linearly in M*N", cpu_seconds=float(sum(times)))
+
+
+def run_reference_arm(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    W = max(ws, args.gpus)
+    vals = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference_ag(W, sample_rows=8)
+        if r is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtfref.so not built"}))
+            return
+        if i >= args.warmup:
+            vals.append(r["value"])
+            info = r
+    v = statistics.median(vals)
+    line = {"metric": METRIC, "value": v, "unit": "us", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": v / 1e3, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": ag_config(W), "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "us", "cores": info["cores"], "kind": "reference",
+                             "sample": info["sample"]},
+            "e2e": {"value": v, "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def ag_config(W):
+    return {"workload": "AG+GEMM BASELINE configs[1]: bf16, M=8192 gathered rows, K=8192 sharded along K, "
+                        "N=28672/W per GPU (Llama-3-70B TP shape)",
+            "M": M_, "K": K_, "N_per_gpu": N_TOTAL // W, "world_size": W, "variant": "pull",
+            "l2": "no flush needed: every input exceeds L2 (A 128 MiB, B 448 MiB / W)",
+            "parallelism": f"tp{W} (A all-gathered along K)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-fd", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    args.warmup = max(args.warmup, 3)
+    ctx = Ctx(args.gpus)
+    pk = peaks()
+    ag_res = bench_ag(ctx, args.steps, args.warmup)
+    fd3 = fd4 = None
+    if not args.no_fd:
+        fd3 = bench_fd(ctx, FD3, args.steps, args.warmup)
+        fd4 = bench_fd(ctx, FD4, max(5, args.steps // 2), args.warmup)
+    if ctx.rank != 0:
+        return
+    W = ctx.W
+    M, N, K = ag_res["M"], ag_res["N"], ag_res["K"]
+    flops = 2.0 * M * N * K
+    us = ag_res["ms"] * 1e3
+    tflops = flops / (ag_res["ms"] * 1e-3) / 1e12
+    cpu = None if args.no_cpu else cpu_reference_ag(W)
+    line = {
+        "metric": METRIC, "value": us, "unit": "us", "n_gpus": W, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ag_res["ms"], "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": ag_config(W),
+        "roofline": {"bound": "tensor", "achieved": tflops, "peak": pk["bf16"], "unit": "TFLOP/s",
+                     "frac": tflops / pk["bf16"], "peak_source": pk["src"] + " burst (MEASURED_PEAKS.json)",
+                     "frac_vs_sustained": tflops / pk["bf16_sus"],
+                     "algorithmic_flop_per_launch": flops,
+                     "traffic": ncu_traffic("ag_gemm_sm100_kernel")},
+        "bsp": {"what": "cuBLAS matmul" + (" after NCCL all_gather_into_tensor + relayout" if W > 1 else
+                                           " (W=1: nothing to gather)"),
+                "value": ag_res["bsp_ms"] * 1e3, "unit": "us",
+                "fused_speedup": ag_res["bsp_ms"] / ag_res["ms"]},
+        "e2e": {"value": ag_res["e2e"]["ms"] * 1e3, "unit": "us",
+                "h2d_bytes_per_step": ag_res["e2e"]["h2d"], "d2h_bytes_per_step": ag_res["e2e"]["d2h"],
+                "what": "tf_ag_gemm via the C ABI from pinned host A-shard and B, C read back, every step"},
+        "gpu_launches": ag_res["launches"],
+        "clocks": ag_res["clocks"],
+        "numerics": {"ag_sampled_rows_norm_err": ag_res["err"], "tol": 4e-3},
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    if fd3:
+        sec = {}
+        for name, cfg, r in (("fd_config3_b1_L128k", FD3, fd3), ("fd_config4_b32_L32k", FD4, fd4)):
+            gbs = r["kv_bytes"] / (r["fused_ms"] * 1e-3) / 1e9
+            sec[name] = {"fused_us": r["fused_ms"] * 1e3, "bsp_us": r["bsp_ms"] * 1e3,
+                         "fused_speedup_vs_bsp": r["bsp_ms"] / r["fused_ms"],
+                         "roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm"], "unit": "GB/s",
+                                      "frac": gbs / pk["hbm"], "algorithmic_bytes_per_launch": r["kv_bytes"]},
+                         "head_rel_err_vs_torch_fp32": r["err"], "config": cfg}
+        line["secondary"] = sec
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()
