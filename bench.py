@@ -265,14 +265,14 @@ def bench_ag_e2e(ctx, w, A_local, B, Cm, shard_ptrs, shape, variant, steps):
     hC = torch.empty(Cm.shape, dtype=Cm.dtype).pin_memory()
     st = torch.cuda.ExternalStream(w.stream(ctx.rank))
     dA = torch.empty_like(A_local)  # staging for the shard (heap copy below)
-    cudart = torch.cuda.cudart()
 
     def step():
         with torch.cuda.stream(st):
             dA.copy_(hA, non_blocking=True)
             B.copy_(hB, non_blocking=True)
         # shard placement into the symmetric heap (device to device, same stream)
-        cudart.cudaMemcpyAsync(shard_ptrs[ctx.rank], dA.data_ptr(), dA.numel() * 2, 3, st.cuda_stream)
+        _abi.check(w.lib.tf_memcpy_async(w.handle, shard_ptrs[ctx.rank], dA.data_ptr(), dA.numel() * 2,
+                                         st.cuda_stream))
         _abi.check(w.lib.tf_ag_gemm_async(w.handle, variant, C.byref(shape), _abi.ptr_array(shard_ptrs),
                                           _abi.ptr_array(ptrs_for(ctx, B.data_ptr())),
                                           _abi.ptr_array(ptrs_for(ctx, Cm.data_ptr())), None, None))

@@ -202,6 +202,8 @@ tf_status tf_fd_flag_counts(tf_world* w, int rank, uint64_t* out, size_t cap,
  * does in fill_shard / slice_shard (ag_gemm.hpp:103-112,
  * flash_decode.hpp:140-160); and caller-owned device buffers. */
 tf_status tf_memcpy(tf_world* w, void* dst, const void* src, size_t bytes);
+/* Stream-ordered variant (stream: cudaStream_t, NULL = legacy default). */
+tf_status tf_memcpy_async(tf_world* w, void* dst, const void* src, size_t bytes, void* stream);
 tf_status tf_device_alloc(tf_world* w, int rank, size_t bytes, void** out);
 tf_status tf_device_free(tf_world* w, int rank, void* p);
 

@@ -104,6 +104,7 @@ SIGNATURES = {
     "tf_fd_flag_counts": (C.c_int, [_P, C.c_int, C.POINTER(C.c_uint64), C.c_size_t,
                                     C.POINTER(C.c_size_t)]),
     "tf_memcpy": (C.c_int, [_P, _P, _P, C.c_size_t]),
+    "tf_memcpy_async": (C.c_int, [_P, _P, _P, C.c_size_t, _P]),
     "tf_device_alloc": (C.c_int, [_P, C.c_int, C.c_size_t, _PP]),
     "tf_device_free": (C.c_int, [_P, C.c_int, _P]),
     "tf_uniform_reals": (C.c_int, [C.c_uint64, C.c_size_t, C.POINTER(C.c_float)]),

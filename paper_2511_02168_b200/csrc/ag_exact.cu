@@ -64,7 +64,9 @@ __global__ void __launch_bounds__(256) exact_gemm_kernel(
         __syncthreads();
         for (int e = threadIdx.x; e < TM * TK; e += 256) {
           const int r = e / TK, c = e % TK;
-          As[r][c] = (i0 + r < m && c < tk) ? A[(i0 + r) * stride + p0 + c] : 0.0f;
+          // ld.cg: inbox bytes land from other SMs/GPUs during the launch and a
+          // line shared with a not-yet-signalled block may sit stale in L1.
+          As[r][c] = (i0 + r < m && c < tk) ? __ldcg(A + (i0 + r) * stride + p0 + c) : 0.0f;
         }
         for (int e = threadIdx.x; e < TK * TN; e += 256) {
           const int r = e / TN, c = e % TN;
@@ -144,7 +146,7 @@ tf_status ag_exact_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh,
       cudaSetDevice(w->ranks[r].device);
       exact_gemm_kernel<<<grid, 256, 0, streams[r]>>>(
           shards, W, kw, kw, static_cast<const float*>(b[r]), static_cast<float*>(c[r]), m, n,
-          bk, nullptr, 0, 0, w->watchdog_ns, w->err_dev, r, -1);
+          bk, nullptr, 0, 0, w->watchdog_ns, w->err_of(r), r, -1);
       TFB_CUDA(cudaGetLastError());
       ++w->launches;
     }
@@ -188,7 +190,7 @@ tf_status ag_exact_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh,
       st.p[0] = stage[r];
       exact_gemm_kernel<<<grid, 256, 0, streams[r]>>>(
           st, 1, k, k, static_cast<const float*>(b[r]), static_cast<float*>(c[r]), m, n, bk,
-          nullptr, 0, 0, w->watchdog_ns, w->err_dev, r, -1);
+          nullptr, 0, 0, w->watchdog_ns, w->err_of(r), r, -1);
       TFB_CUDA(cudaGetLastError());
       ++w->launches;
     }
@@ -229,7 +231,7 @@ tf_status ag_exact_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh,
     exact_gemm_kernel<<<grid, 256, 0, streams[r]>>>(
         st, W, kw, k, static_cast<const float*>(b[r]), static_cast<float*>(c[r]), m, n, bk,
         reinterpret_cast<const uint64_t*>(w->ptr(r, fb.offset)), n_kb, epoch, w->watchdog_ns,
-        w->err_dev, r, fb.id);
+        w->err_of(r), r, fb.id);
     TFB_CUDA(cudaGetLastError());
     ++w->launches;
     // The producer must finish before the caller reuses the shard.

@@ -32,6 +32,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "ag_internal.hpp"
@@ -42,20 +43,26 @@ namespace {
 
 using namespace sm100;
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2;           // 16 KB
-constexpr int B_BYTES = BK * BN * 2;           // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 48 KB
-constexpr int GROUP_M = 16;
+constexpr int BM = 128, BN = 256, BK = 64;  // BM: rows per CTA; a CTA pair covers 256
+constexpr int GROUP_M = 16;                  // pair-tiles per raster group (L2 reuse of B)
 constexpr int NUM_THREADS = 256;
 constexpr int TMEM_COLS = 512;
-constexpr uint32_t IDESC = idesc_bf16(BM, BN, /*a MN-major*/ 0, /*b MN-major*/ 1);
-constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+
+template <int CG>
+struct Cfg {
+  static constexpr int STAGES = CG == 2 ? 6 : 4;
+  static constexpr int BN_CTA = BN / CG;                // B columns staged per CTA
+  static constexpr int B_BYTES = BK * BN_CTA * 2;       // 16 KB (pair) / 32 KB
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t IDESC = idesc_bf16(BM * CG, BN, /*A K-major*/ 0, /*B MN-major*/ 1);
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024 + 256;
+};
 
 struct AgTcParams {
   int M, N, K, kw, W;
   int own;          // rank whose shard map serves its own k-range; -1: all from inbox
-  int num_m, num_n, num_tiles, kb_total, kbw;
+  int num_m, num_n, num_tiles, kb_total, kbw;  // num_m counts 128-row blocks
   __nv_bfloat16* C;
   const uint64_t* ready;  // [num_m][W] local board; nullptr: ungated
   uint64_t epoch;
@@ -66,16 +73,19 @@ struct AgTcParams {
   uint64_t watchdog_ns;
   DevErr* err;
   int board;
+  int dbg;  // TFB_DEBUG knobs: 1 skip C stores, 2 skip MMAs (profiling aids)
   const __nv_bfloat16* peer_shard[64];
 };
 
-__device__ __forceinline__ void tile_coords(const AgTcParams& p, int t, int& mb, int& nb) {
-  const int per_group = GROUP_M * p.num_n;
+// Pair-tile raster: GROUP_M pair-rows at a time, column-major inside the
+// group, so concurrently running clusters share B panels in L2.
+__device__ __forceinline__ void tile_coords(int num_mt, int num_n, int t, int& mt, int& nb) {
+  const int per_group = GROUP_M * num_n;
   const int group = t / per_group;
   const int first_m = group * GROUP_M;
-  const int gsize = min(p.num_m - first_m, GROUP_M);
+  const int gsize = min(num_mt - first_m, GROUP_M);
   const int r = t % per_group;
-  mb = first_m + r % gsize;
+  mt = first_m + r % gsize;
   nb = r / gsize;
 }
 
@@ -83,70 +93,193 @@ __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `p` (a local smem object) in CTA `rank`.
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// Barriers a pair's peer can complete are polled (see mbar_wait_cluster).
+template <int CG>
+__device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity) {
+  if (CG == 2) mbar_wait_cluster(bar, parity);
+  else mbar_wait(bar, parity);
+}
+
+template <int CG>
+__device__ __forceinline__ void tma_load_a(void* dst, const CUtensorMap* map, uint32_t bar_cluster,
+                                           int c0, int c1) {
+  if (CG == 2)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(bar_cluster)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+        "{%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(bar_cluster)
+        : "memory");
+}
+
+template <int CG>
+__device__ __forceinline__ void mma_issue(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  if (CG == 2)
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  else
+    mma_bf16_ss(d_tmem, a_desc, b_desc, idesc, accumulate);
+}
+
+// tcgen05.commit: arrive on `bar` in every CTA of the pair once the issued
+// MMAs retired.
+template <int CG>
+__device__ __forceinline__ void mma_commit_all(uint64_t* bar) {
+  if (CG == 2)
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+        "[%0], %1;" ::"r"(smem_u32(bar)),
+        "h"(uint16_t(3))
+        : "memory");
+  else
+    mma_commit(bar);
+}
+
+template <int CG>
+__device__ __forceinline__ void tmem_alloc_cg(uint32_t* slot) {
+  if (CG == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  } else {
+    tmem_alloc(slot, TMEM_COLS);
+  }
+}
+
+template <int CG>
+__device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr) {
+  if (CG == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(TMEM_COLS)
+                 : "memory");
+  else
+    tmem_dealloc(taddr, TMEM_COLS);
+}
+
+// CG = 2: a CTA pair (cluster of 2) computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 -- each CTA stages its own 128 rows of A and 128
+// of the 256 B columns, the leader issues M=256 N=256 MMAs that read both
+// CTAs' smem, and each CTA's TMEM holds its 128 x 256 accumulator.  Halves
+// the smem->tensor and L2->smem bytes per FLOP versus CG = 1.
+template <int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     ag_gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA_own,
                          const __grid_constant__ CUtensorMap tmA_inbox,
                          const __grid_constant__ CUtensorMap tmB, const AgTcParams p) {
+  using K_ = Cfg<CG>;
+  constexpr int STAGES = K_::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
   uint8_t* smB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * K_::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* pfull = tempty + 2;  // leader: peer's stage landed (local_full mode)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pfull + STAGES);
+  const bool local_full = (p.dbg & 4) != 0;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;
+  const bool leader = crank == 0;
+  const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
+  const int num_mt = (p.num_m + CG - 1) / CG;  // pair-tile rows
+  const int num_tiles = num_mt * p.num_n;
+
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA_own);
     tma_prefetch(&tmA_inbox);
     tma_prefetch(&tmB);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], local_full ? 1 : CG);  // one arrive per CTA (leader's copy is used)
       mbar_init(&empty[s], 1);
+      mbar_init(&pfull[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 4 * CG);
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 1) tmem_alloc_cg<CG>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ===== TMA producer =====
+    // ===== TMA producer (both CTAs) =====
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        int mb, nb;
-        tile_coords(p, t, mb, nb);
-        const int m0 = mb * BM, n0 = nb * BN;
+      for (int t = cid; t < num_tiles; t += ncl) {
+        int mt, nb;
+        tile_coords(num_mt, p.num_n, t, mt, nb);
+        const int mb = mt * CG + int(crank);  // this CTA's 128-row block
+        const int m0 = mb * BM, n0 = nb * BN + int(crank) * K_::BN_CTA;
         uint64_t ready_mask = 0;
         for (int i = 0; i < p.kb_total; ++i) {
           const int kb = p.own >= 0 ? (i + p.own * p.kbw) % p.kb_total : i;
           const int src = kb / p.kbw;
-          mbar_wait(&empty[stage], phase ^ 1);
+          bwait<CG>(&empty[stage], phase ^ 1);
           const bool from_own = src == p.own;
-          if (!from_own && p.ready && !((ready_mask >> src) & 1ull)) {
+          if (!from_own && p.ready && mb < p.num_m && !((ready_mask >> src) & 1ull)) {
             wait_geq(p.ready + size_t(mb) * p.W + src, p.epoch, p.watchdog_ns, p.err, kWaitSignal,
                      p.own, p.board, src, mb, 0);
             fence_proxy_async_global();
             ready_mask |= 1ull << src;
           }
-          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
           uint8_t* a_dst = smA + stage * A_BYTES;
-          if (from_own) tma_load_2d(a_dst, &tmA_own, &full[stage], kb * BK - p.own * p.kw, m0);
-          else tma_load_2d(a_dst, &tmA_inbox, &full[stage], kb * BK, m0);
-          uint8_t* b_dst = smB + stage * B_BYTES;
+          uint8_t* b_dst = smB + stage * K_::B_BYTES;
+          if (CG == 2 && local_full) {
+            // Each CTA's TMA completes on its own barrier; the peer's MMA-side
+            // thread forwards completion to the leader (pfull).
+            mbar_arrive_expect_tx(&full[stage], K_::STAGE_BYTES);
+            const uint32_t bar = smem_u32(&full[stage]);
+            if (from_own) tma_load_a<1>(a_dst, &tmA_own, bar, kb * BK - p.own * p.kw, m0);
+            else tma_load_a<1>(a_dst, &tmA_inbox, bar, kb * BK, m0);
 #pragma unroll
-          for (int c = 0; c < BN / 64; ++c)
-            tma_load_2d(b_dst + c * (BK * 128), &tmB, &full[stage], n0 + 64 * c, kb * BK);
+            for (int c = 0; c < K_::BN_CTA / 64; ++c)
+              tma_load_a<1>(b_dst + c * (BK * 128), &tmB, bar, n0 + 64 * c, kb * BK);
+          } else {
+            const uint32_t bar = CG == 2 ? mapa(&full[stage], 0) : smem_u32(&full[stage]);
+            if (leader) mbar_arrive_expect_tx(&full[stage], CG * K_::STAGE_BYTES);
+            else mbar_arrive_cluster(bar);
+            if (from_own) tma_load_a<CG>(a_dst, &tmA_own, bar, kb * BK - p.own * p.kw, m0);
+            else tma_load_a<CG>(a_dst, &tmA_inbox, bar, kb * BK, m0);
+#pragma unroll
+            for (int c = 0; c < K_::BN_CTA / 64; ++c)
+              tma_load_a<CG>(b_dst + c * (BK * 128), &tmB, bar, n0 + 64 * c, kb * BK);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -155,21 +288,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer =====
-    if (lane == 0) {
+    // ===== MMA issuer (leader CTA, one thread) =====
+    if (lane == 0 && leader) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t aphase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        mbar_wait(&tempty[acc], aphase ^ 1);
+      for (int t = cid; t < num_tiles; t += ncl) {
+        bwait<CG>(&tempty[acc], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
         for (int i = 0; i < p.kb_total; ++i) {
-          mbar_wait(&full[stage], phase);
+          bwait<CG>(&full[stage], phase);
+          if (CG == 2 && local_full) bwait<CG>(&pfull[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smA + stage * A_BYTES);
-          const uint32_t b_addr = smem_u32(smB + stage * B_BYTES);
+          const uint32_t b_addr = smem_u32(smB + stage * K_::B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // A: K-major SW128, 8-row groups 1024 B apart; +32 B per K=16.
@@ -177,30 +311,46 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // B: MN-major SW128, 64-col chunks 8 KB apart (LBO), 8-row K
             // groups 1024 B apart (SBO); +16 rows (2 KB) per K=16.
             const uint64_t bd = smem_desc_sw128(b_addr + k * 2048, BK * 128, 1024);
-            mma_bf16_ss(d_tmem, ad, bd, IDESC, (i | k) != 0);
+            if (!(p.dbg & 2)) mma_issue<CG>(d_tmem, ad, bd, K_::IDESC, (i | k) != 0);
           }
-          mma_commit(&empty[stage]);
+          mma_commit_all<CG>(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(&tfull[acc]);
+        mma_commit_all<CG>(&tfull[acc]);
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
       }
+    } else if (lane == 0 && CG == 2 && local_full) {
+      // Peer CTA: forward "my half of this stage landed" to the leader.
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t pfull0 = mapa(&pfull[0], 0);
+      for (int t = cid; t < num_tiles; t += ncl) {
+        for (int i = 0; i < p.kb_total; ++i) {
+          mbar_wait(&full[stage], phase);
+          mbar_arrive_cluster(pfull0 + uint32_t(stage) * 8);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
     }
   } else if (warp < 6) {
-    // ===== epilogue: TMEM -> registers -> bf16 -> global =====
+    // ===== epilogue (both CTAs): TMEM -> registers -> bf16 -> global =====
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int acc = 0;
     uint32_t aphase = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      int mb, nb;
-      tile_coords(p, t, mb, nb);
-      mbar_wait(&tfull[acc], aphase);
+    const uint32_t tempty_leader0 = CG == 2 ? mapa(&tempty[0], 0) : smem_u32(&tempty[0]);
+    for (int t = cid; t < num_tiles; t += ncl) {
+      int mt, nb;
+      tile_coords(num_mt, p.num_n, t, mt, nb);
+      bwait<CG>(&tfull[acc], aphase);
       tc_fence_after();
-      const int row = mb * BM + 32 * q + lane;
+      const int row = (mt * CG + int(crank)) * BM + 32 * q + lane;
       __nv_bfloat16* crow = p.C + size_t(row) * p.N;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
@@ -208,7 +358,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tmem_ld_32x32b_x32(tmem_base + (uint32_t(32 * q) << 16) + uint32_t(acc * BN + 32 * c), r);
         tmem_ld_wait();
         const int col0 = nb * BN + 32 * c;
-        if (row < p.M) {
+        if (row < p.M && !(p.dbg & 1)) {
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
             if (col0 + 8 * v < p.N) {
@@ -224,7 +374,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(tempty_leader0 + uint32_t(acc) * 8);
+        else mbar_arrive(&tempty[acc]);
+      }
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }
@@ -272,10 +425,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync();
+  else __syncthreads();
   if (warp == 1) {
     __syncwarp();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    tmem_dealloc_cg<CG>(tmem_base);
   }
   if (threadIdx.x == 0 && p.ctr) {
     __threadfence();
@@ -396,7 +550,7 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
                              cudaStream_t st, int board, unsigned grid_cap) {
   const int W = w->W;
   const size_t kw = sh.k / W;
-  CUtensorMap mOwn, mInbox, mB;
+  CUtensorMap mOwn{}, mInbox{}, mB{};
   if (shard) TFB_CHECK(make_map(&mOwn, shard, kw, sh.m, kw, BK, BM));
   if (inbox) TFB_CHECK(make_map(&mInbox, inbox, sh.k, sh.m, sh.k, BK, BM));
   if (!shard) mOwn = mInbox;
@@ -419,19 +573,37 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   p.epoch = epoch;
   p.gather = gather;
   p.watchdog_ns = w->watchdog_ns;
-  p.err = w->err_dev;
+  p.err = w->err_of(r);
   p.board = board;
-  static bool attr_set[64] = {};
+  if (const char* e = std::getenv("TFB_DEBUG")) p.dbg = std::atoi(e);
+  static bool attr_set[2][64] = {};
   const int dev = w->ranks[r].device;
   cudaSetDevice(dev);
-  if (!attr_set[dev & 63]) {
-    TFB_CUDA(cudaFuncSetAttribute(ag_gemm_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(SMEM_BYTES)));
-    attr_set[dev & 63] = true;
+  // CTA pairs (cta_group::2, 256 x 256 tiles) whenever there are two 128-row
+  // blocks to pair; single CTAs for skinny M.
+  const int CG = (p.num_m >= 2 && !(p.dbg & 8)) ? 2 : 1;
+  auto kern = CG == 2 ? ag_gemm_sm100_kernel<2> : ag_gemm_sm100_kernel<1>;
+  const size_t smem = CG == 2 ? Cfg<2>::SMEM : Cfg<1>::SMEM;
+  if (!attr_set[CG - 1][dev & 63]) {
+    TFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr_set[CG - 1][dev & 63] = true;
   }
-  const unsigned grid = std::max(1u, std::min(unsigned(p.num_tiles), grid_cap));
-  ag_gemm_sm100_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(mOwn, mInbox, mB, p);
-  TFB_CUDA(cudaGetLastError());
+  const unsigned pair_tiles = unsigned((p.num_m + CG - 1) / CG) * unsigned(p.num_n);
+  unsigned grid = std::min(pair_tiles * CG, grid_cap / CG * CG);
+  grid = std::max(grid, unsigned(CG));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (p.dbg & 16) ? 2 : CG;  // 16: 1-CTA kernel in 2-clusters (diagnosis)
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TFB_CUDA(cudaLaunchKernelEx(&cfg, kern, mOwn, mInbox, mB, p));
   ++w->launches;
   return TF_OK;
 }

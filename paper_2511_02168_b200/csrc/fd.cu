@@ -44,6 +44,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "world.hpp"
@@ -131,14 +132,17 @@ __device__ __forceinline__ float combine_elem(int mode, float ao, float bo, floa
 template <int MAXE>
 __device__ __forceinline__ void fold_row(float& am, float& al, float* ao, const float* row,
                                          int d, int tid, int nthreads) {
-  const float bm = row[0], bl = row[1];
+  // Rows were written by other CTAs (or peers) during this launch: read them
+  // through L2 (ld.cg).  L1 is not coherent, and a line shared with a
+  // neighbouring row may already sit in this SM's L1 from an earlier fold.
+  const float bm = __ldcg(row), bl = __ldcg(row + 1);
   float m, l, ax = 0.f, ay = 0.f;
   int mode;
   combine_scalars(am, al, bm, bl, &m, &l, &ax, &ay, &mode);
 #pragma unroll
   for (int i = 0; i < MAXE; ++i) {
     const int e = tid + i * nthreads;
-    if (e < d) ao[i] = combine_elem(mode, ao[i], row[2 + e], ax, ay);
+    if (e < d) ao[i] = combine_elem(mode, ao[i], __ldcg(row + 2 + e), ax, ay);
   }
   am = m;
   al = l;
@@ -245,6 +249,7 @@ __device__ __forceinline__ uint32_t w4(const uint4& v, int i) {
 }
 
 constexpr int kFastWarps = 4;
+constexpr int kFoldW = 2048;  // split weights cached in smem for the group fold
 constexpr int kFastThreads = kFastWarps * 32;
 
 // d index held by O^T accumulator row r of PV tile (i, j) (see header).
@@ -427,6 +432,7 @@ __global__ void __launch_bounds__(kFastThreads) fd_attention_kernel(const FdPara
   __shared__ unsigned int s_item;
   __shared__ int s_last;
   __shared__ FastSmem fsm;
+  __shared__ float s_M[32], s_L[32], s_w[kFoldW];
   const int G = P.B * P.Hkv;
   const unsigned total = unsigned(P.nlocal) * G * P.S;
   const int d = P.d, row_len = d + 2;
@@ -443,7 +449,7 @@ __global__ void __launch_bounds__(kFastThreads) fd_attention_kernel(const FdPara
     float* wsrow = grp + size_t(sp) * P.gs * row_len;
     if (FAST) fast_split(P, lr, g, sp, wsrow, fsm);
     else generic_split(P, lr, g, sp, wsrow);
-    if (err_raised(P.err)) break;
+    __threadfence();  // every writer publishes its ws bytes before the ticket
     // Ticket: the last split of the group folds all S splits.
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -456,34 +462,57 @@ __global__ void __launch_bounds__(kFastThreads) fd_attention_kernel(const FdPara
     if (!s_last) continue;
     const FdRank& R = P.r[lr];
     const int b = g / P.Hkv, kvh = g % P.Hkv;
-    // Rank partial rows for (b, kvh*gs + h): fold splits ascending.
-    for (int h = threadIdx.x >> 5; h < P.gs; h += blockDim.x >> 5) {
-      const int lane = threadIdx.x & 31;
-      float am = -INFINITY, al = 0.0f, ao[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) ao[i] = 0.0f;
+    // Rank partial rows for (b, kvh*gs + h): fold the S split partials.
+    // Max-first and fully parallel (every split row is loaded independently,
+    // ld.cg through L2): M = max m_s, w_s = exp(m_s - M), l = sum l_s w_s,
+    // o = sum o_s w_s -- the same monoid as combine_partials
+    // (tilemath.hpp:186-220) evaluated in one pass instead of S dependent
+    // steps (the serial chain was the tail of every launch).  Identical code
+    // in every schedule, so schedules stay bitwise equal.
+    for (int h = threadIdx.x; h < P.gs; h += blockDim.x) {
+      float M = -INFINITY;
       for (int s = 0; s < P.S; ++s) {
-        const volatile float* src = grp + (size_t(s) * P.gs + h) * row_len;
-        fold_row<8>(am, al, ao, const_cast<const float*>(src), d, lane, 32);
+        const float* row = grp + (size_t(s) * P.gs + h) * row_len;
+        if (__ldcg(row + 1) != 0.0f) M = fmaxf(M, __ldcg(row));
+      }
+      float L = 0.0f;
+      for (int s = 0; s < P.S; ++s) {
+        const float* row = grp + (size_t(s) * P.gs + h) * row_len;
+        const float l = __ldcg(row + 1);
+        const float w = l != 0.0f ? expf(__ldcg(row) - M) : 0.0f;
+        if (size_t(s) * P.gs + h < kFoldW) s_w[s * P.gs + h] = w;
+        L = __fadd_rn(L, __fmul_rn(l, w));
+      }
+      s_M[h] = M;
+      s_L[h] = L;
+    }
+    __syncthreads();
+    const size_t base_src = size_t(R.rank) * P.B * P.Hq * row_len;
+    for (int idx = threadIdx.x; idx < P.gs * (d + 2); idx += blockDim.x) {
+      const int h = idx / (d + 2), e = idx % (d + 2);
+      float val;
+      if (e == 0) {
+        val = s_M[h];
+      } else if (e == 1) {
+        val = s_L[h];
+      } else {
+        const float M = s_M[h];
+        float o = 0.0f;
+        for (int s = 0; s < P.S; ++s) {
+          const float* row = grp + (size_t(s) * P.gs + h) * row_len;
+          const float w = (size_t(s) * P.gs + h < kFoldW)
+                              ? s_w[s * P.gs + h]
+                              : (__ldcg(row + 1) != 0.0f ? expf(__ldcg(row) - M) : 0.0f);
+          if (w != 0.0f) o = __fadd_rn(o, __fmul_rn(__ldcg(row + e), w));
+        }
+        val = o;
       }
       const int hq = kvh * P.gs + h;
-      const size_t roff = (size_t(b) * P.Hq + hq) * row_len;
-      auto emit = [&](float* dst) {
-        if (lane == 0) {
-          dst[0] = am;
-          dst[1] = al;
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int e = lane + 32 * i;
-          if (e < d) dst[2 + e] = ao[i];
-        }
-      };
+      const size_t roff = (size_t(b) * P.Hq + hq) * row_len + e;
       if (P.push) {
-        for (int dst = 0; dst < P.W; ++dst)
-          emit(P.inbox_all[dst] + size_t(R.rank) * P.B * P.Hq * row_len + roff);
+        for (int dst = 0; dst < P.W; ++dst) P.inbox_all[dst][base_src + roff] = val;
       } else {
-        emit(R.pub + roff);
+        R.pub[roff] = val;
       }
     }
     if (P.push) {
@@ -494,7 +523,7 @@ __global__ void __launch_bounds__(kFastThreads) fd_attention_kernel(const FdPara
       }
     }
   }
-  if (P.fold_inline && !err_raised(P.err)) {
+  if (P.fold_inline) {
     // Fold phase: every compute item has been claimed by a CTA that never
     // blocks before pushing, so these waits always complete.
     const unsigned nfold = unsigned(P.nlocal) * G;
@@ -627,6 +656,7 @@ __global__ void fd_fold_kernel(const float* src_rows, void* out, FdParams P, int
 }  // namespace
 
 static bool fast_ok(const tf_fd_shape& s) {
+  if (std::getenv("TFB_FD_GENERIC")) return false;  // debugging aid
   return s.kv_dtype == TF_BF16 && s.head_dim == 128 && s.q_heads / s.kv_heads == 8;
 }
 
@@ -638,6 +668,7 @@ static int choose_splits(const tf_fd_shape& s, size_t len, int sms) {
   long want = (long(sms) * 4 + groups - 1) / groups;
   long maxs = long((len + 63) / 64);
   long S = std::max(1L, std::min(want, maxs));
+  if (const char* e = std::getenv("TFB_FD_SPLITS")) S = std::max(1L, std::min(std::atol(e), maxs));
   return int(S);
 }
 
@@ -727,7 +758,7 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   P.kv_bf16 = sh.kv_dtype == TF_BF16;
   P.out_bf16 = sh.out_dtype == TF_BF16;
   P.watchdog_ns = w->watchdog_ns;
-  P.err = w->err_dev;
+  P.err = nullptr;  // set per launch (per device)
   P.board = fb.id;
   for (int r = 0; r < W; ++r) {
     P.inbox_all[r] = inbox_of(r);
@@ -756,6 +787,7 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
                           reinterpret_cast<float*>(w->ptr(r, pub_off)), inbox_of(r),
                           reinterpret_cast<uint64_t*>(w->ptr(r, fb.offset)), r};
         }
+        Q.err = w->err_of(lead);
         Q.ws = reinterpret_cast<float*>(w->ptr(lead, ws_off));
         Q.ticket = reinterpret_cast<unsigned long long*>(w->ptr(lead, tick_off));
         Q.ctr = reinterpret_cast<unsigned int*>(w->ptr(lead, ctr_off));
@@ -794,7 +826,12 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   if (fused) return launch_attention(/*push=*/1, /*fold_inline=*/1);
   TFB_CHECK(launch_attention(0, 0));
   TFB_CHECK(world_barrier(w, st));
-  const FdParams PP = P;
+  FdParams PP = P;
+  auto with_err = [&](int r) {
+    FdParams x = PP;
+    x.err = w->err_of(r);
+    return x;
+  };
   if (variant == TF_FD_BSP) {
     size_t stage_off;
     TFB_CHECK(heap_get(w, "fd.stage" + geo, sizeof(float) * W * row_floats, &stage_off));
@@ -816,7 +853,7 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
       cudaSetDevice(w->ranks[r].device);
       float* stage = (inbox_opt && inbox_opt[r]) ? static_cast<float*>(inbox_opt[r])
                                                  : reinterpret_cast<float*>(w->ptr(r, stage_off));
-      fd_fold_kernel<<<sh.batch * sh.q_heads, 32, 0, st[r]>>>(stage, out[r], PP, r, nullptr, 0);
+      fd_fold_kernel<<<sh.batch * sh.q_heads, 32, 0, st[r]>>>(stage, out[r], with_err(r), r, nullptr, 0);
       TFB_CUDA(cudaGetLastError());
       ++w->launches;
     }
@@ -827,7 +864,7 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   for (int r = 0; r < W; ++r) {
     if (!w->ranks[r].local) continue;
     cudaSetDevice(w->ranks[r].device);
-    FdParams Q = PP;
+    FdParams Q = with_err(r);
     Q.r[0].flags = reinterpret_cast<uint64_t*>(w->ptr(r, fb.offset));
     fd_push_kernel<<<W, 256, 0, st[r]>>>(reinterpret_cast<float*>(w->ptr(r, pub_off)), row_floats,
                                          r, W, Q, wait_all);
@@ -839,7 +876,7 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
     if (!w->ranks[r].local) continue;
     cudaSetDevice(w->ranks[r].device);
     fd_fold_kernel<<<sh.batch * sh.q_heads, 32, 0, st[r]>>>(
-        inbox_of(r), out[r], PP, r, reinterpret_cast<uint64_t*>(w->ptr(r, fb.offset)),
+        inbox_of(r), out[r], with_err(r), r, reinterpret_cast<uint64_t*>(w->ptr(r, fb.offset)),
         wait_all ? 0 : 1);
     TFB_CUDA(cudaGetLastError());
     ++w->launches;

@@ -72,6 +72,9 @@ tf_status heap_get(World* w, const std::string& name, size_t bytes, size_t* offs
     if (!w->ranks[r].local) continue;
     TFB_CUDA(cudaSetDevice(w->ranks[r].device));
     TFB_CUDA(cudaMemset(w->ranks[r].heap + off, 0, bytes));
+    // The world's streams are non-blocking: they do not order against the
+    // legacy-stream memset, so finish it before any kernel can read the zeros.
+    TFB_CUDA(cudaDeviceSynchronize());
   }
   w->heap_used = off + bytes;
   w->heap[name] = HeapEntry{off, bytes};
@@ -119,9 +122,19 @@ std::vector<cudaStream_t> resolve_streams(World* w, void* const* streams) {
 }
 
 tf_status check_record(World* w) {
-  DevErr* e = w->err_host;
-  const int code = *reinterpret_cast<volatile int*>(&e->code);
-  if (code == 0) return TF_OK;
+  DevErr rec{};
+  DevErr* dev_rec = nullptr;
+  for (auto& kv : w->errs) {
+    cudaSetDevice(kv.first);
+    TFB_CUDA(cudaMemcpy(&rec, kv.second, sizeof(DevErr), cudaMemcpyDeviceToHost));
+    if (rec.code != 0) {
+      dev_rec = kv.second;
+      break;
+    }
+  }
+  if (!dev_rec) return TF_OK;
+  DevErr* e = &rec;
+  const int code = rec.code;
   std::string msg;
   const std::string rank = "rank " + std::to_string(e->rank) + ": ";
   const std::string board = (e->board >= 0 && e->board < (int)w->board_names.size())
@@ -152,8 +165,11 @@ tf_status check_record(World* w) {
     default:
       msg = rank + "device error";
   }
-  std::memset(e, 0, sizeof(DevErr));
-  return set_error(static_cast<tf_status>(code), msg);
+  for (auto& kv : w->errs) {
+    cudaSetDevice(kv.first);
+    cudaMemset(kv.second, 0, sizeof(DevErr));
+  }
+  return set_error(static_cast<tf_status>(code == -1 ? TF_ERR_WORLD : code), msg);
 }
 
 tf_status sync_and_check(World* w, const std::vector<cudaStream_t>& streams) {
@@ -264,7 +280,7 @@ tf_status world_barrier(World* w, const std::vector<cudaStream_t>& streams) {
     uint64_t** table = reinterpret_cast<uint64_t**>(w->ptr(r, off));
     TFB_CUDA(cudaMemcpyAsync(table, cells.data(), sizeof(uint64_t*) * w->W,
                              cudaMemcpyHostToDevice, streams[r]));
-    barrier_kernel<<<1, 32, 0, streams[r]>>>(table, r, w->W, epoch, w->watchdog_ns, w->err_dev,
+    barrier_kernel<<<1, 32, 0, streams[r]>>>(table, r, w->W, epoch, w->watchdog_ns, w->err_of(r),
                                              b.id);
     TFB_CUDA(cudaGetLastError());
     ++w->launches;
@@ -273,10 +289,20 @@ tf_status world_barrier(World* w, const std::vector<cudaStream_t>& streams) {
 }
 
 static tf_status world_init_common(World* w) {
-  TFB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&w->err_host), sizeof(DevErr),
-                         cudaHostAllocMapped | cudaHostAllocPortable));
-  std::memset(w->err_host, 0, sizeof(DevErr));
-  TFB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&w->err_dev), w->err_host, 0));
+  for (const RankRes& rr : w->ranks) {
+    if (!rr.local || w->errs.count(rr.device)) continue;
+    DevErr* e = nullptr;
+    TFB_CUDA(cudaSetDevice(rr.device));
+    TFB_CUDA(cudaMalloc(reinterpret_cast<void**>(&e), sizeof(DevErr)));
+    TFB_CUDA(cudaMemset(e, 0, sizeof(DevErr)));
+    w->errs[rr.device] = e;
+  }
+  // Heap/record memsets ran on the legacy stream; the world's non-blocking
+  // streams must not overtake them.
+  for (auto& kv : w->errs) {
+    TFB_CUDA(cudaSetDevice(kv.first));
+    TFB_CUDA(cudaDeviceSynchronize());
+  }
   return TF_OK;
 }
 
@@ -464,7 +490,10 @@ tf_status tf_world_destroy(tf_world* tw) {
       cudaIpcCloseMemHandle(rr.heap);
     }
   }
-  if (w->err_host) cudaFreeHost(w->err_host);
+  for (auto& kv : w->errs) {
+    cudaSetDevice(kv.first);
+    cudaFree(kv.second);
+  }
   delete tw;
   return TF_OK;
 }
@@ -499,6 +528,7 @@ tf_status tf_world_reset_heap(tf_world* tw) {
     if (!w->ranks[r].local) continue;
     TFB_CUDA(cudaSetDevice(w->ranks[r].device));
     TFB_CUDA(cudaMemset(w->ranks[r].heap, 0, w->heap_bytes));
+    TFB_CUDA(cudaDeviceSynchronize());
   }
   return TF_OK;
 }
@@ -572,7 +602,7 @@ tf_status tf_wait_signal(tf_world* tw, const char* board, int rank, int row, int
   if (!w->ranks[rank].local)
     return set_error(TF_ERR_BOUNDS, "wait_signal: rank " + std::to_string(rank) + " is not local");
   cudaSetDevice(w->ranks[rank].device);
-  wait_kernel<<<1, 1, 0, w->ranks[rank].stream>>>(cell, expected, w->watchdog_ns, w->err_dev, rank,
+  wait_kernel<<<1, 1, 0, w->ranks[rank].stream>>>(cell, expected, w->watchdog_ns, w->err_of(rank), rank,
                                                   b.id, row, slot);
   TFB_CUDA(cudaGetLastError());
   ++w->launches;
@@ -627,7 +657,7 @@ tf_status tf_signal_soak(tf_world* tw, uint64_t seed, int rounds, uint64_t* viol
     soak_kernel<<<w->W, 64, 0, streams[r]>>>(
         reinterpret_cast<uint32_t* const*>(t), reinterpret_cast<uint64_t* const*>(t + 64),
         reinterpret_cast<uint64_t* const*>(t + 128), r, w->W, seed, rounds, base,
-        reinterpret_cast<unsigned long long*>(w->ptr(r, cnt_off)), w->watchdog_ns, w->err_dev,
+        reinterpret_cast<unsigned long long*>(w->ptr(r, cnt_off)), w->watchdog_ns, w->err_of(r),
         fb.id);
     TFB_CUDA(cudaGetLastError());
     ++w->launches;
@@ -667,6 +697,13 @@ tf_status tf_memcpy(tf_world* tw, void* dst, const void* src, size_t bytes) {
   return TF_OK;
 }
 
+tf_status tf_memcpy_async(tf_world* tw, void* dst, const void* src, size_t bytes, void* stream) {
+  if (!tw || (!dst && bytes) || (!src && bytes)) return set_error(TF_ERR_CONFIG, "tf_memcpy_async: NULL argument");
+  if (bytes == 0) return TF_OK;
+  TFB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+  return TF_OK;
+}
+
 tf_status tf_device_alloc(tf_world* tw, int rank, size_t bytes, void** out) {
   if (!tw || !out) return set_error(TF_ERR_CONFIG, "tf_device_alloc: NULL argument");
   World* w = &tw->impl;
@@ -675,6 +712,7 @@ tf_status tf_device_alloc(tf_world* tw, int rank, size_t bytes, void** out) {
   TFB_CUDA(cudaSetDevice(w->ranks[rank].device));
   TFB_CUDA(cudaMalloc(out, bytes ? bytes : 1));
   TFB_CUDA(cudaMemset(*out, 0, bytes ? bytes : 1));
+  TFB_CUDA(cudaDeviceSynchronize());
   return TF_OK;
 }
 

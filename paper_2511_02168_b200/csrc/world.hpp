@@ -59,8 +59,9 @@ struct World {
   std::map<std::string, HeapEntry> heap;
   std::map<std::string, BoardEntry> boards;
   std::vector<std::string> board_names;  // id -> name
-  DevErr* err_host = nullptr;
-  DevErr* err_dev = nullptr;
+  // Error records in device memory, one per local device: cheap to poll
+  // from spinning kernels; the host reads them after a sync.
+  std::map<int, DevErr*> errs;
   uint64_t launches = 0;
   uint64_t barrier_epoch = 0;
   uint64_t ag_epoch = 0;
@@ -74,6 +75,7 @@ struct World {
   bool loopback = false;
 
   char* ptr(int rank, size_t offset) const { return ranks[rank].heap + offset; }
+  DevErr* err_of(int r) const { return errs.at(ranks[r].device); }
   bool is_local(int r) const { return r >= first_local && r < first_local + n_local; }
 };
 
