@@ -51,7 +51,8 @@ constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 
 template <int CG>
 struct Cfg {
-  static constexpr int STAGES = CG == 2 ? 6 : 4;
+  // As deep as 227 KB of smem allows: the ring must cover the TMA round trip.
+  static constexpr int STAGES = CG == 2 ? 7 : 4;
   static constexpr int BN_CTA = BN / CG;                // B columns staged per CTA
   static constexpr int B_BYTES = BK * BN_CTA * 2;       // 16 KB (pair) / 32 KB
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -79,11 +80,14 @@ struct AgTcParams {
 
 // Pair-tile raster: GROUP_M pair-rows at a time, column-major inside the
 // group, so concurrently running clusters share B panels in L2.
+__constant__ int g_group_m;  // raster group (pair-rows); GROUP_M unless overridden
+
 __device__ __forceinline__ void tile_coords(int num_mt, int num_n, int t, int& mt, int& nb) {
-  const int per_group = GROUP_M * num_n;
+  const int gm = g_group_m > 0 ? g_group_m : GROUP_M;
+  const int per_group = gm * num_n;
   const int group = t / per_group;
-  const int first_m = group * GROUP_M;
-  const int gsize = min(num_mt - first_m, GROUP_M);
+  const int first_m = group * gm;
+  const int gsize = min(num_mt - first_m, gm);
   const int r = t % per_group;
   mt = first_m + r % gsize;
   nb = r / gsize;
@@ -108,13 +112,15 @@ __device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
   return r;
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
 // Barriers a pair's peer can complete are polled (see mbar_wait_cluster).
+__constant__ int g_dbg_flags;  // diagnosis knobs mirrored from AgTcParams::dbg
+
 template <int CG>
 __device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity) {
-  if (CG == 2) mbar_wait_cluster(bar, parity);
+  if (CG == 2 && (g_dbg_flags & 32)) mbar_wait_cluster(bar, parity);
   else mbar_wait(bar, parity);
 }
 
@@ -522,6 +528,18 @@ EncodeFn encode_fn() {
   return fn;
 }
 
+CUtensorMapL2promotion l2_promotion() {
+  if (const char* e = std::getenv("TFB_L2PROMO")) {
+    switch (std::atoi(e)) {
+      case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+      case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+      case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+      default: break;
+    }
+  }
+  return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 // 2-D bf16 map: `inner` contiguous elements per row, `outer` rows, row pitch
 // `pitch_elems`; box {box_inner, box_outer}; 128-byte swizzle.
 tf_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
@@ -534,7 +552,7 @@ tf_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t ou
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
   return TF_OK;
@@ -589,6 +607,7 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
     attr_set[CG - 1][dev & 63] = true;
   }
   const unsigned pair_tiles = unsigned((p.num_m + CG - 1) / CG) * unsigned(p.num_n);
+  if (const char* e = std::getenv("TFB_GRID")) grid_cap = std::min(grid_cap, unsigned(std::atoi(e)));
   unsigned grid = std::min(pair_tiles * CG, grid_cap / CG * CG);
   grid = std::max(grid, unsigned(CG));
   cudaLaunchConfig_t cfg{};
@@ -603,6 +622,17 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  {
+    static int last_dbg[64] = {}, last_gm[64] = {};
+    int gm = 0;
+    if (const char* e = std::getenv("TFB_GROUP_M")) gm = std::atoi(e);
+    if (last_dbg[dev & 63] != p.dbg || last_gm[dev & 63] != gm) {
+      TFB_CUDA(cudaMemcpyToSymbol(g_dbg_flags, &p.dbg, sizeof(int)));
+      TFB_CUDA(cudaMemcpyToSymbol(g_group_m, &gm, sizeof(int)));
+      last_dbg[dev & 63] = p.dbg;
+      last_gm[dev & 63] = gm;
+    }
+  }
   TFB_CUDA(cudaLaunchKernelEx(&cfg, kern, mOwn, mInbox, mB, p));
   ++w->launches;
   return TF_OK;

@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kFastThreads) fd_attention_kernel(const FdPara
   __shared__ unsigned int s_item;
   __shared__ int s_last;
   __shared__ FastSmem fsm;
-  __shared__ float s_M[32], s_L[32], s_w[kFoldW];
+  __shared__ float s_M[32], s_L[32], s_w[kFoldW], s_l[kFoldW];
   const int G = P.B * P.Hkv;
   const unsigned total = unsigned(P.nlocal) * G * P.S;
   const int d = P.d, row_len = d + 2;
@@ -469,50 +469,112 @@ __global__ void __launch_bounds__(kFastThreads) fd_attention_kernel(const FdPara
     // (tilemath.hpp:186-220) evaluated in one pass instead of S dependent
     // steps (the serial chain was the tail of every launch).  Identical code
     // in every schedule, so schedules stay bitwise equal.
-    for (int h = threadIdx.x; h < P.gs; h += blockDim.x) {
-      float M = -INFINITY;
-      for (int s = 0; s < P.S; ++s) {
-        const float* row = grp + (size_t(s) * P.gs + h) * row_len;
-        if (__ldcg(row + 1) != 0.0f) M = fmaxf(M, __ldcg(row));
-      }
-      float L = 0.0f;
-      for (int s = 0; s < P.S; ++s) {
-        const float* row = grp + (size_t(s) * P.gs + h) * row_len;
-        const float l = __ldcg(row + 1);
-        const float w = l != 0.0f ? expf(__ldcg(row) - M) : 0.0f;
-        if (size_t(s) * P.gs + h < kFoldW) s_w[s * P.gs + h] = w;
-        L = __fadd_rn(L, __fmul_rn(l, w));
-      }
-      s_M[h] = M;
-      s_L[h] = L;
-    }
-    __syncthreads();
     const size_t base_src = size_t(R.rank) * P.B * P.Hq * row_len;
-    for (int idx = threadIdx.x; idx < P.gs * (d + 2); idx += blockDim.x) {
-      const int h = idx / (d + 2), e = idx % (d + 2);
-      float val;
-      if (e == 0) {
-        val = s_M[h];
-      } else if (e == 1) {
-        val = s_L[h];
-      } else {
-        const float M = s_M[h];
-        float o = 0.0f;
-        for (int s = 0; s < P.S; ++s) {
-          const float* row = grp + (size_t(s) * P.gs + h) * row_len;
-          const float w = (size_t(s) * P.gs + h < kFoldW)
-                              ? s_w[s * P.gs + h]
-                              : (__ldcg(row + 1) != 0.0f ? expf(__ldcg(row) - M) : 0.0f);
-          if (w != 0.0f) o = __fadd_rn(o, __fmul_rn(__ldcg(row + e), w));
-        }
-        val = o;
-      }
+    auto put = [&](int h, int e, float val) {
       const int hq = kvh * P.gs + h;
       const size_t roff = (size_t(b) * P.Hq + hq) * row_len + e;
       if (P.push) {
         for (int dst = 0; dst < P.W; ++dst) P.inbox_all[dst][base_src + roff] = val;
       } else {
         R.pub[roff] = val;
+      }
+    };
+    const int SG = P.S * P.gs;
+    if (SG <= kFoldW && (d % 2) == 0) {
+      // (1) every (split, head) m/l pair, loaded in parallel
+      for (int i = threadIdx.x; i < SG; i += blockDim.x) {
+        const float* row = grp + size_t(i) * row_len;  // i = s * gs + h
+        const float l = __ldcg(row + 1);
+        s_w[i] = l != 0.0f ? __ldcg(row) : -INFINITY;
+        s_l[i] = l;
+      }
+      __syncthreads();
+      // (2) per-head max
+      for (int h = threadIdx.x; h < P.gs; h += blockDim.x) {
+        float M = -INFINITY;
+        for (int s = 0; s < P.S; ++s) M = fmaxf(M, s_w[s * P.gs + h]);
+        s_M[h] = M;
+      }
+      __syncthreads();
+      // (3) weights
+      for (int i = threadIdx.x; i < SG; i += blockDim.x)
+        s_w[i] = s_l[i] != 0.0f ? expf(s_w[i] - s_M[i % P.gs]) : 0.0f;
+      __syncthreads();
+      // (4) normalisers, and the weighted o sums with 8-byte loads, four
+      //     independent accumulators per thread so many loads are in flight
+      for (int h = threadIdx.x; h < P.gs; h += blockDim.x) {
+        float L = 0.0f;
+        for (int s = 0; s < P.S; ++s) L = __fadd_rn(L, __fmul_rn(s_l[s * P.gs + h], s_w[s * P.gs + h]));
+        s_L[h] = L;
+      }
+      const int pairs = P.gs * (d / 2);
+      for (int pi = threadIdx.x; pi < pairs; pi += blockDim.x) {
+        const int h = pi / (d / 2), e = 2 * (pi % (d / 2));
+        float2 acc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = make_float2(0.f, 0.f);
+        int s = 0;
+        for (; s + 4 <= P.S; s += 4) {
+          float2 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            v[u] = __ldcg(reinterpret_cast<const float2*>(grp + (size_t(s + u) * P.gs + h) * row_len + 2 + e));
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float w = s_w[(s + u) * P.gs + h];
+            acc[u].x = __fadd_rn(acc[u].x, __fmul_rn(v[u].x, w));
+            acc[u].y = __fadd_rn(acc[u].y, __fmul_rn(v[u].y, w));
+          }
+        }
+        for (; s < P.S; ++s) {
+          const float2 v = __ldcg(reinterpret_cast<const float2*>(grp + (size_t(s) * P.gs + h) * row_len + 2 + e));
+          const float w = s_w[s * P.gs + h];
+          acc[0].x = __fadd_rn(acc[0].x, __fmul_rn(v.x, w));
+          acc[0].y = __fadd_rn(acc[0].y, __fmul_rn(v.y, w));
+        }
+        put(h, 2 + e, __fadd_rn(__fadd_rn(acc[0].x, acc[1].x), __fadd_rn(acc[2].x, acc[3].x)));
+        put(h, 3 + e, __fadd_rn(__fadd_rn(acc[0].y, acc[1].y), __fadd_rn(acc[2].y, acc[3].y)));
+      }
+      __syncthreads();
+      for (int h = threadIdx.x; h < P.gs; h += blockDim.x) {
+        put(h, 0, s_M[h]);
+        put(h, 1, s_L[h]);
+      }
+    } else {
+      // Large S x gs: per-head scalar fold (weights recomputed).
+      for (int h = threadIdx.x; h < P.gs; h += blockDim.x) {
+        float M = -INFINITY;
+        for (int s = 0; s < P.S; ++s) {
+          const float* row = grp + (size_t(s) * P.gs + h) * row_len;
+          if (__ldcg(row + 1) != 0.0f) M = fmaxf(M, __ldcg(row));
+        }
+        float L = 0.0f;
+        for (int s = 0; s < P.S; ++s) {
+          const float* row = grp + (size_t(s) * P.gs + h) * row_len;
+          const float l = __ldcg(row + 1);
+          L = __fadd_rn(L, __fmul_rn(l, l != 0.0f ? expf(__ldcg(row) - M) : 0.0f));
+        }
+        s_M[h] = M;
+        s_L[h] = L;
+      }
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < P.gs * (d + 2); idx += blockDim.x) {
+        const int h = idx / (d + 2), e = idx % (d + 2);
+        float val;
+        if (e == 0) {
+          val = s_M[h];
+        } else if (e == 1) {
+          val = s_L[h];
+        } else {
+          float o = 0.0f;
+          for (int s = 0; s < P.S; ++s) {
+            const float* row = grp + (size_t(s) * P.gs + h) * row_len;
+            const float w = __ldcg(row + 1) != 0.0f ? expf(__ldcg(row) - s_M[h]) : 0.0f;
+            if (w != 0.0f) o = __fadd_rn(o, __fmul_rn(__ldcg(row + e), w));
+          }
+          val = o;
+        }
+        put(h, e, val);
       }
     }
     if (P.push) {
@@ -665,7 +727,9 @@ static bool fast_ok(const tf_fd_shape& s) {
 // and every rank cuts identically.
 static int choose_splits(const tf_fd_shape& s, size_t len, int sms) {
   const long groups = long(s.batch) * s.kv_heads;
-  long want = (long(sms) * 4 + groups - 1) / groups;
+  // ~2 items per SM: enough CTAs to saturate HBM, few enough splits that the
+  // group fold (S rows per head) stays short (measured sweep, profiles/).
+  long want = (long(sms) * 2 + groups - 1) / groups;
   long maxs = long((len + 63) / 64);
   long S = std::max(1L, std::min(want, maxs));
   if (const char* e = std::getenv("TFB_FD_SPLITS")) S = std::max(1L, std::min(std::atol(e), maxs));
