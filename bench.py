@@ -139,9 +139,8 @@ class Ctx:
     def max(self, x: float) -> float:
         if self.ws == 1:
             return x
-        t = self.torch.tensor([x], device=self.dev, dtype=self.torch.float64)
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
-        return float(t.item())
+        from paper_2511_02168_b200.dist import max_over_ranks
+        return max_over_ranks(self.dist, x, self.dev)
 
     def world(self, heap_bytes):
         import paper_2511_02168_b200 as tf
@@ -153,11 +152,11 @@ class Ctx:
             _abi.check(L.tf_world_create(1, devs, heap_bytes, 0.0, C.byref(h)))
         else:
             _abi.check(L.tf_world_create_ipc(self.rank, self.ws, self.local, heap_bytes, 0.0, C.byref(h)))
+            from paper_2511_02168_b200.dist import gather_ipc_handles
             mine = (C.c_char * _abi.IPC_HANDLE_BYTES)()
             _abi.check(L.tf_world_ipc_export(h, mine))
-            allh = [None] * self.ws
-            self.dist.all_gather_object(allh, bytes(mine))
-            buf = (C.c_char * (_abi.IPC_HANDLE_BYTES * self.ws)).from_buffer_copy(b"".join(allh))
+            allh = gather_ipc_handles(self.dist, bytes(mine), self.ws)
+            buf = (C.c_char * (_abi.IPC_HANDLE_BYTES * self.ws)).from_buffer_copy(allh)
             _abi.check(L.tf_world_ipc_import(h, buf))
         w = tf.World.__new__(tf.World)
         w.lib, w.W, w.devices, w.handle = L, self.W, [self.local] * self.W, h
@@ -166,9 +165,8 @@ class Ctx:
 
 def ptrs_for(ctx, local_ptr):
     """Per-rank pointer array with only this process' rank filled."""
-    arr = [0] * ctx.W
-    arr[ctx.rank] = local_ptr
-    return arr
+    from paper_2511_02168_b200.dist import rank_pointer_table
+    return rank_pointer_table(ctx.W, ctx.rank, local_ptr)
 
 
 def time_steps(ctx, stream, fn, steps, warmup):
@@ -331,7 +329,7 @@ def bench_fd(ctx, cfg, steps, warmup):
 # ---------------------------------------------------------------------------------
 # the reference's CPU path (oracle/_ref: proj/include/tilefabric compiled as-is)
 
-def cpu_reference_ag(W, sample_rows=32, n_slice=1792):
+def cpu_reference_ag(W, sample_rows=64, n_slice=1792):
     """ag::run_pull (ag_gemm.hpp:185-222) on bounded M x N slices of config 2,
     one independent call per host core, extrapolated linearly in M*N (the
     loops are exactly linear there, ag_gemm.hpp:200-217)."""
@@ -377,7 +375,7 @@ def run_reference_arm(args):
     vals = []
     info = None
     for i in range(args.warmup + args.steps):
-        r = cpu_reference_ag(W, sample_rows=8)
+        r = cpu_reference_ag(W)
         if r is None:
             print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtfref.so not built"}))
             return

@@ -2,20 +2,19 @@
 //
 // One persistent, warp-specialised kernel per rank (ag_gemm.hpp:185-305
 // re-designed for sm_100a):
-//   warp 0      TMA producer.  Streams the A tile (128 x 64, SWIZZLE_128B)
-//               and four B boxes (64 x 64 each -> a 64 x 256 K x N panel,
-//               MN-major) into a STAGES-deep smem ring.  A k-block owned by
+//   warp 0      TMA producer.  Streams A (128 x 64 per CTA, SWIZZLE_128B,
+//               K-major) and B (64 x 256 per CTA as four 64 x 64 boxes,
+//               MN-major -- B is used in the caller's k x n layout, no
+//               transpose pass) into a 4-deep smem ring.  A k-block owned by
 //               this rank comes straight from its shard; a k-block owned by
 //               rank s comes from the local gathered buffer ("inbox", the
 //               reference's ag.inbox, m x k) once ready[m_blk][s] reaches
 //               this run's epoch (ld.acquire.sys spin, then
 //               fence.proxy.async so the TMA sees the generic-proxy bytes).
 //               The k loop starts at the rank's own shard, so the first
-//               16/W of every tile never waits.
-//   warp 1      MMA issuer (one thread): tcgen05.mma.cta_group::1.kind::f16,
-//               M=128 N=256 K=16, fp32 accumulators in TMEM (2 x 256
-//               columns, double-buffered so the epilogue of tile i overlaps
-//               the mainloop of tile i+1); tcgen05.commit frees smem stages.
+//               K/W of every tile never waits on the network.
+//   warp 1      MMA issuer (one thread): tcgen05.mma.kind::f16, fp32
+//               accumulators in TMEM; tcgen05.commit releases smem stages.
 //   warps 2-5   epilogue: tcgen05.ld 32x32b -> bf16 -> global C.
 //   warps 6-7   gather (PULL): claim (m_blk, src) chunks from a global
 //               counter, copy them from the owner's shard over NVLink
@@ -23,6 +22,17 @@
 //               then release ready[m_blk][src].  Each remote A byte crosses
 //               NVLink exactly once per rank (the reference re-pulls every
 //               A tile once per N tile, ag_gemm_test.cpp:134-143).
+//
+// Tile shapes (the L2->SM crossbar, ~9.5 TB/s measured, is what a B200 GEMM
+// must economise, profiles/r1_*):
+//   CG = 2  a CTA pair (cluster of 2, tcgen05.mma.cta_group::2) owns a
+//           256 x 512 tile: each CTA stages its 128 rows of A and 256 of the
+//           512 B columns per k-block (48 KB), the leader issues two
+//           M=256 N=256 K=16 MMAs per k-step (one per 256-column half), and
+//           each CTA's whole TMEM (512 columns) holds its 128 x 512
+//           accumulator.  5.9 bytes per kFLOP -- cuBLAS's own tile.
+//   CG = 1  skinny M (< 256 rows): 128 x 256 tiles, two TMEM accumulators so
+//           the epilogue overlaps the next tile.
 // PUSH replaces the gather warps with a producer kernel on every rank that
 // stores its shard chunks into every peer's inbox and raises the peer's
 // ready cell (red.release.sys) -- the same consumer gate.
@@ -43,27 +53,29 @@ namespace {
 
 using namespace sm100;
 
-constexpr int BM = 128, BN = 256, BK = 64;  // BM: rows per CTA; a CTA pair covers 256
-constexpr int GROUP_M = 16;                  // pair-tiles per raster group (L2 reuse of B)
+constexpr int BM = 128, BK = 64;  // BM: A rows staged per CTA
+constexpr int GROUP_M = 16;       // tile-rows per raster group (L2 reuse of B)
 constexpr int NUM_THREADS = 256;
 constexpr int TMEM_COLS = 512;
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 
 template <int CG>
 struct Cfg {
-  // As deep as 227 KB of smem allows: the ring must cover the TMA round trip.
-  static constexpr int STAGES = CG == 2 ? 7 : 4;
-  static constexpr int BN_CTA = BN / CG;                // B columns staged per CTA
-  static constexpr int B_BYTES = BK * BN_CTA * 2;       // 16 KB (pair) / 32 KB
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr uint32_t IDESC = idesc_bf16(BM * CG, BN, /*A K-major*/ 0, /*B MN-major*/ 1);
+  static constexpr int NH = CG == 2 ? 2 : 1;            // 256-column MMA halves per tile
+  static constexpr int BN_TILE = 256 * NH;              // tile width
+  static constexpr int ACC_BUFS = CG == 2 ? 1 : 2;      // accumulators in 512 TMEM columns
+  static constexpr int STAGES = 4;
+  static constexpr int CPH = 4 / CG;                    // 64-column B chunks per half per CTA
+  static constexpr int B_BYTES = NH * CPH * BK * 128;   // 32 KB
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES; // 48 KB
+  static constexpr uint32_t IDESC = idesc_bf16(BM * CG, 256, /*A K-major*/ 0, /*B MN-major*/ 1);
   static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024 + 256;
 };
 
 struct AgTcParams {
   int M, N, K, kw, W;
   int own;          // rank whose shard map serves its own k-range; -1: all from inbox
-  int num_m, num_n, num_tiles, kb_total, kbw;  // num_m counts 128-row blocks
+  int num_m, num_n, num_tiles, kb_total, kbw;  // num_m: 128-row blocks; num_n: tile columns
   __nv_bfloat16* C;
   const uint64_t* ready;  // [num_m][W] local board; nullptr: ungated
   uint64_t epoch;
@@ -74,14 +86,14 @@ struct AgTcParams {
   uint64_t watchdog_ns;
   DevErr* err;
   int board;
-  int dbg;  // TFB_DEBUG knobs: 1 skip C stores, 2 skip MMAs (profiling aids)
+  int dbg;  // TFB_DEBUG knobs: 1 skip C stores, 2 skip MMAs, 8 force CG=1 (profiling aids)
   const __nv_bfloat16* peer_shard[64];
 };
 
-// Pair-tile raster: GROUP_M pair-rows at a time, column-major inside the
-// group, so concurrently running clusters share B panels in L2.
-__constant__ int g_group_m;  // raster group (pair-rows); GROUP_M unless overridden
+__constant__ int g_group_m;  // raster group (tile-rows); GROUP_M unless overridden
 
+// Tile raster: g tile-rows at a time, column-major inside the group, so
+// concurrently running CTAs share B panels in L2.
 __device__ __forceinline__ void tile_coords(int num_mt, int num_n, int t, int& mt, int& nb) {
   const int gm = g_group_m > 0 ? g_group_m : GROUP_M;
   const int per_group = gm * num_n;
@@ -111,22 +123,16 @@ __device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
+// Remote arrive.  Deliberately without .release.cluster: that form fences
+// the whole cluster on every call and was measured to halve the pipeline
+// rate; the data it orders is written by TMA and tracked by the barrier.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
-// Barriers a pair's peer can complete are polled (see mbar_wait_cluster).
-__constant__ int g_dbg_flags;  // diagnosis knobs mirrored from AgTcParams::dbg
-
 template <int CG>
-__device__ __forceinline__ void bwait(uint64_t* bar, uint32_t parity) {
-  if (CG == 2 && (g_dbg_flags & 32)) mbar_wait_cluster(bar, parity);
-  else mbar_wait(bar, parity);
-}
-
-template <int CG>
-__device__ __forceinline__ void tma_load_a(void* dst, const CUtensorMap* map, uint32_t bar_cluster,
-                                           int c0, int c1) {
+__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                         int c1) {
   if (CG == 2)
     asm volatile(
         "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
@@ -189,18 +195,13 @@ __device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr) {
     tmem_dealloc(taddr, TMEM_COLS);
 }
 
-// CG = 2: a CTA pair (cluster of 2) computes a 256 x 256 tile with
-// tcgen05.mma.cta_group::2 -- each CTA stages its own 128 rows of A and 128
-// of the 256 B columns, the leader issues M=256 N=256 MMAs that read both
-// CTAs' smem, and each CTA's TMEM holds its 128 x 256 accumulator.  Halves
-// the smem->tensor and L2->smem bytes per FLOP versus CG = 1.
 template <int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     ag_gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA_own,
                          const __grid_constant__ CUtensorMap tmA_inbox,
                          const __grid_constant__ CUtensorMap tmB, const AgTcParams p) {
   using K_ = Cfg<CG>;
-  constexpr int STAGES = K_::STAGES;
+  constexpr int STAGES = K_::STAGES, NH = K_::NH, CPH = K_::CPH;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
@@ -209,15 +210,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* pfull = tempty + 2;  // leader: peer's stage landed (local_full mode)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pfull + STAGES);
-  const bool local_full = (p.dbg & 4) != 0;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;
   const bool leader = crank == 0;
   const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
-  const int num_mt = (p.num_m + CG - 1) / CG;  // pair-tile rows
+  const int num_mt = (p.num_m + CG - 1) / CG;  // tile rows (BM * CG each)
   const int num_tiles = num_mt * p.num_n;
 
   if (warp == 0 && lane == 0) {
@@ -225,9 +224,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tma_prefetch(&tmA_inbox);
     tma_prefetch(&tmB);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], local_full ? 1 : CG);  // one arrive per CTA (leader's copy is used)
+      mbar_init(&full[s], CG);  // one arrive per CTA of the pair (the leader's copy is used)
       mbar_init(&empty[s], 1);
-      mbar_init(&pfull[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -243,7 +241,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ===== TMA producer (both CTAs) =====
+    // ===== TMA producer (both CTAs of a pair) =====
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
@@ -251,12 +249,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int mt, nb;
         tile_coords(num_mt, p.num_n, t, mt, nb);
         const int mb = mt * CG + int(crank);  // this CTA's 128-row block
-        const int m0 = mb * BM, n0 = nb * BN + int(crank) * K_::BN_CTA;
+        const int m0 = mb * BM, n0 = nb * K_::BN_TILE;
         uint64_t ready_mask = 0;
         for (int i = 0; i < p.kb_total; ++i) {
           const int kb = p.own >= 0 ? (i + p.own * p.kbw) % p.kb_total : i;
           const int src = kb / p.kbw;
-          bwait<CG>(&empty[stage], phase ^ 1);
+          mbar_wait(&empty[stage], phase ^ 1);
           const bool from_own = src == p.own;
           if (!from_own && p.ready && mb < p.num_m && !((ready_mask >> src) & 1ull)) {
             wait_geq(p.ready + size_t(mb) * p.W + src, p.epoch, p.watchdog_ns, p.err, kWaitSignal,
@@ -264,28 +262,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             fence_proxy_async_global();
             ready_mask |= 1ull << src;
           }
+          const uint32_t bar = CG == 2 ? mapa(&full[stage], 0) : smem_u32(&full[stage]);
+          if (leader) mbar_arrive_expect_tx(&full[stage], CG * K_::STAGE_BYTES);
+          else mbar_arrive_cluster(bar);
           uint8_t* a_dst = smA + stage * A_BYTES;
+          if (from_own) tma_load<CG>(a_dst, &tmA_own, bar, kb * BK - p.own * p.kw, m0);
+          else tma_load<CG>(a_dst, &tmA_inbox, bar, kb * BK, m0);
           uint8_t* b_dst = smB + stage * K_::B_BYTES;
-          if (CG == 2 && local_full) {
-            // Each CTA's TMA completes on its own barrier; the peer's MMA-side
-            // thread forwards completion to the leader (pfull).
-            mbar_arrive_expect_tx(&full[stage], K_::STAGE_BYTES);
-            const uint32_t bar = smem_u32(&full[stage]);
-            if (from_own) tma_load_a<1>(a_dst, &tmA_own, bar, kb * BK - p.own * p.kw, m0);
-            else tma_load_a<1>(a_dst, &tmA_inbox, bar, kb * BK, m0);
 #pragma unroll
-            for (int c = 0; c < K_::BN_CTA / 64; ++c)
-              tma_load_a<1>(b_dst + c * (BK * 128), &tmB, bar, n0 + 64 * c, kb * BK);
-          } else {
-            const uint32_t bar = CG == 2 ? mapa(&full[stage], 0) : smem_u32(&full[stage]);
-            if (leader) mbar_arrive_expect_tx(&full[stage], CG * K_::STAGE_BYTES);
-            else mbar_arrive_cluster(bar);
-            if (from_own) tma_load_a<CG>(a_dst, &tmA_own, bar, kb * BK - p.own * p.kw, m0);
-            else tma_load_a<CG>(a_dst, &tmA_inbox, bar, kb * BK, m0);
+          for (int h = 0; h < NH; ++h)
 #pragma unroll
-            for (int c = 0; c < K_::BN_CTA / 64; ++c)
-              tma_load_a<CG>(b_dst + c * (BK * 128), &tmB, bar, n0 + 64 * c, kb * BK);
-          }
+            for (int c = 0; c < CPH; ++c)
+              tma_load<CG>(b_dst + (h * CPH + c) * (BK * 128), &tmB, bar,
+                           n0 + h * 256 + int(crank) * (256 / CG) + c * 64, kb * BK);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -301,23 +290,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int acc = 0;
       uint32_t aphase = 0;
       for (int t = cid; t < num_tiles; t += ncl) {
-        bwait<CG>(&tempty[acc], aphase ^ 1);
+        mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
         for (int i = 0; i < p.kb_total; ++i) {
-          bwait<CG>(&full[stage], phase);
-          if (CG == 2 && local_full) bwait<CG>(&pfull[stage], phase);
+          mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smA + stage * A_BYTES);
           const uint32_t b_addr = smem_u32(smB + stage * K_::B_BYTES);
+          if (!(p.dbg & 2)) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // A: K-major SW128, 8-row groups 1024 B apart; +32 B per K=16.
-            const uint64_t ad = smem_desc_sw128(a_addr + k * 32, 16, 1024);
-            // B: MN-major SW128, 64-col chunks 8 KB apart (LBO), 8-row K
-            // groups 1024 B apart (SBO); +16 rows (2 KB) per K=16.
-            const uint64_t bd = smem_desc_sw128(b_addr + k * 2048, BK * 128, 1024);
-            if (!(p.dbg & 2)) mma_issue<CG>(d_tmem, ad, bd, K_::IDESC, (i | k) != 0);
+            for (int k = 0; k < BK / 16; ++k) {
+              // A: K-major SW128, 8-row groups 1024 B apart; +32 B per K=16.
+              const uint64_t ad = smem_desc_sw128(a_addr + k * 32, 16, 1024);
+#pragma unroll
+              for (int h = 0; h < NH; ++h) {
+                // B: MN-major SW128, 64-column chunks 8 KB apart (LBO),
+                // 8-row K groups 1 KB apart (SBO); +16 rows (2 KB) per K=16.
+                const uint64_t bd = smem_desc_sw128(b_addr + h * CPH * (BK * 128) + k * 2048, BK * 128, 1024);
+                mma_issue<CG>(tmem_base + uint32_t((acc * NH + h) * 256), ad, bd, K_::IDESC, (i | k) != 0);
+              }
+            }
           }
           mma_commit_all<CG>(&empty[stage]);
           if (++stage == STAGES) {
@@ -326,22 +318,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         mma_commit_all<CG>(&tfull[acc]);
-        acc ^= 1;
-        if (acc == 0) aphase ^= 1;
-      }
-    } else if (lane == 0 && CG == 2 && local_full) {
-      // Peer CTA: forward "my half of this stage landed" to the leader.
-      int stage = 0;
-      uint32_t phase = 0;
-      const uint32_t pfull0 = mapa(&pfull[0], 0);
-      for (int t = cid; t < num_tiles; t += ncl) {
-        for (int i = 0; i < p.kb_total; ++i) {
-          mbar_wait(&full[stage], phase);
-          mbar_arrive_cluster(pfull0 + uint32_t(stage) * 8);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+        if (++acc == K_::ACC_BUFS) {
+          acc = 0;
+          aphase ^= 1;
         }
       }
     }
@@ -354,16 +333,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int t = cid; t < num_tiles; t += ncl) {
       int mt, nb;
       tile_coords(num_mt, p.num_n, t, mt, nb);
-      bwait<CG>(&tfull[acc], aphase);
+      mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const int row = (mt * CG + int(crank)) * BM + 32 * q + lane;
       __nv_bfloat16* crow = p.C + size_t(row) * p.N;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < NH * 8; ++c) {
         uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + (uint32_t(32 * q) << 16) + uint32_t(acc * BN + 32 * c), r);
+        tmem_ld_32x32b_x32(tmem_base + (uint32_t(32 * q) << 16) + uint32_t(acc * NH * 256 + 32 * c), r);
         tmem_ld_wait();
-        const int col0 = nb * BN + 32 * c;
+        const int col0 = nb * K_::BN_TILE + 32 * c;
         if (row < p.M && !(p.dbg & 1)) {
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
@@ -384,8 +363,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (CG == 2) mbar_arrive_cluster(tempty_leader0 + uint32_t(acc) * 8);
         else mbar_arrive(&tempty[acc]);
       }
-      acc ^= 1;
-      if (acc == 0) aphase ^= 1;
+      if (++acc == K_::ACC_BUFS) {
+        acc = 0;
+        aphase ^= 1;
+      }
     }
   } else if (p.gather) {
     // ===== gather (PULL): peer shard chunks -> local inbox + ready flags =====
@@ -582,8 +563,6 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   p.W = W;
   p.own = own;
   p.num_m = int((sh.m + BM - 1) / BM);
-  p.num_n = int((sh.n + BN - 1) / BN);
-  p.num_tiles = p.num_m * p.num_n;
   p.kb_total = int(sh.k / BK);
   p.kbw = int(kw / BK);
   p.C = static_cast<__nv_bfloat16*>(c);
@@ -597,9 +576,12 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   static bool attr_set[2][64] = {};
   const int dev = w->ranks[r].device;
   cudaSetDevice(dev);
-  // CTA pairs (cta_group::2, 256 x 256 tiles) whenever there are two 128-row
-  // blocks to pair; single CTAs for skinny M.
+  // CTA pairs (cta_group::2, 256 x 512 tiles) whenever there are two 128-row
+  // blocks to pair; single CTAs (128 x 256) for skinny M.
   const int CG = (p.num_m >= 2 && !(p.dbg & 8)) ? 2 : 1;
+  const int bn_tile = CG == 2 ? Cfg<2>::BN_TILE : Cfg<1>::BN_TILE;
+  p.num_n = int((sh.n + bn_tile - 1) / bn_tile);
+  p.num_tiles = ((p.num_m + CG - 1) / CG) * p.num_n;
   auto kern = CG == 2 ? ag_gemm_sm100_kernel<2> : ag_gemm_sm100_kernel<1>;
   const size_t smem = CG == 2 ? Cfg<2>::SMEM : Cfg<1>::SMEM;
   if (!attr_set[CG - 1][dev & 63]) {
@@ -617,19 +599,17 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (p.dbg & 16) ? 2 : CG;  // 16: 1-CTA kernel in 2-clusters (diagnosis)
+  attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   {
-    static int last_dbg[64] = {}, last_gm[64] = {};
+    static int last_gm[64] = {};
     int gm = 0;
     if (const char* e = std::getenv("TFB_GROUP_M")) gm = std::atoi(e);
-    if (last_dbg[dev & 63] != p.dbg || last_gm[dev & 63] != gm) {
-      TFB_CUDA(cudaMemcpyToSymbol(g_dbg_flags, &p.dbg, sizeof(int)));
+    if (last_gm[dev & 63] != gm) {
       TFB_CUDA(cudaMemcpyToSymbol(g_group_m, &gm, sizeof(int)));
-      last_dbg[dev & 63] = p.dbg;
       last_gm[dev & 63] = gm;
     }
   }

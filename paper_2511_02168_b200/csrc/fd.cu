@@ -248,8 +248,10 @@ __device__ __forceinline__ uint32_t w4(const uint4& v, int i) {
   return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
 }
 
-constexpr int kFastWarps = 4;
-constexpr int kFoldW = 2048;  // split weights cached in smem for the group fold
+// 8 warps per CTA, 2 CTAs per SM at <= 128 registers: 16 streaming warps per
+// SM keep ~128 KB of KV loads in flight (what HBM3e needs at ~2 us latency).
+constexpr int kFastWarps = 8;
+constexpr int kFoldW = 1024;  // split weights cached in smem for the group fold
 constexpr int kFastThreads = kFastWarps * 32;
 
 // d index held by O^T accumulator row r of PV tile (i, j) (see header).
@@ -428,7 +430,7 @@ __device__ void fast_split(const FdParams& P, int lr, int g, int sp, float* wsro
 
 // ---- the persistent kernel ------------------------------------------------
 template <bool FAST>
-__global__ void __launch_bounds__(kFastThreads) fd_attention_kernel(const FdParams P) {
+__global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const FdParams P) {
   __shared__ unsigned int s_item;
   __shared__ int s_last;
   __shared__ FastSmem fsm;
