@@ -69,7 +69,8 @@ struct Cfg {
   static constexpr int B_BYTES = NH * CPH * BK * 128;   // 32 KB
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES; // 48 KB
   static constexpr uint32_t IDESC = idesc_bf16(BM * CG, 256, /*A K-major*/ 0, /*B MN-major*/ 1);
-  static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024 + 256;
+  static constexpr int EPI_BYTES = 4 * 2 * 4096;         // C staging for TMA stores
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + EPI_BYTES + 1024 + 256;
 };
 
 struct AgTcParams {
@@ -199,14 +200,16 @@ template <int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     ag_gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA_own,
                          const __grid_constant__ CUtensorMap tmA_inbox,
-                         const __grid_constant__ CUtensorMap tmB, const AgTcParams p) {
+                         const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmC, const AgTcParams p) {
   using K_ = Cfg<CG>;
   constexpr int STAGES = K_::STAGES, NH = K_::NH, CPH = K_::CPH;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
   uint8_t* smB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * K_::STAGE_BYTES);
+  uint8_t* smStage = smem + STAGES * K_::STAGE_BYTES;  // epilogue: 4 warps x 2 x 4 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(smStage + K_::EPI_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -223,6 +226,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tma_prefetch(&tmA_own);
     tma_prefetch(&tmA_inbox);
     tma_prefetch(&tmB);
+    tma_prefetch(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], CG);  // one arrive per CTA of the pair (the leader's copy is used)
       mbar_init(&empty[s], 1);
@@ -335,26 +339,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tile_coords(num_mt, p.num_n, t, mt, nb);
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
-      const int row = (mt * CG + int(crank)) * BM + 32 * q + lane;
-      __nv_bfloat16* crow = p.C + size_t(row) * p.N;
+      // 64-column slabs: two tcgen05.ld (32 columns each) -> bf16 -> a
+      // SWIZZLE_128B smem box [32 rows][64 cols] (conflict-free: 16-byte
+      // chunk j of row r sits at j ^ (r & 7)) -> one TMA store per warp per
+      // slab, double-buffered so the next slab's TMEM reads overlap the store.
+      const int row0 = (mt * CG + int(crank)) * BM + 32 * q;
+      uint8_t* stg = smStage + q * (2 * 4096);
 #pragma unroll 1
-      for (int c = 0; c < NH * 8; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + (uint32_t(32 * q) << 16) + uint32_t(acc * NH * 256 + 32 * c), r);
+      for (int cc = 0; cc < NH * 4; ++cc) {
+        uint32_t r0[32], r1[32];
+        const uint32_t tcol = uint32_t(acc * NH * 256 + 64 * cc);
+        tmem_ld_32x32b_x32(tmem_base + (uint32_t(32 * q) << 16) + tcol, r0);
+        tmem_ld_32x32b_x32(tmem_base + (uint32_t(32 * q) << 16) + tcol + 32, r1);
         tmem_ld_wait();
-        const int col0 = nb * K_::BN_TILE + 32 * c;
-        if (row < p.M && !(p.dbg & 1)) {
+        uint8_t* buf = stg + (cc & 1) * 4096;
+        if (cc >= 2 && lane == 0) bulk_wait_read<1>();
+        __syncwarp();
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            if (col0 + 8 * v < p.N) {
-              uint4 pk;
-              pk.x = pack_bf16x2(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1]));
-              pk.y = pack_bf16x2(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3]));
-              pk.z = pack_bf16x2(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5]));
-              pk.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
-              *reinterpret_cast<uint4*>(crow + col0 + 8 * v) = pk;
-            }
-          }
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t* src = j < 4 ? &r0[8 * j] : &r1[8 * (j - 4)];
+          uint4 pk;
+          pk.x = pack_bf16x2(__uint_as_float(src[0]), __uint_as_float(src[1]));
+          pk.y = pack_bf16x2(__uint_as_float(src[2]), __uint_as_float(src[3]));
+          pk.z = pack_bf16x2(__uint_as_float(src[4]), __uint_as_float(src[5]));
+          pk.w = pack_bf16x2(__uint_as_float(src[6]), __uint_as_float(src[7]));
+          *reinterpret_cast<uint4*>(buf + lane * 128 + ((j ^ (lane & 7)) * 16)) = pk;
+        }
+        fence_proxy_async_shared();
+        __syncwarp();
+        if (lane == 0 && !(p.dbg & 1) && row0 < p.M) {
+          tma_store_2d(&tmC, buf, nb * K_::BN_TILE + 64 * cc, row0);
+          bulk_commit();
         }
       }
       tc_fence_before();
@@ -368,6 +383,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         aphase ^= 1;
       }
     }
+    if (lane == 0) bulk_wait_all();  // C stores complete before the CTA retires
   } else if (p.gather) {
     // ===== gather (PULL): peer shard chunks -> local inbox + ready flags =====
     const int gt = threadIdx.x - 6 * 32;  // 0..63
@@ -549,7 +565,9 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
                              cudaStream_t st, int board, unsigned grid_cap) {
   const int W = w->W;
   const size_t kw = sh.k / W;
-  CUtensorMap mOwn{}, mInbox{}, mB{};
+  CUtensorMap mOwn{}, mInbox{}, mB{}, mC{};
+  // C: 64-column x 32-row boxes, one per epilogue warp per store.
+  TFB_CHECK(make_map(&mC, c, sh.n, sh.m, sh.n, 64, 32));
   if (shard) TFB_CHECK(make_map(&mOwn, shard, kw, sh.m, kw, BK, BM));
   if (inbox) TFB_CHECK(make_map(&mInbox, inbox, sh.k, sh.m, sh.k, BK, BM));
   if (!shard) mOwn = mInbox;
@@ -613,7 +631,7 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
       last_gm[dev & 63] = gm;
     }
   }
-  TFB_CUDA(cudaLaunchKernelEx(&cfg, kern, mOwn, mInbox, mB, p));
+  TFB_CUDA(cudaLaunchKernelEx(&cfg, kern, mOwn, mInbox, mB, mC, p));
   ++w->launches;
   return TF_OK;
 }
