@@ -1,0 +1,151 @@
+"""GPU: the multi-process world (one process per rank, CUDA-IPC symmetric heap,
+handles exchanged over torch.distributed) -- the path bench.py takes under
+torchrun on 8 GPUs -- exercised with 2 processes sharing the one GPU of the
+test box.  Both AG+GEMM schedules and fused Flash Decode must match the CPU
+oracle exactly as in the single-process world."""
+import ctypes as C
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ.setdefault("TILEFABRIC_WATCHDOG_SECS", "20")
+    import torch
+    import torch.distributed as dist
+    from paper_2511_02168_b200 import _abi
+    from paper_2511_02168_b200.dist import gather_ipc_handles, rank_pointer_table
+    from oracle.oracle import Oracle
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = {"rank": rank}
+    try:
+        O = Oracle()
+        L = _abi.lib()
+        h = C.c_void_p()
+        _abi.check(L.tf_world_create_ipc(rank, world, 0, 256 << 20, 0.0, C.byref(h)))
+        mine = (C.c_char * 64)()
+        _abi.check(L.tf_world_ipc_export(h, mine))
+        allh = gather_ipc_handles(dist, bytes(mine), world)
+        _abi.check(L.tf_world_ipc_import(h, (C.c_char * (64 * world)).from_buffer_copy(allh)))
+
+        # ---- AG+GEMM, fp32 exact path: bitwise vs reference::gemm ----
+        m, n, k = 24, 40, 64
+        a, b = O.ag_problem(3, m, n, k)
+        want = O.gemm(a, b)
+        kw = k // world
+        shards = (C.c_void_p * world)()
+        _abi.check(L.tf_heap_alloc(h, b"ag.a", m * kw * 4, shards))
+        shard = torch.from_numpy(np.ascontiguousarray(a[:, rank * kw:(rank + 1) * kw])).cuda()
+        _abi.check(L.tf_memcpy(h, shards[rank], shard.data_ptr(), shard.numel() * 4))
+        B = torch.from_numpy(b).cuda()
+        Cm = torch.zeros(m, n, device="cuda")
+        torch.cuda.synchronize()
+        dist.barrier()
+        shape = _abi.AgShape(m, n, k, 8, 8, 8, _abi.TF_F32)
+        res = {}
+        for name, var in (("pull", _abi.TF_AG_PULL), ("push", _abi.TF_AG_PUSH), ("baseline", _abi.TF_AG_BASELINE)):
+            Cm.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            _abi.check(L.tf_ag_gemm(h, var, C.byref(shape), shards,
+                                    _abi.ptr_array(rank_pointer_table(world, rank, B.data_ptr())),
+                                    _abi.ptr_array(rank_pointer_table(world, rank, Cm.data_ptr())), None, None))
+            res[name] = bool(np.array_equal(Cm.cpu().numpy().view(np.uint32), want.view(np.uint32)))
+            dist.barrier()
+        out["ag_f32"] = res
+
+        # ---- AG+GEMM, bf16 tensor-core path (pull + push) ----
+        m2, n2, k2 = 256, 512, 128 * world
+        a2, b2 = O.ag_problem(4, m2, n2, k2)
+        a2, _ = O.round_bf16(a2)
+        b2, _ = O.round_bf16(b2)
+        kw2 = k2 // world
+        sh2 = (C.c_void_p * world)()
+        _abi.check(L.tf_heap_alloc(h, b"ag.a.bf16", m2 * kw2 * 2, sh2))
+        s2 = torch.from_numpy(np.ascontiguousarray(a2[:, rank * kw2:(rank + 1) * kw2])).bfloat16().cuda()
+        _abi.check(L.tf_memcpy(h, sh2[rank], s2.data_ptr(), s2.numel() * 2))
+        B2 = torch.from_numpy(b2).bfloat16().cuda()
+        C2 = torch.zeros(m2, n2, device="cuda", dtype=torch.bfloat16)
+        ref2 = (torch.from_numpy(a2).double() @ torch.from_numpy(b2).double()).float().numpy()
+        torch.cuda.synchronize()
+        shape2 = _abi.AgShape(m2, n2, k2, 0, 0, 0, _abi.TF_BF16)
+        res2 = {}
+        for name, var in (("pull", _abi.TF_AG_PULL), ("push", _abi.TF_AG_PUSH)):
+            C2.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            _abi.check(L.tf_ag_gemm(h, var, C.byref(shape2), sh2,
+                                    _abi.ptr_array(rank_pointer_table(world, rank, B2.data_ptr())),
+                                    _abi.ptr_array(rank_pointer_table(world, rank, C2.data_ptr())), None, None))
+            c = C2.float().cpu().numpy()
+            res2[name] = float(np.abs(c - ref2).max() / np.abs(ref2).max())
+            dist.barrier()
+        out["ag_bf16_err"] = res2
+
+        # ---- Flash Decode, fused, fp32: every rank's output identical ----
+        qf, kf, vf, scale = O.fd_problem(5, 2, 8, 96)
+        want_fd = O.attention(qf, kf, vf, scale)
+        ln = 96 // world
+        qd = torch.from_numpy(qf).cuda()
+        kd = torch.from_numpy(np.ascontiguousarray(kf[:, rank * ln:(rank + 1) * ln])).cuda()
+        vd = torch.from_numpy(np.ascontiguousarray(vf[:, rank * ln:(rank + 1) * ln])).cuda()
+        od = torch.zeros(2, 8, device="cuda")
+        torch.cuda.synchronize()
+        dist.barrier()
+        fshape = _abi.FdShape(1, 2, 2, 8, 96, float(scale), _abi.TF_F32, _abi.TF_F32)
+        tbl = lambda p: _abi.ptr_array(rank_pointer_table(world, rank, p))  # noqa: E731
+        for variant in (_abi.TF_FD_FUSED, _abi.TF_FD_BSP, _abi.TF_FD_FINE_WAITS):
+            od.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            _abi.check(L.tf_flash_decode(h, variant, C.byref(fshape), tbl(qd.data_ptr()), tbl(kd.data_ptr()),
+                                         tbl(vd.data_ptr()), tbl(od.data_ptr()), None, None))
+            o = od.cpu().numpy()
+            out.setdefault("fd_err", []).append(O.head_rel_err(o, want_fd))
+            outs = [None] * world
+            dist.all_gather_object(outs, o.tobytes())
+            out.setdefault("fd_ranks_equal", []).append(all(x == outs[0] for x in outs))
+            dist.barrier()
+        L.tf_world_destroy(h)
+    except Exception as e:  # surface the failure to the parent
+        out["error"] = repr(e)
+    finally:
+        q.put(out)
+        dist.destroy_process_group()
+
+
+def test_two_process_ipc_world_on_one_gpu():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert "error" not in r, r
+        assert all(r["ag_f32"].values()), r
+        for name, err in r["ag_bf16_err"].items():
+            assert err <= 4e-3, (name, err)
+        assert all(e <= 1e-5 for e in r["fd_err"]), r
+        assert all(r["fd_ranks_equal"]), r
