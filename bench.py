@@ -86,7 +86,7 @@ class ClockSampler:
                                           0x100: "display_clocks"}.get(bit, names.get(bit, hex(bit))))
             except Exception:
                 pass
-            time.sleep(0.02)
+            time.sleep(0.005)
 
     def __enter__(self):
         if self.N:
@@ -284,6 +284,58 @@ def bench_ag_e2e(ctx, w, A_local, B, Cm, shard_ptrs, shape, variant, steps):
 
 
 # ---------------------------------------------------------------------------------
+# AG+GEMM M-sweep (BASELINE configs[4]: M 128..16384, K = N = 8192), secondary
+
+def bench_msweep(ctx, steps, warmup, Ms=(128, 256, 512, 1024, 2048, 4096, 8192, 16384)):
+    from paper_2511_02168_b200 import _abi
+    torch = ctx.torch
+    W = ctx.W
+    K = N = 8192
+    kw = K // W
+    Mmax = max(Ms)
+    w = ctx.world(Mmax * kw * 2 + 2 * 2 * Mmax * K * 2 + (64 << 20))
+    out = {}
+    try:
+        g = torch.Generator(device=ctx.dev).manual_seed(3 + ctx.rank)
+        shard_ptrs = w.alloc("ag.a.sweep", Mmax * kw * 2)
+        A = (torch.rand(Mmax, kw, device=ctx.dev, generator=g) * 2 - 1).bfloat16()
+        w.memcpy(shard_ptrs[ctx.rank], A.data_ptr(), A.numel() * 2)
+        B = (torch.rand(K, N, device=ctx.dev, generator=g) * 2 - 1).bfloat16()
+        Cm = torch.empty(Mmax, N, device=ctx.dev, dtype=torch.bfloat16)
+        gathered = torch.empty(W, Mmax, kw, device=ctx.dev, dtype=torch.bfloat16)
+        torch.cuda.synchronize()
+        for M in Ms:
+            shape = _abi.AgShape(M, N, K, 0, 0, 0, _abi.TF_BF16)
+            res = {}
+            for name, var in (("pull", _abi.TF_AG_PULL), ("push", _abi.TF_AG_PUSH)):
+                args = (w.handle, var, C.byref(shape), _abi.ptr_array(shard_ptrs),
+                        _abi.ptr_array(ptrs_for(ctx, B.data_ptr())), _abi.ptr_array(ptrs_for(ctx, Cm.data_ptr())),
+                        None, None)
+                res[name] = time_steps(ctx, w.stream(ctx.rank), lambda: _abi.check(w.lib.tf_ag_gemm_async(*args)),
+                                       steps, warmup) * 1e3
+                if W == 1:
+                    break  # nothing to exchange: pull == push
+            Am = A[:M]
+
+            def bsp():
+                if W > 1:
+                    ctx.dist.all_gather_into_tensor(gathered[:, :M], Am)
+                    a = gathered[:, :M].permute(1, 0, 2).reshape(M, K)
+                else:
+                    a = Am
+                torch.matmul(a, B, out=Cm[:M])
+
+            res["bsp"] = time_steps(ctx, torch.cuda.current_stream(), bsp, steps, warmup) * 1e3
+            best = min(v for k, v in res.items() if k != "bsp")
+            res["tflops"] = 2.0 * M * N * K / (best * 1e-6) / 1e12
+            res["fused_speedup_vs_bsp"] = res["bsp"] / best
+            out[str(M)] = {k: round(v, 3) for k, v in res.items()}
+        return out
+    finally:
+        w.close()
+
+
+# ---------------------------------------------------------------------------------
 # Flash Decode (secondary)
 
 def bench_fd(ctx, cfg, steps, warmup):
@@ -404,11 +456,12 @@ def ag_config(W):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-fd", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the config-5 M sweep")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
@@ -417,7 +470,9 @@ def main():
     ctx = Ctx(args.gpus)
     pk = peaks()
     ag_res = bench_ag(ctx, args.steps, args.warmup)
-    fd3 = fd4 = None
+    fd3 = fd4 = sweep = None
+    if not args.no_sweep:
+        sweep = bench_msweep(ctx, max(5, args.steps // 4), args.warmup)
     if not args.no_fd:
         fd3 = bench_fd(ctx, FD3, args.steps, args.warmup)
         fd4 = bench_fd(ctx, FD4, max(5, args.steps // 2), args.warmup)
@@ -462,6 +517,10 @@ def main():
                                       "frac": gbs / pk["hbm"], "algorithmic_bytes_per_launch": r["kv_bytes"]},
                          "head_rel_err_vs_torch_fp32": r["err"], "config": cfg}
         line["secondary"] = sec
+    if sweep:
+        line.setdefault("secondary", {})["ag_msweep_K8192_N8192"] = {
+            "what": "BASELINE configs[4] at this world size: latency us (fused pull/push vs BSP), TFLOP/s",
+            "points": sweep}
     print(json.dumps(line))
 
 

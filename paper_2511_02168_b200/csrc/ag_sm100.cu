@@ -88,6 +88,9 @@ struct AgTcParams {
   DevErr* err;
   int board;
   int dbg;  // TFB_DEBUG knobs: 1 skip C stores, 2 skip MMAs, 8 force CG=1 (profiling aids)
+  int ksplit;  // > 1: skinny-M split-K, fp32 partials [ksplit][M][N] via tmP, then reduce
+  int kbs;     // k-blocks per split
+  int Mp;      // M rounded up to 128: row pitch between splits in the workspace
   const __nv_bfloat16* peer_shard[64];
 };
 
@@ -201,7 +204,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ag_gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA_own,
                          const __grid_constant__ CUtensorMap tmA_inbox,
                          const __grid_constant__ CUtensorMap tmB,
-                         const __grid_constant__ CUtensorMap tmC, const AgTcParams p) {
+                         const __grid_constant__ CUtensorMap tmC,
+                         const __grid_constant__ CUtensorMap tmP, const AgTcParams p) {
   using K_ = Cfg<CG>;
   constexpr int STAGES = K_::STAGES, NH = K_::NH, CPH = K_::CPH;
   extern __shared__ uint8_t smem_raw[];
@@ -220,13 +224,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const bool leader = crank == 0;
   const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
   const int num_mt = (p.num_m + CG - 1) / CG;  // tile rows (BM * CG each)
-  const int num_tiles = num_mt * p.num_n;
+  // Work items: (tile, k-split).  Split ks covers k-block slots
+  // [ks*kbs, min((ks+1)*kbs, kb_total)) of the rank's rotated k order.
+  const int num_tiles = num_mt * p.num_n * p.ksplit;
+  auto item_coords = [&](int t, int& mt, int& nb, int& i0, int& i1) {
+    const int ks = t % p.ksplit;
+    tile_coords(num_mt, p.num_n, t / p.ksplit, mt, nb);
+    i0 = ks * p.kbs;
+    i1 = min(p.kb_total, i0 + p.kbs);
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA_own);
     tma_prefetch(&tmA_inbox);
     tma_prefetch(&tmB);
     tma_prefetch(&tmC);
+    tma_prefetch(&tmP);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], CG);  // one arrive per CTA of the pair (the leader's copy is used)
       mbar_init(&empty[s], 1);
@@ -250,12 +263,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cid; t < num_tiles; t += ncl) {
-        int mt, nb;
-        tile_coords(num_mt, p.num_n, t, mt, nb);
+        int mt, nb, i0, i1;
+        item_coords(t, mt, nb, i0, i1);
         const int mb = mt * CG + int(crank);  // this CTA's 128-row block
         const int m0 = mb * BM, n0 = nb * K_::BN_TILE;
         uint64_t ready_mask = 0;
-        for (int i = 0; i < p.kb_total; ++i) {
+        for (int i = i0; i < i1; ++i) {
           const int kb = p.own >= 0 ? (i + p.own * p.kbw) % p.kb_total : i;
           const int src = kb / p.kbw;
           mbar_wait(&empty[stage], phase ^ 1);
@@ -294,9 +307,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int acc = 0;
       uint32_t aphase = 0;
       for (int t = cid; t < num_tiles; t += ncl) {
+        int mt_, nb_, i0, i1;
+        item_coords(t, mt_, nb_, i0, i1);
         mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
-        for (int i = 0; i < p.kb_total; ++i) {
+        for (int i = i0; i < i1; ++i) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smA + stage * A_BYTES);
@@ -311,7 +326,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 // B: MN-major SW128, 64-column chunks 8 KB apart (LBO),
                 // 8-row K groups 1 KB apart (SBO); +16 rows (2 KB) per K=16.
                 const uint64_t bd = smem_desc_sw128(b_addr + h * CPH * (BK * 128) + k * 2048, BK * 128, 1024);
-                mma_issue<CG>(tmem_base + uint32_t((acc * NH + h) * 256), ad, bd, K_::IDESC, (i | k) != 0);
+                mma_issue<CG>(tmem_base + uint32_t((acc * NH + h) * 256), ad, bd, K_::IDESC,
+                              ((i - i0) | k) != 0);
               }
             }
           }
@@ -336,9 +352,47 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tempty_leader0 = CG == 2 ? mapa(&tempty[0], 0) : smem_u32(&tempty[0]);
     for (int t = cid; t < num_tiles; t += ncl) {
       int mt, nb;
-      tile_coords(num_mt, p.num_n, t, mt, nb);
+      int i0_, i1_;
+      item_coords(t, mt, nb, i0_, i1_);
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
+      if (p.ksplit > 1) {
+        // Split-K: this split's fp32 partial -> [ks][M][N] workspace, 32-col
+        // slabs (128-byte rows), same swizzled staging + TMA store.
+        const int ks = t % p.ksplit;
+        const int row0 = (mt * CG + int(crank)) * BM + 32 * q;
+        uint8_t* stg = smStage + q * (2 * 4096);
+#pragma unroll 1
+        for (int cc = 0; cc < NH * 8; ++cc) {
+          uint32_t r0[32];
+          tmem_ld_32x32b_x32(tmem_base + (uint32_t(32 * q) << 16) + uint32_t(acc * NH * 256 + 32 * cc), r0);
+          tmem_ld_wait();
+          uint8_t* buf = stg + (cc & 1) * 4096;
+          if (cc >= 2 && lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<uint4*>(buf + lane * 128 + ((j ^ (lane & 7)) * 16)) =
+                make_uint4(r0[4 * j], r0[4 * j + 1], r0[4 * j + 2], r0[4 * j + 3]);
+          fence_proxy_async_shared();
+          __syncwarp();
+          if (lane == 0 && row0 < p.M) {
+            tma_store_2d(&tmP, buf, nb * K_::BN_TILE + 32 * cc, ks * p.Mp + row0);
+            bulk_commit();
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (CG == 2) mbar_arrive_cluster(tempty_leader0 + uint32_t(acc) * 8);
+          else mbar_arrive(&tempty[acc]);
+        }
+        if (++acc == K_::ACC_BUFS) {
+          acc = 0;
+          aphase ^= 1;
+        }
+        continue;
+      }
       // 64-column slabs: two tcgen05.ld (32 columns each) -> bf16 -> a
       // SWIZZLE_128B smem box [32 rows][64 cols] (conflict-free: 16-byte
       // chunk j of row r sits at j ^ (r & 7)) -> one TMA store per warp per
@@ -506,6 +560,31 @@ __global__ void __launch_bounds__(256) ag_push_kernel(const PushParams p) {
   }
 }
 
+// Split-K reduce: C = bf16(sum_ks P[ks]) in ascending ks (deterministic), 8
+// consecutive columns per thread (two 16-byte loads per split, one store).
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ P,
+                                                            __nv_bfloat16* __restrict__ C, int M, int N,
+                                                            int Mp, int ksplit) {
+  const size_t vecs = size_t(M) * N / 8;
+  const size_t split_stride = size_t(Mp) * N;
+  for (size_t v = blockIdx.x * size_t(blockDim.x) + threadIdx.x; v < vecs; v += size_t(gridDim.x) * blockDim.x) {
+    const size_t e = v * 8;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int s = 0; s < ksplit; ++s) {
+      const float4 a = __ldcs(reinterpret_cast<const float4*>(P + s * split_stride + e));
+      const float4 b = __ldcs(reinterpret_cast<const float4*>(P + s * split_stride + e + 4));
+      acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+      acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+    }
+    uint4 o;
+    o.x = pack_bf16x2(acc[0], acc[1]);
+    o.y = pack_bf16x2(acc[2], acc[3]);
+    o.z = pack_bf16x2(acc[4], acc[5]);
+    o.w = pack_bf16x2(acc[6], acc[7]);
+    *reinterpret_cast<uint4*>(C + e) = o;
+  }
+}
+
 // ---- host ------------------------------------------------------------------------
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -540,14 +619,15 @@ CUtensorMapL2promotion l2_promotion() {
 // 2-D bf16 map: `inner` contiguous elements per row, `outer` rows, row pitch
 // `pitch_elems`; box {box_inner, box_outer}; 128-byte swizzle.
 tf_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
-                   uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer) {
+                   uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer, bool f32 = false) {
   EncodeFn enc = encode_fn();
   if (!enc) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {pitch_elems * 2};
+  cuuint64_t strides[1] = {pitch_elems * (f32 ? 4 : 2)};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+  CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(base), dims, strides, box,
                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
@@ -600,13 +680,35 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   const int bn_tile = CG == 2 ? Cfg<2>::BN_TILE : Cfg<1>::BN_TILE;
   p.num_n = int((sh.n + bn_tile - 1) / bn_tile);
   p.num_tiles = ((p.num_m + CG - 1) / CG) * p.num_n;
+  // Skinny M: too few tiles to occupy the SMs -> split K across CTAs (fp32
+  // partials, deterministic ascending reduce).  BASELINE config 5's low end.
+  p.ksplit = 1;
+  {
+    const unsigned busy = unsigned(p.num_tiles) * CG;
+    int ks = 1;
+    if (busy * 2 <= grid_cap) ks = int(std::min<unsigned>(grid_cap / busy, 16));
+    ks = std::min(ks, std::max(1, p.kb_total / 4));  // >= 4 k-blocks per split
+    if (const char* e = std::getenv("TFB_KSPLIT")) ks = std::max(1, std::atoi(e));
+    p.kbs = (p.kb_total + ks - 1) / ks;
+    p.ksplit = (p.kb_total + p.kbs - 1) / p.kbs;
+  }
+  p.Mp = int((sh.m + BM - 1) / BM * BM);
+  CUtensorMap mP = mC;
+  float* partial = nullptr;
+  if (p.ksplit > 1) {
+    size_t off;
+    const size_t bytes = size_t(p.ksplit) * p.Mp * sh.n * 4;
+    TFB_CHECK(heap_get(w, "ag.splitk[" + std::to_string(bytes) + "]", bytes, &off));
+    partial = reinterpret_cast<float*>(w->ptr(r, off));
+    TFB_CHECK(make_map(&mP, partial, sh.n, size_t(p.ksplit) * p.Mp, sh.n, 32, 32, /*f32=*/true));
+  }
   auto kern = CG == 2 ? ag_gemm_sm100_kernel<2> : ag_gemm_sm100_kernel<1>;
   const size_t smem = CG == 2 ? Cfg<2>::SMEM : Cfg<1>::SMEM;
   if (!attr_set[CG - 1][dev & 63]) {
     TFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr_set[CG - 1][dev & 63] = true;
   }
-  const unsigned pair_tiles = unsigned((p.num_m + CG - 1) / CG) * unsigned(p.num_n);
+  const unsigned pair_tiles = unsigned((p.num_m + CG - 1) / CG) * unsigned(p.num_n) * unsigned(p.ksplit);
   if (const char* e = std::getenv("TFB_GRID")) grid_cap = std::min(grid_cap, unsigned(std::atoi(e)));
   unsigned grid = std::min(pair_tiles * CG, grid_cap / CG * CG);
   grid = std::max(grid, unsigned(CG));
@@ -631,8 +733,16 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
       last_gm[dev & 63] = gm;
     }
   }
-  TFB_CUDA(cudaLaunchKernelEx(&cfg, kern, mOwn, mInbox, mB, mC, p));
+  TFB_CUDA(cudaLaunchKernelEx(&cfg, kern, mOwn, mInbox, mB, mC, mP, p));
   ++w->launches;
+  if (p.ksplit > 1) {
+    const size_t vecs = sh.m * sh.n / 8;
+    const unsigned blocks = unsigned(std::min<size_t>((vecs + 255) / 256, size_t(w->sm_count) * 16));
+    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(partial, static_cast<__nv_bfloat16*>(c), int(sh.m), int(sh.n),
+                                                 p.Mp, p.ksplit);
+    TFB_CUDA(cudaGetLastError());
+    ++w->launches;
+  }
   return TF_OK;
 }
 
@@ -667,8 +777,16 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
   TFB_CHECK(heap_get(w, "ag.inbox.bf16[" + std::to_string(m * k) + "]", 2 * m * k * 2, &inbox_off));
   TFB_CHECK(heap_get(w, "ag.ctr", 256, &ctr_off));
   BoardEntry rb;
-  TFB_CHECK(board_next_epoch(w, "ag.ready", num_m, W, &rb));
-  w->ag_flags = FlagSnapshot{w->board_names[rb.id], size_t(num_m) * W, rb.epoch};
+  // Only the signalling schedules (pull, push) advance the ready board's
+  // epoch; BASELINE never touches it (every rank/process must agree on e).
+  if (variant == TF_AG_BASELINE) {
+    const std::string bname = "ag.ready[" + std::to_string(num_m) + "x" + std::to_string(W) + "]";
+    TFB_CHECK(board_get(w, bname, num_m, W, &rb));
+    rb.epoch = w->boards[bname].epoch;
+  } else {
+    TFB_CHECK(board_next_epoch(w, "ag.ready", num_m, W, &rb));
+    w->ag_flags = FlagSnapshot{w->board_names[rb.id], size_t(num_m) * W, rb.epoch};
+  }
   const int parity = int(rb.epoch & 1);
   auto inbox_of = [&](int r) -> __nv_bfloat16* {
     if (gathered && gathered[r]) return static_cast<__nv_bfloat16*>(gathered[r]);

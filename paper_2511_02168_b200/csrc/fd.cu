@@ -786,8 +786,15 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   // W x 1 in the reference, flash_decode.hpp:357).
   const bool fused = variant == TF_FD_FUSED;
   BoardEntry fb;
-  TFB_CHECK(board_next_epoch(w, "fd.flags", W, fused ? G : 1, &fb));
-  w->fd_flags = FlagSnapshot{w->board_names[fb.id], size_t(W) * (fused ? G : 1), fb.epoch};
+  // Only schedules that signal advance the board's epoch: every rank (every
+  // process, in an IPC world) must agree on "run e waits for >= e".
+  if (variant == TF_FD_BSP) {
+    TFB_CHECK(board_get(w, "fd.flags[" + std::to_string(W) + "x1]", W, 1, &fb));
+    fb.epoch = w->boards["fd.flags[" + std::to_string(W) + "x1]"].epoch;
+  } else {
+    TFB_CHECK(board_next_epoch(w, "fd.flags", W, fused ? G : 1, &fb));
+    w->fd_flags = FlagSnapshot{w->board_names[fb.id], size_t(W) * (fused ? G : 1), fb.epoch};
+  }
   // Inbox / pubs / stage in the symmetric heap.  The internal inbox is
   // double-buffered by epoch parity: a fast peer's next push can never land
   // in the buffer a slow rank is still folding.

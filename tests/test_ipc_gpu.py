@@ -88,7 +88,8 @@ def _worker(rank, world, port, q):
         torch.cuda.synchronize()
         shape2 = _abi.AgShape(m2, n2, k2, 0, 0, 0, _abi.TF_BF16)
         res2 = {}
-        for name, var in (("pull", _abi.TF_AG_PULL), ("push", _abi.TF_AG_PUSH)):
+        for name, var in (("pull", _abi.TF_AG_PULL), ("baseline", _abi.TF_AG_BASELINE), ("push", _abi.TF_AG_PUSH),
+                          ("pull2", _abi.TF_AG_PULL)):
             C2.zero_()
             torch.cuda.synchronize()
             dist.barrier()
@@ -112,7 +113,8 @@ def _worker(rank, world, port, q):
         dist.barrier()
         fshape = _abi.FdShape(1, 2, 2, 8, 96, float(scale), _abi.TF_F32, _abi.TF_F32)
         tbl = lambda p: _abi.ptr_array(rank_pointer_table(world, rank, p))  # noqa: E731
-        for variant in (_abi.TF_FD_FUSED, _abi.TF_FD_BSP, _abi.TF_FD_FINE_WAITS):
+        for variant in (_abi.TF_FD_FUSED, _abi.TF_FD_BSP, _abi.TF_FD_FINE_WAITS, _abi.TF_FD_INDEPENDENT_AG,
+                        _abi.TF_FD_FUSED):
             od.zero_()
             torch.cuda.synchronize()
             dist.barrier()
@@ -143,7 +145,7 @@ def test_two_process_ipc_world_on_one_gpu():
     for p in procs:
         p.join(timeout=60)
     for r in res:
-        assert "error" not in r, r
+        assert "error" not in r, r.get("error")
         assert all(r["ag_f32"].values()), r
         for name, err in r["ag_bf16_err"].items():
             assert err <= 4e-3, (name, err)
