@@ -120,6 +120,12 @@ tf_status tf_wait_signal(tf_world* w, const char* board, int rank, int row,
                          int slot, uint64_t expected);
 tf_status tf_read_signal(tf_world* w, const char* board, int rank, int row,
                          int slot, uint64_t* value);
+/* World barrier on the device (RankCtx::barrier, fabric.hpp:574-584): every
+ * local rank's stream runs one barrier kernel.  only_rank >= 0 enters the
+ * barrier with that rank alone (the reference's mismatched-barrier
+ * diagnostic, acceptance_test.cpp:342-353): TF_ERR_DEADLOCK "barrier
+ * generation G: only X of W ranks arrived within the watchdog". */
+tf_status tf_world_barrier(tf_world* w, int only_rank);
 /* Signal-carries-data soak on the device (harness.hpp:146-195 analogue):
  * `rounds` producer/consumer handshakes between every ordered rank pair,
  * payload written before each release, checked after each acquire.

@@ -94,6 +94,7 @@ SIGNATURES = {
     "tf_wait_signal": (C.c_int, [_P, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_uint64]),
     "tf_read_signal": (C.c_int, [_P, C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
     "tf_signal_soak": (C.c_int, [_P, C.c_uint64, C.c_int, C.POINTER(C.c_uint64)]),
+    "tf_world_barrier": (C.c_int, [_P, C.c_int]),
     "tf_ag_gemm": (C.c_int, [_P, C.c_int, C.POINTER(AgShape), _PP, _PP, _PP, _PP, _PP]),
     "tf_ag_gemm_async": (C.c_int, [_P, C.c_int, C.POINTER(AgShape), _PP, _PP, _PP, _PP, _PP]),
     "tf_ag_flag_counts": (C.c_int, [_P, C.c_int, C.POINTER(C.c_uint64), C.c_size_t,

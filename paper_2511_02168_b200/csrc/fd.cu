@@ -267,38 +267,55 @@ __device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
   const int lane = threadIdx.x & 31;
   const int gq = lane >> 2, t = lane & 3;
   const float sl2 = P.scale * kLog2e;
-  // Q^T fragments: head gq, d positions 8(t+4i) .. +8.
-  uint4 qv[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) qv[i] = *reinterpret_cast<const uint4*>(Q + size_t(gq) * 128 + 8 * (t + 4 * i));
+  // Q^T fragments (head gq, d positions 8(t+4i) .. +8) are read from the
+  // CTA's smem copy of the group's q each tile: 16 registers the KV software
+  // pipeline needs more.
+  const uint4* sq = reinterpret_cast<const uint4*>(Q);
   float o[8][4];
 #pragma unroll
   for (int x = 0; x < 8; ++x) o[x][0] = o[x][1] = o[x][2] = o[x][3] = 0.0f;
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
   int badl = 0;
+  // Software pipeline without extra registers: tile j+1's K is loaded into
+  // the K registers right after tile j's QK product consumed them, and its V
+  // right after tile j's PV product, so one tile is always in flight while
+  // the current one computes.
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  uint4 k_a[4], k_b[4], v_a[4], v_b[4];
+  auto load_k = [&](size_t j0) {
+    const size_t ka = j0 + gq, kb8 = j0 + gq + 8;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      k_a[i] = ka < ke ? ldg_stream(K + ka * 128 + 8 * (t + 4 * i)) : z;
+      k_b[i] = kb8 < ke ? ldg_stream(K + kb8 * 128 + 8 * (t + 4 * i)) : z;
+    }
+  };
+  auto load_v = [&](size_t j0) {
+    const size_t ka = j0 + gq, kb8 = j0 + gq + 8;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v_a[i] = ka < ke ? ldg_stream(V + ka * 128 + 8 * (t + 4 * i)) : z;
+      v_b[i] = kb8 < ke ? ldg_stream(V + kb8 * 128 + 8 * (t + 4 * i)) : z;
+    }
+  };
+  if (kb < ke) {
+    load_k(kb);
+    load_v(kb);
+  }
   for (size_t j0 = kb; j0 < ke; j0 += 16) {
     const size_t ka = j0 + gq, kb8 = j0 + gq + 8;
     const bool va = ka < ke, vb = kb8 < ke;
-    uint4 k_a[4], k_b[4], v_a[4], v_b[4];
-    const uint4 z = make_uint4(0, 0, 0, 0);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      k_a[i] = va ? ldg_stream(K + ka * 128 + 8 * (t + 4 * i)) : z;
-      k_b[i] = vb ? ldg_stream(K + kb8 * 128 + 8 * (t + 4 * i)) : z;
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      v_a[i] = va ? ldg_stream(V + ka * 128 + 8 * (t + 4 * i)) : z;
-      v_b[i] = vb ? ldg_stream(V + kb8 * 128 + 8 * (t + 4 * i)) : z;
-    }
     // S^T = K . Q^T over 8 k-steps of 16 d.
     float s[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int st = 0; st < 8; ++st) {
-      const int i = st >> 1, h = st & 1;
-      mma_bf16(s, w4(k_a[i], 2 * h), w4(k_b[i], 2 * h), w4(k_a[i], 2 * h + 1),
-               w4(k_b[i], 2 * h + 1), w4(qv[i], 2 * h), w4(qv[i], 2 * h + 1));
+    for (int i = 0; i < 4; ++i) {
+      const uint4 qv = sq[gq * 16 + t + 4 * i];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        mma_bf16(s, w4(k_a[i], 2 * h), w4(k_b[i], 2 * h), w4(k_a[i], 2 * h + 1),
+                 w4(k_b[i], 2 * h + 1), w4(qv, 2 * h), w4(qv, 2 * h + 1));
     }
+    load_k(j0 + 16);  // next tile's K (masked past the range)
     // log2-domain scores; rows g (key ka) and g+8 (key kb8); cols 2t, 2t+1.
     float x0 = va ? s[0] * sl2 : -INFINITY, x1 = va ? s[1] * sl2 : -INFINITY;
     float x2 = vb ? s[2] * sl2 : -INFINITY, x3 = vb ? s[3] * sl2 : -INFINITY;
@@ -341,6 +358,7 @@ __device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
         mma_bf16(o[2 * i + jp], a0, a1, a2, a3, pb0, pb1);
       }
     }
+    load_v(j0 + 16);  // next tile's V
   }
   // Per-head normalizer: sum the per-lane partials over the 8 key rows.
 #pragma unroll
@@ -373,6 +391,7 @@ struct FastSmem {
   float m[kFastWarps][8];
   float l[kFastWarps][8];
   float o[kFastWarps][8 * 128];
+  uint4 q[8 * 16];  // the group's 8 q heads x 128 d (bf16), fragment-ordered reads
   int bad;
 };
 
@@ -389,8 +408,10 @@ __device__ void fast_split(const FdParams& P, int lr, int g, int sp, float* wsro
   const __nv_bfloat16* V = static_cast<const __nv_bfloat16*>(R.v) + (size_t(b) * P.Hkv + kvh) * P.len * 128;
   const __nv_bfloat16* Q = static_cast<const __nv_bfloat16*>(R.q) + (size_t(b) * P.Hq + kvh * 8) * 128;
   if (threadIdx.x == 0) sm.bad = 0;
+  for (int i = threadIdx.x; i < 8 * 16; i += blockDim.x) sm.q[i] = reinterpret_cast<const uint4*>(Q)[i];
   __syncthreads();
-  fast_warp_range(P, K, V, Q, wb, we, sm.m[warp], sm.l[warp], sm.o[warp], &sm.bad);
+  fast_warp_range(P, K, V, reinterpret_cast<const __nv_bfloat16*>(sm.q), wb, we, sm.m[warp], sm.l[warp],
+                  sm.o[warp], &sm.bad);
   __syncthreads();
   if (sm.bad) {
     if (threadIdx.x == 0)

@@ -266,7 +266,7 @@ __global__ void soak_kernel(uint32_t* const* mail, uint64_t* const* flags,
   }
 }
 
-tf_status world_barrier(World* w, const std::vector<cudaStream_t>& streams) {
+tf_status world_barrier(World* w, const std::vector<cudaStream_t>& streams, int only_rank) {
   BoardEntry b;
   TFB_CHECK(board_get(w, "tf.barrier", 1, 1, &b));
   const uint64_t epoch = ++w->barrier_epoch;
@@ -275,7 +275,7 @@ tf_status world_barrier(World* w, const std::vector<cudaStream_t>& streams) {
   size_t off;
   TFB_CHECK(heap_get(w, "tf.barrier.table", sizeof(uint64_t*) * 64, &off));
   for (int r = 0; r < w->W; ++r) {
-    if (!w->ranks[r].local) continue;
+    if (!w->ranks[r].local || (only_rank >= 0 && r != only_rank)) continue;
     cudaSetDevice(w->ranks[r].device);
     uint64_t** table = reinterpret_cast<uint64_t**>(w->ptr(r, off));
     TFB_CUDA(cudaMemcpyAsync(table, cells.data(), sizeof(uint64_t*) * w->W,
@@ -672,6 +672,33 @@ tf_status tf_signal_soak(tf_world* tw, uint64_t seed, int rounds, uint64_t* viol
   }
   *violations = total;
   return TF_OK;
+}
+
+tf_status tf_world_barrier(tf_world* tw, int only_rank) {
+  if (!tw) return set_error(TF_ERR_CONFIG, "NULL world");
+  World* w = &tw->impl;
+  if (only_rank >= w->W) return set_error(TF_ERR_BOUNDS, "tf_world_barrier: rank out of range");
+  auto streams = resolve_streams(w, nullptr);
+  TFB_CHECK(world_barrier(w, streams, only_rank));
+  tf_status s = sync_and_check(w, streams);
+  if (s != TF_OK && only_rank >= 0) {
+    const std::string msg = tf_last_error();
+    // The lone waiter gave up; re-align the barrier counters so the world
+    // stays usable: the missing ranks' arrivals are added on their behalf.
+    BoardEntry b;
+    board_get(w, "tf.barrier", 1, 1, &b);
+    for (int r = 0; r < w->W; ++r) {
+      if (r == only_rank || !w->ranks[r].local) continue;
+      for (int q = 0; q < w->W; ++q) {
+        uint64_t* cell = reinterpret_cast<uint64_t*>(w->ptr(q, b.offset));
+        cudaSetDevice(w->ranks[r].device);
+        signal_kernel<<<1, 1, 0, streams[r]>>>(cell);
+      }
+    }
+    sync_and_check(w, streams);
+    set_error(s, msg);
+  }
+  return s;
 }
 
 tf_status tf_world_sync(tf_world* tw) {

@@ -103,7 +103,7 @@ tf_status board_next_epoch(World* w, const std::string& base, int rows, int slot
 // Device-side world barrier over every rank (fabric.hpp:574-584): one tiny
 // kernel per local rank, red.release.sys onto every rank's barrier cell,
 // then an acquire spin on its own.
-tf_status world_barrier(World* w, const std::vector<cudaStream_t>& streams);
+tf_status world_barrier(World* w, const std::vector<cudaStream_t>& streams, int only_rank = -1);
 // Resolve caller streams (NULL -> world streams).
 std::vector<cudaStream_t> resolve_streams(World* w, void* const* streams);
 // Wait for local streams and turn the device error record into a status.

@@ -134,6 +134,10 @@ class World:
         _abi.check(self.lib.tf_read_signal(self.handle, board.encode(), rank, row, slot, C.byref(v)))
         return v.value
 
+    def barrier(self, only_rank: int = -1) -> None:
+        """RankCtx::barrier on the device; only_rank >= 0 enters it alone."""
+        _abi.check(self.lib.tf_world_barrier(self.handle, only_rank))
+
     def soak(self, seed: int, rounds: int) -> int:
         v = C.c_uint64()
         _abi.check(self.lib.tf_signal_soak(self.handle, seed, rounds, C.byref(v)))

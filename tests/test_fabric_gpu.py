@@ -69,3 +69,26 @@ def test_signal_carries_data_soak():
         for seed in range(1, 11):
             total += w.soak(seed, 100)
         assert total == 0
+
+
+def test_device_barrier_and_mismatch_diagnostic():
+    # acceptance_test.cpp:342-353: the lone waiter names the generation and
+    # "1 of 2"; the world stays usable afterwards.
+    with world(2, watchdog=0.2) as w:
+        w.barrier()
+        w.barrier()
+        with pytest.raises(tf.DeadlockError) as e:
+            w.barrier(only_rank=0)
+        msg = str(e.value)
+        assert "barrier generation" in msg and "1 of 2" in msg, msg
+        w.barrier()  # re-aligned
+
+
+def test_watchdog_is_configurable_and_bounded():
+    import time
+    with world(2, watchdog=0.1) as w:
+        w.board("t.never", 1, 1)
+        t0 = time.time()
+        with pytest.raises(tf.DeadlockError):
+            w.wait_signal("t.never", 1, 0, 0, 5)
+        assert time.time() - t0 < 5.0

@@ -116,3 +116,44 @@ def test_rejects_bad_shapes():
     p = tf.fd.make_problem(1, 2, 4, 64)
     with pytest.raises(tf.ConfigError):
         tf.fd.run_fused(p, tf.WorldConfig(world_size=3))
+
+
+def test_edge_shapes(oracle):
+    # One key per rank; a single head; tiny head_dim (acceptance grid's corners).
+    for (h, d, kv, w) in ((1, 4, 4, 4), (1, 4, 8, 8), (3, 5, 12, 2), (2, 256, 64, 2)):
+        p = tf.fd.make_problem(11 + h + d, h, d, kv)
+        want = oracle.attention(p.q[0], p.k[0], p.v[0], p.scale)
+        for variant in ALL:
+            run = tf.fd.run_fd(p, variant, tf.WorldConfig(world_size=w))
+            assert oracle.head_rel_err(run.out[0], want) <= 1e-5, (h, d, kv, w, variant)
+
+
+def test_non_finite_score_raises_numeric_error():
+    # tilemath_test.cpp:183-190: a non-finite score is a NumericError that
+    # names the head and the position.
+    p = tf.fd.make_problem(2, 2, 4, 16)
+    p.q = p.q.copy()
+    p.q[0, 1, 0] = np.inf
+    with pytest.raises(tf.NumericError) as e:
+        tf.fd.run_fused(p, tf.WorldConfig(world_size=2))
+    assert "head 1" in str(e.value)
+
+
+def test_gqa_bf16_eight_rank_loopback(oracle):
+    # Config-3 geometry (8 q heads per KV head, d=128) in an 8-rank world.
+    B, Hq, Hkv, d, L = 1, 16, 2, 128, 8 * 512
+    rng = np.random.default_rng(8)
+    qb, _ = oracle.round_bf16(rng.uniform(-1, 1, (B, Hq, d)).astype(np.float32))
+    kb, _ = oracle.round_bf16(rng.uniform(-1, 1, (B, Hkv, L, d)).astype(np.float32))
+    vb, _ = oracle.round_bf16(rng.uniform(-1, 1, (B, Hkv, L, d)).astype(np.float32))
+    p = tf.fd.DecodeProblem(Hq, d, L, float(1 / np.sqrt(np.float32(d))), qb, kb, vb, batch=B, kv_heads=Hkv)
+    gs = Hq // Hkv
+    want = np.concatenate([oracle.attention(np.ascontiguousarray(qb[0, g * gs:(g + 1) * gs]),
+                                            np.repeat(kb[0, g:g + 1], gs, 0), np.repeat(vb[0, g:g + 1], gs, 0),
+                                            p.scale) for g in range(Hkv)])
+    run = tf.fd.run_fused(p, tf.WorldConfig(world_size=8), dtype=1, out_dtype=0)
+    assert oracle.head_rel_err(run.out[0], want) <= 2e-3
+    for out in run.out[1:]:
+        assert np.array_equal(out.view(np.uint32), run.out[0].view(np.uint32))
+    for counts in run.flag_counts:
+        assert counts == [1] * 8
