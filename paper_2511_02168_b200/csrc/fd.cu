@@ -276,10 +276,6 @@ __device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
   for (int x = 0; x < 8; ++x) o[x][0] = o[x][1] = o[x][2] = o[x][3] = 0.0f;
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
   int badl = 0;
-  // Software pipeline without extra registers: tile j+1's K is loaded into
-  // the K registers right after tile j's QK product consumed them, and its V
-  // right after tile j's PV product, so one tile is always in flight while
-  // the current one computes.
   const uint4 z = make_uint4(0, 0, 0, 0);
   uint4 k_a[4], k_b[4], v_a[4], v_b[4];
   auto load_k = [&](size_t j0) {
@@ -298,13 +294,14 @@ __device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
       v_b[i] = kb8 < ke ? ldg_stream(V + kb8 * 128 + 8 * (t + 4 * i)) : z;
     }
   };
-  if (kb < ke) {
-    load_k(kb);
-    load_v(kb);
-  }
+  // (A one-tile-ahead register pipeline was measured: it spills at the
+  //  128-register budget 16 warps/SM need and lost 10 %; the loads are issued
+  //  at the top of each tile instead and the 16 resident warps overlap them.)
   for (size_t j0 = kb; j0 < ke; j0 += 16) {
     const size_t ka = j0 + gq, kb8 = j0 + gq + 8;
     const bool va = ka < ke, vb = kb8 < ke;
+    load_k(j0);
+    load_v(j0);
     // S^T = K . Q^T over 8 k-steps of 16 d.
     float s[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -315,7 +312,6 @@ __device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
         mma_bf16(s, w4(k_a[i], 2 * h), w4(k_b[i], 2 * h), w4(k_a[i], 2 * h + 1),
                  w4(k_b[i], 2 * h + 1), w4(qv, 2 * h), w4(qv, 2 * h + 1));
     }
-    load_k(j0 + 16);  // next tile's K (masked past the range)
     // log2-domain scores; rows g (key ka) and g+8 (key kb8); cols 2t, 2t+1.
     float x0 = va ? s[0] * sl2 : -INFINITY, x1 = va ? s[1] * sl2 : -INFINITY;
     float x2 = vb ? s[2] * sl2 : -INFINITY, x3 = vb ? s[3] * sl2 : -INFINITY;
@@ -358,7 +354,6 @@ __device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
         mma_bf16(o[2 * i + jp], a0, a1, a2, a3, pb0, pb1);
       }
     }
-    load_v(j0 + 16);  // next tile's V
   }
   // Per-head normalizer: sum the per-lane partials over the 8 key rows.
 #pragma unroll
