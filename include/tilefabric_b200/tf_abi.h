@@ -226,6 +226,22 @@ tf_status tf_world_sync(tf_world* w);
  * gpu_launches evidence). */
 uint64_t tf_launch_count(const tf_world* w);
 
+/* The Three Taxes measured on the device (taxmeter.hpp:45-63):
+ * kernel launches (launch tax), acquire waits on signal boards and their
+ * spin time (wait_idle), device-barrier waits and their time (bulk-sync
+ * tax), bytes stored into staging/inbox tensors (staged_bytes, the
+ * inter-kernel locality proxy).  Wait counters are accumulated per device by
+ * every spinning thread (%globaltimer); in a loopback world all ranks share
+ * one device's counters.  tf_tax_reset zeroes them. */
+typedef struct {
+  uint64_t launches;
+  uint64_t signal_waits, wait_idle_ns;
+  uint64_t barrier_waits, bulk_sync_ns;
+  uint64_t staged_bytes;
+} tf_taxes;
+tf_status tf_tax_report(tf_world* w, int rank, tf_taxes* out);
+tf_status tf_tax_reset(tf_world* w);
+
 #ifdef __cplusplus
 }
 #endif

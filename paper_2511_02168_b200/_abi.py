@@ -73,6 +73,15 @@ class FdShape(C.Structure):
                 ("kv_dtype", C.c_int), ("out_dtype", C.c_int)]
 
 
+class Taxes(C.Structure):
+    """tf_taxes: the Three Taxes measured on the device (taxmeter.hpp:45-63)."""
+    _fields_ = [("launches", C.c_uint64), ("signal_waits", C.c_uint64), ("wait_idle_ns", C.c_uint64),
+                ("barrier_waits", C.c_uint64), ("bulk_sync_ns", C.c_uint64), ("staged_bytes", C.c_uint64)]
+
+    def as_dict(self):
+        return {f: int(getattr(self, f)) for f, _ in self._fields_}
+
+
 # name -> (restype, argtypes); every symbol tf_abi.h declares.
 _P = C.c_void_p
 _PP = C.POINTER(C.c_void_p)
@@ -111,6 +120,8 @@ SIGNATURES = {
     "tf_uniform_reals": (C.c_int, [C.c_uint64, C.c_size_t, C.POINTER(C.c_float)]),
     "tf_world_sync": (C.c_int, [_P]),
     "tf_launch_count": (C.c_uint64, [_P]),
+    "tf_tax_report": (C.c_int, [_P, C.c_int, C.POINTER(Taxes)]),
+    "tf_tax_reset": (C.c_int, [_P]),
 }
 
 _lib = None

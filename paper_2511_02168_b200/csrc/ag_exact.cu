@@ -171,6 +171,9 @@ tf_status ag_exact_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh,
       if (!(gathered && gathered[r])) stage[r] = reinterpret_cast<float*>(w->ptr(r, stage_off));
   }
 
+  for (int r = 0; r < W; ++r)
+    if (w->ranks[r].local) w->stage(r, sizeof(float) * m * k);  // the gathered copy lands in HBM
+
   if (variant == TF_AG_BASELINE) {
     TFB_CHECK(world_barrier(w, streams));  // "ag.sync"
     for (int r = 0; r < W; ++r) {

@@ -794,6 +794,10 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
   };
   auto ready_of = [&](int r) { return reinterpret_cast<uint64_t*>(w->ptr(r, rb.offset)); };
   auto ctr_of = [&](int r, int slot) { return reinterpret_cast<unsigned int*>(w->ptr(r, ctr_off)) + slot * 4; };
+  // Every schedule lands the gathered operand in HBM once per rank (PULL via
+  // the gather warps; the reference's pull re-fetches tiles instead).
+  for (int r = 0; r < W; ++r)
+    if (w->ranks[r].local) w->stage(r, m * k * 2);
 
   if (variant == TF_AG_BASELINE) {
     TFB_CHECK(world_barrier(w, streams));

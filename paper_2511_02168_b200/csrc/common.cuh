@@ -24,6 +24,9 @@ struct DevErr {
   uint64_t expected;
   uint64_t observed;
   uint64_t aux;   // numeric: flat (head, position); barrier: generation
+  // Three-Tax meter (taxmeter.hpp:45-63 on the device): every acquire wait
+  // adds its spin time; barrier waits are kept apart (bulk-sync tax).
+  unsigned long long waits, wait_ns, barriers, barrier_ns;
 };
 
 enum : int { kWaitSignal = 0, kWaitBarrier = 1, kNumeric = 2, kEmpty = 3 };
@@ -97,23 +100,36 @@ static __device__ __noinline__ bool wait_geq(const uint64_t* cell, uint64_t expe
                                       uint64_t watchdog_ns, DevErr* err, int kind,
                                       int rank, int board, int row, int slot,
                                       uint64_t aux) {
+  const bool barrier = kind == kWaitBarrier;
   uint64_t seen = ld_acquire_sys(cell);
-  if (seen >= expected) return true;
+  if (seen >= expected) {
+    atomicAdd(barrier ? &err->barriers : &err->waits, 1ull);
+    return true;
+  }
   const uint64_t t0 = globaltimer_ns();
   unsigned ns = 32;
+  bool ok = true;
   for (uint32_t polls = 1;; ++polls) {
     seen = ld_acquire_sys(cell);
-    if (seen >= expected) return true;
+    if (seen >= expected) break;
     if ((polls & 255u) == 0) {
-      if (err_raised(err)) return false;
+      if (err_raised(err)) {
+        ok = false;
+        break;
+      }
       if (globaltimer_ns() - t0 > watchdog_ns) {
         raise_err(err, TF_ERR_DEADLOCK, kind, rank, board, row, slot, expected, seen, aux);
-        return false;
+        ok = false;
+        break;
       }
     }
     __nanosleep(ns);
     if (ns < 1024) ns <<= 1;
   }
+  const unsigned long long dt = globaltimer_ns() - t0;
+  atomicAdd(barrier ? &err->barriers : &err->waits, 1ull);
+  atomicAdd(barrier ? &err->barrier_ns : &err->wait_ns, dt);
+  return ok;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {

@@ -912,6 +912,10 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
     return TF_OK;
   };
 
+  // Every schedule lands W wire rows per rank in an inbox / stage
+  // (flash_decode_test.cpp:167-196: W*W*wire*4 bytes world-wide).
+  for (int r = 0; r < W; ++r)
+    if (w->ranks[r].local) w->stage(r, sizeof(float) * W * row_floats);
   if (fused) return launch_attention(/*push=*/1, /*fold_inline=*/1);
   TFB_CHECK(launch_attention(0, 0));
   TFB_CHECK(world_barrier(w, st));

@@ -167,7 +167,7 @@ tf_status check_record(World* w) {
   }
   for (auto& kv : w->errs) {
     cudaSetDevice(kv.first);
-    cudaMemset(kv.second, 0, sizeof(DevErr));
+    cudaMemset(kv.second, 0, offsetof(DevErr, waits));  // keep the tax counters
   }
   return set_error(static_cast<tf_status>(code == -1 ? TF_ERR_WORLD : code), msg);
 }
@@ -699,6 +699,37 @@ tf_status tf_world_barrier(tf_world* tw, int only_rank) {
     set_error(s, msg);
   }
   return s;
+}
+
+tf_status tf_tax_report(tf_world* tw, int rank, tf_taxes* out) {
+  if (!tw || !out) return set_error(TF_ERR_CONFIG, "tf_tax_report: NULL argument");
+  World* w = &tw->impl;
+  if (rank < 0 || rank >= w->W || !w->ranks[rank].local)
+    return set_error(TF_ERR_BOUNDS, "tf_tax_report: rank " + std::to_string(rank) + " is not local");
+  DevErr rec{};
+  cudaSetDevice(w->ranks[rank].device);
+  TFB_CUDA(cudaMemcpy(&rec, w->err_of(rank), sizeof(DevErr), cudaMemcpyDeviceToHost));
+  out->launches = w->launches - w->tax_launch_base;
+  out->signal_waits = rec.waits;
+  out->wait_idle_ns = rec.wait_ns;
+  out->barrier_waits = rec.barriers;
+  out->bulk_sync_ns = rec.barrier_ns;
+  out->staged_bytes = w->staged_bytes.empty() ? 0 : w->staged_bytes[rank];
+  return TF_OK;
+}
+
+tf_status tf_tax_reset(tf_world* tw) {
+  if (!tw) return set_error(TF_ERR_CONFIG, "NULL world");
+  World* w = &tw->impl;
+  TFB_CHECK(sync_and_check(w, resolve_streams(w, nullptr)));
+  for (auto& kv : w->errs) {
+    TFB_CUDA(cudaSetDevice(kv.first));
+    TFB_CUDA(cudaMemset(reinterpret_cast<char*>(kv.second) + offsetof(DevErr, waits), 0,
+                        sizeof(DevErr) - offsetof(DevErr, waits)));
+  }
+  w->tax_launch_base = w->launches;
+  std::fill(w->staged_bytes.begin(), w->staged_bytes.end(), 0);
+  return TF_OK;
 }
 
 tf_status tf_world_sync(tf_world* tw) {

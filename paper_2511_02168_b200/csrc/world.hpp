@@ -63,6 +63,12 @@ struct World {
   // from spinning kernels; the host reads them after a sync.
   std::map<int, DevErr*> errs;
   uint64_t launches = 0;
+  uint64_t tax_launch_base = 0;        // tf_tax_reset point
+  std::vector<uint64_t> staged_bytes;  // per rank: bytes landed in staging/inbox tensors
+  void stage(int r, uint64_t bytes) {
+    if (staged_bytes.size() != size_t(W)) staged_bytes.assign(W, 0);
+    staged_bytes[r] += bytes;
+  }
   uint64_t barrier_epoch = 0;
   uint64_t ag_epoch = 0;
   uint64_t fd_epoch = 0;

@@ -134,6 +134,15 @@ class World:
         _abi.check(self.lib.tf_read_signal(self.handle, board.encode(), rank, row, slot, C.byref(v)))
         return v.value
 
+    def taxes(self, rank: int = 0) -> dict:
+        """The Three Taxes measured on the device (tf_tax_report)."""
+        t = _abi.Taxes()
+        _abi.check(self.lib.tf_tax_report(self.handle, rank, C.byref(t)))
+        return t.as_dict()
+
+    def tax_reset(self) -> None:
+        _abi.check(self.lib.tf_tax_reset(self.handle))
+
     def barrier(self, only_rank: int = -1) -> None:
         """RankCtx::barrier on the device; only_rank >= 0 enters it alone."""
         _abi.check(self.lib.tf_world_barrier(self.handle, only_rank))
@@ -193,6 +202,7 @@ class ag:  # namespace tilefabric::ag
         flag_counts: List[List[int]]
         gathered: List[np.ndarray]
         launches: int
+        taxes: list = None  # per rank: tf_taxes (the Three Taxes, measured on the device)
 
     @staticmethod
     def make_problem(seed: int, m: int, n: int, k: int, tiles: Optional[TileSpec] = None):
@@ -232,6 +242,7 @@ class ag:  # namespace tilefabric::ag
                 _abi.ptr_array([c.data_ptr() for c in bufs_c]),
                 _abi.ptr_array(gathered) if variant != _abi.TF_AG_PULL else None, None))
             launches = w.launches() - before
+            taxes = [w.taxes(r) for r in range(W)]
             cs = [c.float().cpu().numpy() for c in bufs_c]
             gath = []
             if variant != _abi.TF_AG_PULL:
@@ -247,7 +258,7 @@ class ag:  # namespace tilefabric::ag
                     buf = (C.c_uint64 * max(1, cnt.value))()
                     _abi.check(w.lib.tf_ag_flag_counts(w.handle, r, buf, cnt.value, C.byref(cnt)))
                     flags.append([int(x) for x in buf[: cnt.value]])
-            return ag.AgGemmRun(cs, flags, gath, launches)
+            return ag.AgGemmRun(cs, flags, gath, launches, taxes)
 
     @staticmethod
     def run_baseline(p, cfg, dtype=_abi.TF_F32):
@@ -317,6 +328,7 @@ class fd:  # namespace tilefabric::fd
         flag_counts: List[List[int]]
         inbox: List[np.ndarray]
         launches: int
+        taxes: list = None  # per rank: tf_taxes (the Three Taxes, measured on the device)
 
     @staticmethod
     def make_problem(seed: int, heads: int, head_dim: int, kv_len: int):
@@ -369,6 +381,7 @@ class fd:  # namespace tilefabric::fd
                 _abi.ptr_array([t.data_ptr() for t in vs]), _abi.ptr_array([t.data_ptr() for t in outs]),
                 _abi.ptr_array(inbox), None))
             launches = w.launches() - before
+            taxes = [w.taxes(r) for r in range(W)]
             out = [o.float().cpu().numpy().reshape(B * H, d) if B > 1 else
                    o.float().cpu().numpy().reshape(H, d) for o in outs]
             boxes = [w.get(inbox[r], (W, B, H, d + 2), np.float32) for r in range(W)]
@@ -379,7 +392,7 @@ class fd:  # namespace tilefabric::fd
                     cnt = C.c_size_t()
                     _abi.check(w.lib.tf_fd_flag_counts(w.handle, r, buf, W, C.byref(cnt)))
                     flags.append([int(x) for x in buf[: cnt.value]])
-            return fd.FdRun(out, flags, boxes, launches)
+            return fd.FdRun(out, flags, boxes, launches, taxes)
 
     @staticmethod
     def run_bsp(p, cfg, **kw):

@@ -86,3 +86,18 @@ def test_rejects_non_divisible_k():
     p = tf.ag.make_problem(5, 4, 4, 10)
     with pytest.raises(tf.ConfigError):
         tf.ag.run_pull(p, tf.WorldConfig(world_size=4))
+
+
+def test_three_taxes_structure():
+    # ag_gemm_test.cpp:101-143 on the GPU: pull needs no barrier, baseline
+    # two per rank; push and baseline stage the gathered M x K operand.
+    w = 4
+    p = tf.ag.make_problem(12, 8, 8, 16)
+    pull = tf.ag.run_pull(p, tf.WorldConfig(world_size=w))
+    push = tf.ag.run_push(p, tf.WorldConfig(world_size=w))
+    base = tf.ag.run_baseline(p, tf.WorldConfig(world_size=w))
+    assert pull.taxes[0]["barrier_waits"] == 0 and pull.taxes[0]["staged_bytes"] == 0
+    assert push.taxes[0]["barrier_waits"] == 0
+    assert base.taxes[0]["barrier_waits"] == 2 * w
+    for t in push.taxes + base.taxes:
+        assert t["staged_bytes"] == p.m * p.k * 4

@@ -157,3 +157,21 @@ def test_gqa_bf16_eight_rank_loopback(oracle):
         assert np.array_equal(out.view(np.uint32), run.out[0].view(np.uint32))
     for counts in run.flag_counts:
         assert counts == [1] * 8
+
+
+def test_three_taxes_measured_on_device():
+    # flash_decode_test.cpp:136-196 on the GPU: fused pays no bulk-sync tax
+    # (no barrier waits), BSP two barriers per rank; every rank stages W wire
+    # rows (W*W*wire*4 bytes world-wide).
+    w = 4
+    p = tf.fd.make_problem(3, 2, 8, 64)
+    wire_bytes = p.heads * (p.head_dim + 2) * 4
+    fused = tf.fd.run_fused(p, tf.WorldConfig(world_size=w))
+    bsp = tf.fd.run_bsp(p, tf.WorldConfig(world_size=w))
+    assert fused.taxes[0]["barrier_waits"] == 0
+    assert fused.launches == 1
+    # loopback: the W ranks share one device's counters
+    assert bsp.taxes[0]["barrier_waits"] == 2 * w
+    for t in fused.taxes + bsp.taxes:
+        assert t["staged_bytes"] == w * wire_bytes
+    assert fused.taxes[0]["signal_waits"] >= w  # one fold wait per source (per group)
