@@ -16,7 +16,7 @@
 //   warp 1      MMA issuer (one thread): tcgen05.mma.kind::f16, fp32
 //               accumulators in TMEM; tcgen05.commit releases smem stages.
 //   warps 2-5   epilogue: tcgen05.ld 32x32b -> bf16 -> global C.
-//   warps 6-7   gather (PULL): claim (m_blk, src) chunks from a global
+//   warps 6-9   gather (PULL): claim (m_blk, src) chunks from a global
 //               counter, copy them from the owner's shard over NVLink
 //               (128-bit peer loads) into the local inbox at column src*kw,
 //               then release ready[m_blk][src].  Each remote A byte crosses
@@ -55,7 +55,8 @@ using namespace sm100;
 
 constexpr int BM = 128, BK = 64;  // BM: A rows staged per CTA
 constexpr int GROUP_M = 16;       // tile-rows per raster group (L2 reuse of B)
-constexpr int NUM_THREADS = 256;
+constexpr int NUM_THREADS = 320;    // 6 role warps + 4 gather warps
+constexpr int GATHER_T = NUM_THREADS - 192;  // gather threads (PULL)
 constexpr int TMEM_COLS = 512;
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 
@@ -440,15 +441,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) bulk_wait_all();  // C stores complete before the CTA retires
   } else if (p.gather) {
     // ===== gather (PULL): peer shard chunks -> local inbox + ready flags =====
-    const int gt = threadIdx.x - 6 * 32;  // 0..63
+    const int gt = threadIdx.x - 6 * 32;  // 0..GATHER_T-1
     __shared__ unsigned int s_chunk;
     const unsigned total = unsigned(p.num_m) * p.W;
     const int vec_per_row = p.kw / 8;  // 16-byte vectors per shard row
     for (;;) {
       if (gt == 0) s_chunk = atomicAdd(&p.ctr[0], 1u);
-      named_bar(1, 64);
+      named_bar(1, GATHER_T);
       const unsigned c = s_chunk;
-      named_bar(1, 64);
+      named_bar(1, GATHER_T);
       if (c >= total) break;
       const int mb = int(c / p.W);
       const int src = (p.own + 1 + int(c % p.W)) % p.W;  // own shard last
@@ -456,16 +457,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint4* s = reinterpret_cast<const uint4*>(p.peer_shard[src] + size_t(r0) * p.kw);
       const int nvec = rows * vec_per_row;
       constexpr int U = 8;
-      for (int base = 0; base < nvec; base += 64 * U) {
+      for (int base = 0; base < nvec; base += GATHER_T * U) {
         uint4 v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int e = base + u * 64 + gt;
+          const int e = base + u * GATHER_T + gt;
           if (e < nvec) v[u] = s[e];
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int e = base + u * 64 + gt;
+          const int e = base + u * GATHER_T + gt;
           if (e < nvec) {
             const int rr = e / vec_per_row, cv = e % vec_per_row;
             *reinterpret_cast<uint4*>(p.inbox + size_t(r0 + rr) * p.K + size_t(src) * p.kw + 8 * cv) = v[u];
@@ -473,7 +474,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
       fence_proxy_async_global();
-      named_bar(1, 64);
+      named_bar(1, GATHER_T);
       if (gt == 0) {
         __threadfence();
         red_release_sys(p.ready_w + size_t(mb) * p.W + src, 1);
@@ -509,7 +510,7 @@ struct PushParams {
   unsigned int* ctr;  // [0] chunk counter, [1] done
 };
 
-__global__ void __launch_bounds__(256) ag_push_kernel(const PushParams p) {
+__global__ void __launch_bounds__(512) ag_push_kernel(const PushParams p) {
   __shared__ unsigned int s_chunk;
   const unsigned total = unsigned(p.num_m) * p.W;
   const int vec_per_row = p.kw / 8;
@@ -527,17 +528,17 @@ __global__ void __launch_bounds__(256) ag_push_kernel(const PushParams p) {
     const uint4* s = reinterpret_cast<const uint4*>(p.shard + size_t(r0) * p.kw);
     __nv_bfloat16* ib = p.inbox[dst];
     const int nvec = rows * vec_per_row;
-    constexpr int U = 4;
-    for (int base = 0; base < nvec; base += 256 * U) {
+    constexpr int U = 8;  // 64 KB of loads in flight per CTA feeding peer stores
+    for (int base = 0; base < nvec; base += 512 * U) {
       uint4 v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int e = base + u * 256 + threadIdx.x;
+        const int e = base + u * 512 + threadIdx.x;
         if (e < nvec) v[u] = s[e];
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int e = base + u * 256 + threadIdx.x;
+        const int e = base + u * 512 + threadIdx.x;
         if (e < nvec) {
           const int rr = e / vec_per_row, cv = e % vec_per_row;
           *reinterpret_cast<uint4*>(ib + size_t(r0 + rr) * p.K + size_t(p.self) * p.kw + 8 * cv) = v[u];
@@ -856,7 +857,7 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
     pp.self = r;
     pp.num_m = num_m;
     pp.ctr = ctr_of(r, 1);
-    ag_push_kernel<<<push_ctas, 256, 0, w->ranks[r].side>>>(pp);
+    ag_push_kernel<<<push_ctas, 512, 0, w->ranks[r].side>>>(pp);
     TFB_CUDA(cudaGetLastError());
     ++w->launches;
   }
