@@ -55,7 +55,10 @@ typedef enum {
   TF_FD_BSP = 0,
   TF_FD_INDEPENDENT_AG = 1,
   TF_FD_FINE_WAITS = 2,
-  TF_FD_FUSED = 3
+  TF_FD_FUSED = 3,
+  /* run_fused with FdOptions::fold_by_arrival (flash_decode.hpp:108-114,
+   * 377-408): fold whichever source landed first; not bitwise reproducible. */
+  TF_FD_FUSED_BY_ARRIVAL = 4
 } tf_fd_variant;
 
 typedef enum { TF_F32 = 0, TF_BF16 = 1 } tf_dtype;

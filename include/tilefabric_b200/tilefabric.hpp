@@ -305,7 +305,7 @@ inline DecodeProblem make_problem(std::uint64_t seed, int heads, int head_dim, s
 }
 
 struct FdOptions {  // :108-114
-  bool fold_by_arrival = false;  // rejected: the B200 fold is always ascending
+  bool fold_by_arrival = false;  // fused only: fold in arrival order (not bitwise reproducible)
 };
 
 struct FdRun {  // :116-123
@@ -317,8 +317,10 @@ struct FdRun {  // :116-123
 
 inline FdRun run_fd(const DecodeProblem& p, Variant variant, const WorldConfig& cfg,
                     const FdOptions& opts = {}) {
-  if (opts.fold_by_arrival)
-    throw ConfigError("fold_by_arrival is not supported: the B200 fold is ascending-source");
+  if (opts.fold_by_arrival) {
+    if (variant != Variant::kFused) throw ConfigError("fold_by_arrival applies to the fused schedule only");
+    variant = static_cast<Variant>(TF_FD_FUSED_BY_ARRIVAL);
+  }
   cfg.validate();
   p.validate(cfg.world_size);
   const int W = cfg.world_size;

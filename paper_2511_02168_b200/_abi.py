@@ -57,7 +57,7 @@ _STATUS = {1: ConfigError, 2: BoundsError, 3: ShapeError, 4: DeadlockError, 5: W
            6: EmptyAttentionError, 7: NumericError, 8: CudaError}
 
 TF_AG_BASELINE, TF_AG_PULL, TF_AG_PUSH = 0, 1, 2
-TF_FD_BSP, TF_FD_INDEPENDENT_AG, TF_FD_FINE_WAITS, TF_FD_FUSED = 0, 1, 2, 3
+TF_FD_BSP, TF_FD_INDEPENDENT_AG, TF_FD_FINE_WAITS, TF_FD_FUSED, TF_FD_FUSED_BY_ARRIVAL = 0, 1, 2, 3, 4
 TF_F32, TF_BF16 = 0, 1
 IPC_HANDLE_BYTES = 64
 

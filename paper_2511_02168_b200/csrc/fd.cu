@@ -85,6 +85,7 @@ struct FdParams {
   unsigned int* ctr;          // [0] compute, [1] fold, [2] done
   int push;                   // push rank partials to every inbox (+ signal)
   int fold_inline;            // fused: fold after compute
+  int by_arrival;             // fused: FdOptions::fold_by_arrival
   float* inbox_all[64];       // every rank's inbox (this parity), this process' view
   uint64_t* flags_all[64];    // every rank's flag board
   FdRank r[kMaxLocal];
@@ -616,29 +617,70 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const FdP
       const int g = item % G, lr = item / G;
       const FdRank& R = P.r[lr];
       const int b = g / P.Hkv, kvh = g % P.Hkv;
-      if (threadIdx.x == 0) {
-        s_last = 1;
-        for (int s = 0; s < P.W; ++s)
-          if (!wait_geq(R.flags + size_t(s) * G + g, P.flag_epoch, P.watchdog_ns, P.err, kWaitSignal,
-                        R.rank, P.board, s, g, 0)) {
-            s_last = 0;
-            break;
-          }
-      }
-      __syncthreads();
-      if (!s_last) break;
-      for (int h = threadIdx.x >> 5; h < P.gs; h += blockDim.x >> 5) {
-        const int lane = threadIdx.x & 31;
-        const int hq = kvh * P.gs + h;
-        const size_t roff = (size_t(b) * P.Hq + hq) * row_len;
-        float am = -INFINITY, al = 0.0f, ao[8];
+      // Per-source waits right before each fold (flash_decode.hpp:409-418):
+      // ascending source order, or -- FdOptions::fold_by_arrival
+      // (:377-408) -- whichever source has landed first.
+      constexpr int MAXH = 4;  // heads per warp (gs <= 32, 8 warps)
+      float am[MAXH], al[MAXH], ao[MAXH][8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) ao[i] = 0.0f;
-        for (int s = 0; s < P.W; ++s) {
-          const float* src = R.inbox + size_t(s) * P.B * P.Hq * row_len + roff;
-          fold_row<8>(am, al, ao, src, d, lane, 32);
+      for (int j = 0; j < MAXH; ++j) {
+        am[j] = -INFINITY;
+        al[j] = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ao[j][i] = 0.0f;
+      }
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      uint64_t folded = 0;
+      bool ok = true;
+      for (int i = 0; i < P.W && ok; ++i) {
+        if (threadIdx.x == 0) {
+          int src = -1;
+          if (!P.by_arrival) {
+            if (wait_geq(R.flags + size_t(i) * G + g, P.flag_epoch, P.watchdog_ns, P.err, kWaitSignal,
+                         R.rank, P.board, i, g, 0))
+              src = i;
+          } else {
+            const uint64_t t0 = globaltimer_ns();
+            for (unsigned polls = 0; src < 0; ++polls) {
+              for (int s = 0; s < P.W; ++s)
+                if (!((folded >> s) & 1ull) && ld_acquire_sys(R.flags + size_t(s) * G + g) >= P.flag_epoch) {
+                  src = s;
+                  break;
+                }
+              if (src < 0 && (polls & 63u) == 63u) {
+                if (err_raised(P.err)) break;
+                if (globaltimer_ns() - t0 > P.watchdog_ns) {
+                  raise_err(P.err, TF_ERR_DEADLOCK, kWaitSignal, R.rank, P.board, -1, g, P.flag_epoch, 0, 0);
+                  break;
+                }
+              }
+            }
+          }
+          s_last = src;
         }
-        if (al == 0.0f) {
+        __syncthreads();
+        const int src = s_last;
+        __syncthreads();
+        if (src < 0) {
+          ok = false;
+          break;
+        }
+        folded |= 1ull << src;
+        const float* base = R.inbox + size_t(src) * P.B * P.Hq * row_len;
+#pragma unroll
+        for (int j = 0; j < MAXH; ++j) {
+          const int h = warp + j * nw;
+          if (h < P.gs)
+            fold_row<8>(am[j], al[j], ao[j], base + (size_t(b) * P.Hq + kvh * P.gs + h) * row_len, d, lane, 32);
+        }
+      }
+      if (!ok) break;
+#pragma unroll
+      for (int j = 0; j < MAXH; ++j) {
+        const int h = warp + j * nw;
+        if (h >= P.gs) continue;
+        const int hq = kvh * P.gs + h;
+        if (al[j] == 0.0f) {
           if (lane == 0)
             raise_err(P.err, TF_ERR_EMPTY_ATTENTION, kEmpty, R.rank, -1, 0, 0, 0, 0, uint64_t(hq));
           continue;
@@ -647,7 +689,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const FdP
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int e = lane + 32 * i;
-          if (e < d) store_out(R.out, ooff + e, ao[i] / al, P.out_bf16);
+          if (e < d) store_out(R.out, ooff + e, ao[j][i] / al[j], P.out_bf16);
         }
       }
     }
@@ -786,7 +828,7 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   if (!tw) return set_error(TF_ERR_CONFIG, "tf_flash_decode: NULL world");
   World* w = &tw->impl;
   TFB_CHECK(fd_validate(w, shape, q, k_shard, v_shard, out));
-  if (variant < TF_FD_BSP || variant > TF_FD_FUSED)
+  if (variant < TF_FD_BSP || variant > TF_FD_FUSED_BY_ARRIVAL)
     return set_error(TF_ERR_CONFIG, "run_fd: unknown variant");
   const tf_fd_shape& sh = *shape;
   auto st = resolve_streams(w, streams);
@@ -800,7 +842,7 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
 
   // Boards: per (src, group) for fused, per src otherwise (fd.flags is
   // W x 1 in the reference, flash_decode.hpp:357).
-  const bool fused = variant == TF_FD_FUSED;
+  const bool fused = variant == TF_FD_FUSED || variant == TF_FD_FUSED_BY_ARRIVAL;
   BoardEntry fb;
   // Only schedules that signal advance the board's epoch: every rank (every
   // process, in an IPC world) must agree on "run e waits for >= e".
@@ -882,6 +924,7 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
         Q.ctr = reinterpret_cast<unsigned int*>(w->ptr(lead, ctr_off));
         Q.push = push;
         Q.fold_inline = fold_inline;
+        Q.by_arrival = variant == TF_FD_FUSED_BY_ARRIVAL;
         cudaSetDevice(kv.first);
         const unsigned items = unsigned(Q.nlocal) * G * S_eff;
         int per_sm = 1;

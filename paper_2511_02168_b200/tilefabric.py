@@ -346,8 +346,10 @@ class fd:  # namespace tilefabric::fd
                dtype: int = _abi.TF_F32, out_dtype: Optional[int] = None):
         """flash_decode.hpp:425-438"""
         if opts is not None and opts.fold_by_arrival:
-            raise ConfigError("fold_by_arrival is not supported: the B200 fold is always "
-                              "ascending-source (bitwise reproducible)")
+            # flash_decode.hpp:377-408: fused only; arrival order, not bitwise reproducible.
+            if int(variant) != _abi.TF_FD_FUSED:
+                raise ConfigError("fold_by_arrival applies to the fused schedule only")
+            variant = _abi.TF_FD_FUSED_BY_ARRIVAL
         cfg.validate()
         p.validate(cfg.world_size)
         torch = _torch()

@@ -218,10 +218,21 @@ int main() {
             for (const auto& out : run.out) EXPECT_TRUE(bitwise(out, run.out[0]));
           }
   });
-  run_test("FdOptions.FoldByArrivalRejected", [] {
+  // flash_decode.hpp:377-408: arrival-order fold -- same result up to
+  // round-off (not bitwise reproducible), fused schedule only.
+  run_test("FdOptions.FoldByArrival", [] {
     fd::FdOptions o;
     o.fold_by_arrival = true;
-    EXPECT_THROW(fd::run_fused(fd::make_problem(1, 2, 4, 64), quick_config(2), o), ConfigError);
+    const auto p = fd::make_problem(5, 2, 8, 96);
+    const auto oracle = oracle_attention(p);
+    for (int w : {1, 2, 4}) {
+      const auto run = fd::run_fused(p, quick_config(w), o);
+      for (const auto& out : run.out)
+        EXPECT_TRUE(tfo_max_head_relative_error(out.data(), oracle.data(), p.heads, p.head_dim) <= 1e-5);
+      for (const auto& counts : run.flag_counts)
+        for (auto c : counts) EXPECT_TRUE(c == 1);
+    }
+    EXPECT_THROW(fd::run_fd(p, fd::Variant::kBsp, quick_config(2), o), ConfigError);
   });
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;

@@ -175,3 +175,18 @@ def test_three_taxes_measured_on_device():
     for t in fused.taxes + bsp.taxes:
         assert t["staged_bytes"] == w * wire_bytes
     assert fused.taxes[0]["signal_waits"] >= w  # one fold wait per source (per group)
+
+
+def test_fold_by_arrival_option(oracle):
+    # flash_decode.hpp:108-114, 377-408: arrival-order fold; equal to the
+    # oracle within tolerance, flags all 1; other schedules reject it.
+    p = tf.fd.make_problem(5, 2, 8, 96)
+    want = oracle.attention(p.q[0], p.k[0], p.v[0], p.scale)
+    for w in (1, 2, 4, 8):
+        run = tf.fd.run_fused(p, tf.WorldConfig(world_size=w), tf.fd.FdOptions(fold_by_arrival=True))
+        for out in run.out:
+            assert oracle.head_rel_err(out, want) <= 1e-5
+        for counts in run.flag_counts:
+            assert counts == [1] * w
+    with pytest.raises(tf.ConfigError):
+        tf.fd.run_bsp(p, tf.WorldConfig(world_size=2), opts=tf.fd.FdOptions(fold_by_arrival=True))
