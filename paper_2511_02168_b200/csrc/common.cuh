@@ -56,6 +56,21 @@ __device__ __forceinline__ void red_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Same-device destination: a gpu-scope release is enough and avoids the
+// MEMBAR.SYS a sys-scope release costs (~us under load).
+__device__ __forceinline__ void red_release_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Ticket counter: release publishes the CTA's prior writes (cumulative over
+// a preceding bar.sync), acquire lets the winner read everyone else's.
+__device__ __forceinline__ unsigned long long atom_add_acq_rel_gpu(unsigned long long* p,
+                                                                   unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ uint64_t atom_add_acq_rel_sys(uint64_t* p, uint64_t v) {
   uint64_t old;
   asm volatile("atom.acq_rel.sys.global.add.u64 %0, [%1], %2;"
@@ -124,7 +139,7 @@ static __device__ __noinline__ bool wait_geq(const uint64_t* cell, uint64_t expe
       }
     }
     __nanosleep(ns);
-    if (ns < 1024) ns <<= 1;
+    if (ns < 256) ns <<= 1;  // short cap: wake-up latency is on the critical path
   }
   const unsigned long long dt = globaltimer_ns() - t0;
   atomicAdd(barrier ? &err->barriers : &err->waits, 1ull);

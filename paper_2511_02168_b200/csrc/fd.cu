@@ -80,12 +80,16 @@ struct FdParams {
   uint64_t watchdog_ns;
   DevErr* err;
   int board;
-  float* ws;                  // [nlocal][G][S][gs][d+2] split partials
+  float* ws;                  // [nlocal][G][S][gs][d+4] split partials [m l - - o[d]]
   unsigned long long* ticket; // [nlocal][G] epoch-valued tickets
+  unsigned long long* claim;  // [nlocal][G] epoch-valued cross-rank fold claims
   unsigned int* ctr;          // [0] compute, [1] fold, [2] done
+  uint64_t local_dst;         // bit dst: dst's inbox/flags live on this launch's device
   int push;                   // push rank partials to every inbox (+ signal)
   int fold_inline;            // fused: fold after compute
+  int direct;                 // fused, W = 1: the final split fold also finalizes out
   int by_arrival;             // fused: FdOptions::fold_by_arrival
+  unsigned long long* trace;  // TFB_TRACE: [grid][16] %globaltimer stamps per CTA (else null)
   float* inbox_all[64];       // every rank's inbox (this parity), this process' view
   uint64_t* flags_all[64];    // every rank's flag board
   FdRank r[kMaxLocal];
@@ -159,8 +163,18 @@ __device__ __forceinline__ void store_out(void* p, size_t idx, float v, int bf16
   else static_cast<float*>(p)[idx] = v;
 }
 
+// Split-partial workspace rows (internal, not the wire format): [m l - - o[d]]
+// so o starts 16-byte aligned and the group fold reads it with 128-bit loads.
+constexpr int kWsO = 4;
+__host__ __device__ __forceinline__ int ws_row(int d) { return d + kWsO; }
+
+// TFB_TRACE phase stamp (slot i of this CTA's 16), for tools/fd_trace.py.
+__device__ __forceinline__ void trace_at(const FdParams& P, int i) {
+  if (P.trace && threadIdx.x == 0) P.trace[size_t(blockIdx.x) * 16 + i] = globaltimer_ns();
+}
+
 // ---- generic split partial: one warp per q-head ----------------------------
-// Writes ws rows [m | l | o] (natural-log m) for the gs heads of the group.
+// Writes ws rows [m | l | - - | o] (natural-log m) for the gs heads of the group.
 __device__ void generic_split(const FdParams& P, int lr, int g, int sp, float* wsrow) {
   const FdRank& R = P.r[lr];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -208,7 +222,7 @@ __device__ void generic_split(const FdParams& P, int lr, int g, int sp, float* w
       }
       m = mn;
     }
-    float* row = wsrow + size_t(h) * (d + 2);
+    float* row = wsrow + size_t(h) * ws_row(d);
     if (lane == 0) {
       row[0] = m;
       row[1] = l;
@@ -216,7 +230,7 @@ __device__ void generic_split(const FdParams& P, int lr, int g, int sp, float* w
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int e = lane + 32 * i;
-      if (e < d) row[2 + e] = o[i];
+      if (e < d) row[kWsO + e] = o[i];
     }
   }
 }
@@ -253,6 +267,7 @@ __device__ __forceinline__ uint32_t w4(const uint4& v, int i) {
 // SM keep ~128 KB of KV loads in flight (what HBM3e needs at ~2 us latency).
 constexpr int kFastWarps = 8;
 constexpr int kFoldW = 1024;  // split weights cached in smem for the group fold
+constexpr int kChunk = 8;     // splits per level-1 fold (two-level split fold)
 constexpr int kFastThreads = kFastWarps * 32;
 
 // d index held by O^T accumulator row r of PV tile (i, j) (see header).
@@ -279,30 +294,26 @@ __device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
   int badl = 0;
   const uint4 z = make_uint4(0, 0, 0, 0);
   uint4 k_a[4], k_b[4], v_a[4], v_b[4];
-  auto load_k = [&](size_t j0) {
-    const size_t ka = j0 + gq, kb8 = j0 + gq + 8;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      k_a[i] = ka < ke ? ldg_stream(K + ka * 128 + 8 * (t + 4 * i)) : z;
-      k_b[i] = kb8 < ke ? ldg_stream(K + kb8 * 128 + 8 * (t + 4 * i)) : z;
-    }
-  };
-  auto load_v = [&](size_t j0) {
-    const size_t ka = j0 + gq, kb8 = j0 + gq + 8;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      v_a[i] = ka < ke ? ldg_stream(V + ka * 128 + 8 * (t + 4 * i)) : z;
-      v_b[i] = kb8 < ke ? ldg_stream(V + kb8 * 128 + 8 * (t + 4 * i)) : z;
-    }
-  };
+  // Row a of each 16-key tile is key j0 + gq, row b is j0 + gq + 8: one
+  // pointer per stream, lane slice folded in, tile/row/chunk offsets as
+  // immediates (64-bit per-load addresses cost registers the loop needs).
+  const __nv_bfloat16* kp = K + (kb + gq) * 128 + 8 * t;
+  const __nv_bfloat16* vp = V + (kb + gq) * 128 + 8 * t;
   // (A one-tile-ahead register pipeline was measured: it spills at the
   //  128-register budget 16 warps/SM need and lost 10 %; the loads are issued
   //  at the top of each tile instead and the 16 resident warps overlap them.)
-  for (size_t j0 = kb; j0 < ke; j0 += 16) {
-    const size_t ka = j0 + gq, kb8 = j0 + gq + 8;
-    const bool va = ka < ke, vb = kb8 < ke;
-    load_k(j0);
-    load_v(j0);
+  for (int rem = int(ke - kb) - gq; rem > -gq; rem -= 16, kp += 16 * 128, vp += 16 * 128) {
+    const bool va = rem > 0, vb = rem > 8;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      k_a[i] = va ? ldg_stream(kp + 32 * i) : z;
+      k_b[i] = vb ? ldg_stream(kp + 8 * 128 + 32 * i) : z;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v_a[i] = va ? ldg_stream(vp + 32 * i) : z;
+      v_b[i] = vb ? ldg_stream(vp + 8 * 128 + 32 * i) : z;
+    }
     // S^T = K . Q^T over 8 k-steps of 16 d.
     float s[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -406,9 +417,11 @@ __device__ void fast_split(const FdParams& P, int lr, int g, int sp, float* wsro
   if (threadIdx.x == 0) sm.bad = 0;
   for (int i = threadIdx.x; i < 8 * 16; i += blockDim.x) sm.q[i] = reinterpret_cast<const uint4*>(Q)[i];
   __syncthreads();
+  trace_at(P, 12);
   fast_warp_range(P, K, V, reinterpret_cast<const __nv_bfloat16*>(sm.q), wb, we, sm.m[warp], sm.l[warp],
                   sm.o[warp], &sm.bad);
   __syncthreads();
+  trace_at(P, 13);
   if (sm.bad) {
     if (threadIdx.x == 0)
       raise_err(P.err, TF_ERR_NUMERIC, kNumeric, R.rank, -1, 0, 0, 0, 0,
@@ -436,25 +449,289 @@ __device__ void fast_split(const FdParams& P, int lr, int g, int sp, float* wsro
       o = o * ax + bo * ay;
       m = mm;
     }
-    float* row = wsrow + size_t(h) * 130;
+    float* row = wsrow + size_t(h) * ws_row(128);
     if (dd == 0) {
       row[0] = m * kLn2;
       row[1] = l;
     }
-    row[2 + dd] = o;
+    row[kWsO + dd] = o;
+  }
+}
+
+// ---- cross-rank fold of one (local rank, group) ---------------------------
+// W inbox rows per q-head, folded in ascending source order with a
+// per-source wait right before each fold (flash_decode.hpp:409-418) or --
+// FdOptions::fold_by_arrival (:377-408) -- whichever source landed first,
+// then finalized (tilemath.hpp:225-239) into out.  Returns false when a wait
+// failed (the error is already raised).
+__device__ __noinline__ bool fold_group(const FdParams& P, int lr, int g, int& s_src) {
+  const int G = P.B * P.Hkv, d = P.d, row_len = d + 2;
+  const FdRank& R = P.r[lr];
+  const int b = g / P.Hkv, kvh = g % P.Hkv;
+  constexpr int MAXH = 4;  // heads per warp (gs <= 32, 8 warps)
+  float am[MAXH], al[MAXH], ao[MAXH][8];
+#pragma unroll
+  for (int j = 0; j < MAXH; ++j) {
+    am[j] = -INFINITY;
+    al[j] = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ao[j][i] = 0.0f;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint64_t folded = 0;
+  for (int i = 0; i < P.W; ++i) {
+    if (threadIdx.x == 0) {
+      int src = -1;
+      if (!P.by_arrival) {
+        if (wait_geq(R.flags + size_t(i) * G + g, P.flag_epoch, P.watchdog_ns, P.err, kWaitSignal,
+                     R.rank, P.board, i, g, 0))
+          src = i;
+      } else {
+        const uint64_t t0 = globaltimer_ns();
+        for (unsigned polls = 0; src < 0; ++polls) {
+          for (int s = 0; s < P.W; ++s)
+            if (!((folded >> s) & 1ull) && ld_acquire_sys(R.flags + size_t(s) * G + g) >= P.flag_epoch) {
+              src = s;
+              break;
+            }
+          if (src < 0 && (polls & 63u) == 63u) {
+            if (err_raised(P.err)) break;
+            if (globaltimer_ns() - t0 > P.watchdog_ns) {
+              raise_err(P.err, TF_ERR_DEADLOCK, kWaitSignal, R.rank, P.board, -1, g, P.flag_epoch, 0, 0);
+              break;
+            }
+          }
+        }
+      }
+      s_src = src;
+    }
+    __syncthreads();
+    const int src = s_src;
+    __syncthreads();
+    if (src < 0) return false;
+    folded |= 1ull << src;
+    const float* base = R.inbox + size_t(src) * P.B * P.Hq * row_len;
+#pragma unroll
+    for (int j = 0; j < MAXH; ++j) {
+      const int h = warp + j * nw;
+      if (h < P.gs)
+        fold_row<8>(am[j], al[j], ao[j], base + (size_t(b) * P.Hq + kvh * P.gs + h) * row_len, d, lane, 32);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < MAXH; ++j) {
+    const int h = warp + j * nw;
+    if (h >= P.gs) continue;
+    const int hq = kvh * P.gs + h;
+    if (al[j] == 0.0f) {
+      if (lane == 0) raise_err(P.err, TF_ERR_EMPTY_ATTENTION, kEmpty, R.rank, -1, 0, 0, 0, 0, uint64_t(hq));
+      continue;
+    }
+    const size_t ooff = (size_t(b) * P.Hq + hq) * d;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = lane + 32 * i;
+      if (e < d) store_out(R.out, ooff + e, ao[j][i] / al[j], P.out_bf16);
+    }
+  }
+  return true;
+}
+
+__device__ __forceinline__ float4 ldcg4(const float* p) {
+  return __ldcg(reinterpret_cast<const float4*>(p));
+}
+
+// ---- split fold: max-first fold of n split-partial rows of a group -------
+// Rows first, first + step, ... (n of them) of the group's workspace; the
+// result goes in place into ws row `first` (level 1 of the two-level fold)
+// or out as the rank's wire rows (to_wire: every inbox when pushing, else
+// the published partial).  Max-first and fully parallel (every row loaded
+// independently, ld.cg through L2): M = max m_i, w_i = exp(m_i - M),
+// l = sum l_i w_i, o = sum o_i w_i -- the same monoid as combine_partials
+// (tilemath.hpp:186-220) evaluated in one pass instead of n dependent steps.
+// Identical code in every schedule, so schedules stay bitwise equal.
+// Non-inlined: its own register allocation keeps the attention loop's.
+__device__ __noinline__ void fold_ws(const FdParams& P, int lr, int g, float* grp, int first, int step,
+                                     int n, int to_wire, float* s_M, float* s_L, float* s_w, float* s_l) {
+  // W = 1, fused: the rank's wire row is also the whole fold (one source),
+  // so finalize out here -- o / l on the same floats fold_group would take
+  // from the inbox (combine with an empty accumulator copies them), bitwise
+  // the same result one dependent round trip earlier.
+  const int direct = to_wire && P.direct;
+  void* const out = P.r[lr].out;
+  const int out_bf16 = P.out_bf16;
+  // Scalars and the peer inbox table into registers / smem once: P lives in
+  // the kernel's parameter space, reached through a generic pointer here,
+  // and the row stores below would otherwise force a reload per use.
+  const int d = P.d, row_len = d + 2, wrl = ws_row(d);
+  const int gs = P.gs, W = P.W, Hq = P.Hq, Hkv = P.Hkv, push = P.push;
+  const int rank = P.r[lr].rank;
+  float* const pub = P.r[lr].pub;
+  __shared__ float* s_inbox[64];
+  if (to_wire && push) {
+    for (int i = threadIdx.x; i < W; i += blockDim.x) s_inbox[i] = P.inbox_all[i];
+    __syncthreads();
+  }
+  const int b = g / Hkv, kvh = g % Hkv;
+  const size_t base_src = size_t(rank) * P.B * Hq * row_len;
+  auto row = [&](int i) { return grp + size_t(first + i * step) * gs * wrl; };  // split row block
+  auto row_off = [&](int h) { return (size_t(b) * Hq + kvh * gs + h) * row_len; };
+  // Result element e of head h; e in wire numbering (0 = m, 1 = l, 2.. = o).
+  auto put = [&](int h, int e, float val) {
+    if (!to_wire) {
+      row(0)[size_t(h) * wrl + (e < 2 ? e : kWsO + e - 2)] = val;
+    } else if (push) {
+      for (int dst = 0; dst < W; ++dst) s_inbox[dst][base_src + row_off(h) + e] = val;
+    } else {
+      pub[row_off(h) + e] = val;
+    }
+  };
+  auto put2 = [&](int h, int e, float x, float y) {  // e even: 8-byte aligned
+    const float2 v2 = make_float2(x, y);
+    if (!to_wire) {
+      *reinterpret_cast<float2*>(row(0) + size_t(h) * wrl + (e < 2 ? e : kWsO + e - 2)) = v2;
+    } else if (push) {
+      for (int dst = 0; dst < W; ++dst)
+        *reinterpret_cast<float2*>(s_inbox[dst] + base_src + row_off(h) + e) = v2;
+    } else {
+      *reinterpret_cast<float2*>(pub + row_off(h) + e) = v2;
+    }
+  };
+  const int NG = n * gs;
+  if (NG <= kFoldW && (d % 4) == 0) {
+    // Each thread owns one (head, 4 d) quad and keeps UF 16-byte loads in
+    // flight; the first UF rows are issued before the m/l round trip, so a
+    // level of the fold (n <= kChunk = UF) costs about one L2 round trip.
+    constexpr int UF = 8;
+    const int qpr = d / 4, quads = gs * qpr;
+    float4 v[UF];
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto load_rows = [&](int h, int e, int i0) {
+#pragma unroll
+      for (int u = 0; u < UF; ++u)
+        v[u] = i0 + u < n ? ldcg4(row(i0 + u) + size_t(h) * wrl + kWsO + e) : z4;
+    };
+    if (int(threadIdx.x) < quads) load_rows(threadIdx.x / qpr, 4 * (threadIdx.x % qpr), 0);
+    // (1) every (row, head) m/l pair, one 8-byte load each
+    for (int i = threadIdx.x; i < NG; i += blockDim.x) {
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(row(i / gs) + size_t(i % gs) * wrl));
+      s_w[i] = ml.y != 0.0f ? ml.x : -INFINITY;
+      s_l[i] = ml.y;
+    }
+    __syncthreads();
+    trace_at(P, to_wire ? 11 : 10);
+    // (2) per-head max
+    for (int h = threadIdx.x; h < gs; h += blockDim.x) {
+      float M = -INFINITY;
+      for (int i = 0; i < n; ++i) M = fmaxf(M, s_w[i * gs + h]);
+      s_M[h] = M;
+    }
+    __syncthreads();
+    // (3) weights, (4) normalisers
+    for (int i = threadIdx.x; i < NG; i += blockDim.x)
+      s_w[i] = s_l[i] != 0.0f ? expf(s_w[i] - s_M[i % gs]) : 0.0f;
+    __syncthreads();
+    for (int h = threadIdx.x; h < gs; h += blockDim.x) {
+      float L = 0.0f;
+      for (int i = 0; i < n; ++i) L = __fadd_rn(L, __fmul_rn(s_l[i * gs + h], s_w[i * gs + h]));
+      s_L[h] = L;
+      if (direct && L == 0.0f)
+        raise_err(P.err, TF_ERR_EMPTY_ATTENTION, kEmpty, rank, -1, 0, 0, 0, 0, uint64_t(kvh * gs + h));
+    }
+    if (direct) __syncthreads();
+    // (5) the weighted o sums
+    bool first_quad = true;
+    for (int pi = threadIdx.x; pi < quads; pi += blockDim.x) {
+      const int h = pi / qpr, e = 4 * (pi % qpr);
+      float4 acc[2] = {z4, z4};
+      for (int i0 = 0; i0 < n; i0 += UF) {
+        if (!first_quad) load_rows(h, e, i0);
+        first_quad = false;
+#pragma unroll
+        for (int u = 0; u < UF; ++u) {
+          if (i0 + u >= n) break;
+          const float w = s_w[(i0 + u) * gs + h];
+          float4& a = acc[u & 1];
+          a.x = __fadd_rn(a.x, __fmul_rn(v[u].x, w));
+          a.y = __fadd_rn(a.y, __fmul_rn(v[u].y, w));
+          a.z = __fadd_rn(a.z, __fmul_rn(v[u].z, w));
+          a.w = __fadd_rn(a.w, __fmul_rn(v[u].w, w));
+        }
+      }
+      const float o0 = __fadd_rn(acc[0].x, acc[1].x), o1 = __fadd_rn(acc[0].y, acc[1].y);
+      const float o2 = __fadd_rn(acc[0].z, acc[1].z), o3 = __fadd_rn(acc[0].w, acc[1].w);
+      put2(h, 2 + e, o0, o1);
+      put2(h, 4 + e, o2, o3);
+      if (direct && s_L[h] != 0.0f) {
+        const size_t ooff = (size_t(b) * Hq + kvh * gs + h) * d + e;
+        const float L = s_L[h];
+        store_out(out, ooff, o0 / L, out_bf16);
+        store_out(out, ooff + 1, o1 / L, out_bf16);
+        store_out(out, ooff + 2, o2 / L, out_bf16);
+        store_out(out, ooff + 3, o3 / L, out_bf16);
+      }
+    }
+    __syncthreads();
+    for (int h = threadIdx.x; h < gs; h += blockDim.x) put2(h, 0, s_M[h], s_L[h]);
+  } else {
+    // Large n x gs or d % 4 != 0: per-head scalar fold (weights recomputed).
+    for (int h = threadIdx.x; h < gs; h += blockDim.x) {
+      float M = -INFINITY;
+      for (int i = 0; i < n; ++i) {
+        const float* r = row(i) + size_t(h) * wrl;
+        if (__ldcg(r + 1) != 0.0f) M = fmaxf(M, __ldcg(r));
+      }
+      float L = 0.0f;
+      for (int i = 0; i < n; ++i) {
+        const float* r = row(i) + size_t(h) * wrl;
+        const float l = __ldcg(r + 1);
+        L = __fadd_rn(L, __fmul_rn(l, l != 0.0f ? expf(__ldcg(r) - M) : 0.0f));
+      }
+      s_M[h] = M;
+      s_L[h] = L;
+      if (direct && L == 0.0f)
+        raise_err(P.err, TF_ERR_EMPTY_ATTENTION, kEmpty, rank, -1, 0, 0, 0, 0, uint64_t(kvh * gs + h));
+    }
+    __syncthreads();
+    // In place: every thread reads all n rows of its elements before any
+    // result element is written, and each element has one owner thread.
+    for (int idx = threadIdx.x; idx < gs * d; idx += blockDim.x) {
+      const int h = idx / d, e = idx % d;
+      float o = 0.0f;
+      for (int i = 0; i < n; ++i) {
+        const float* r = row(i) + size_t(h) * wrl;
+        const float w = __ldcg(r + 1) != 0.0f ? expf(__ldcg(r) - s_M[h]) : 0.0f;
+        if (w != 0.0f) o = __fadd_rn(o, __fmul_rn(__ldcg(r + kWsO + e), w));
+      }
+      put(h, 2 + e, o);
+      if (direct && s_L[h] != 0.0f) store_out(out, (size_t(b) * Hq + kvh * gs + h) * d + e, o / s_L[h], out_bf16);
+    }
+    __syncthreads();
+    for (int h = threadIdx.x; h < gs; h += blockDim.x) {
+      put(h, 0, s_M[h]);
+      put(h, 1, s_L[h]);
+    }
   }
 }
 
 // ---- the persistent kernel ------------------------------------------------
 template <bool FAST>
-__global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const FdParams P) {
+__global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __grid_constant__ FdParams P) {
   __shared__ unsigned int s_item;
-  __shared__ int s_last;
+  __shared__ int s_last, s_src;
   __shared__ FastSmem fsm;
   __shared__ float s_M[32], s_L[32], s_w[kFoldW], s_l[kFoldW];
   const int G = P.B * P.Hkv;
   const unsigned total = unsigned(P.nlocal) * G * P.S;
-  const int d = P.d, row_len = d + 2;
+  const int d = P.d, row_len = d + 2, wrl = ws_row(d);
+  unsigned long long* tr = P.trace ? P.trace + size_t(blockIdx.x) * 16 : nullptr;
+  auto stamp = [&](int i) {
+    if (tr && threadIdx.x == 0) tr[i] = globaltimer_ns();
+  };
+  stamp(0);
+  if (tr && threadIdx.x == 0)
+    for (int i = 1; i < 16; ++i)
+      if (i != 12 && i != 13) tr[i] = 0;
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(&P.ctr[0], 1u);
     __syncthreads();
@@ -464,236 +741,89 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const FdP
     const int sp = item % P.S;
     const int g = (item / P.S) % G;
     const int lr = item / (unsigned(P.S) * G);
-    float* grp = P.ws + ((size_t(lr) * G + g) * P.S) * P.gs * row_len;
-    float* wsrow = grp + size_t(sp) * P.gs * row_len;
+    float* grp = P.ws + ((size_t(lr) * G + g) * P.S) * P.gs * wrl;
+    float* wsrow = grp + size_t(sp) * P.gs * wrl;
     if (FAST) fast_split(P, lr, g, sp, wsrow, fsm);
     else generic_split(P, lr, g, sp, wsrow);
-    __threadfence();  // every writer publishes its ws bytes before the ticket
-    // Ticket: the last split of the group folds all S splits.
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      const unsigned long long tk = atomicAdd(&P.ticket[size_t(lr) * G + g], 1ull);
-      s_last = (tk == P.epoch * P.S - 1) ? 1 : 0;
-      __threadfence();
-    }
-    __syncthreads();
-    if (!s_last) continue;
-    const FdRank& R = P.r[lr];
-    const int b = g / P.Hkv, kvh = g % P.Hkv;
-    // Rank partial rows for (b, kvh*gs + h): fold the S split partials.
-    // Max-first and fully parallel (every split row is loaded independently,
-    // ld.cg through L2): M = max m_s, w_s = exp(m_s - M), l = sum l_s w_s,
-    // o = sum o_s w_s -- the same monoid as combine_partials
-    // (tilemath.hpp:186-220) evaluated in one pass instead of S dependent
-    // steps (the serial chain was the tail of every launch).  Identical code
-    // in every schedule, so schedules stay bitwise equal.
-    const size_t base_src = size_t(R.rank) * P.B * P.Hq * row_len;
-    auto put = [&](int h, int e, float val) {
-      const int hq = kvh * P.gs + h;
-      const size_t roff = (size_t(b) * P.Hq + hq) * row_len + e;
-      if (P.push) {
-        for (int dst = 0; dst < P.W; ++dst) P.inbox_all[dst][base_src + roff] = val;
-      } else {
-        R.pub[roff] = val;
-      }
+    stamp(1);
+    // Two-level ticketed fold.  Level 1: the last split of each chunk of
+    // kChunk consecutive splits folds the chunk in place into its first
+    // row.  Level 2: the last chunk to finish folds the chunk rows into the
+    // rank's wire rows.  Each level is ~one L2 round trip (kChunk rows, all
+    // loads in flight), where one CTA folding all S rows paid S/UF of them.
+    const int nch = (P.S + kChunk - 1) / kChunk;
+    const int c = sp / kChunk, c0 = c * kChunk, cn = min(kChunk, P.S - c0);
+    unsigned long long* tks = P.ticket + (size_t(lr) * G + g) * (nch + 1);
+    auto ticket = [&](int slot, int count) {
+      __syncthreads();
+      if (threadIdx.x == 0) s_last = atom_add_acq_rel_gpu(&tks[slot], 1ull) == P.epoch * count - 1;
+      __syncthreads();
+      return s_last != 0;
     };
-    const int SG = P.S * P.gs;
-    if (SG <= kFoldW && (d % 2) == 0) {
-      // (1) every (split, head) m/l pair, loaded in parallel
-      for (int i = threadIdx.x; i < SG; i += blockDim.x) {
-        const float* row = grp + size_t(i) * row_len;  // i = s * gs + h
-        const float l = __ldcg(row + 1);
-        s_w[i] = l != 0.0f ? __ldcg(row) : -INFINITY;
-        s_l[i] = l;
-      }
-      __syncthreads();
-      // (2) per-head max
-      for (int h = threadIdx.x; h < P.gs; h += blockDim.x) {
-        float M = -INFINITY;
-        for (int s = 0; s < P.S; ++s) M = fmaxf(M, s_w[s * P.gs + h]);
-        s_M[h] = M;
-      }
-      __syncthreads();
-      // (3) weights
-      for (int i = threadIdx.x; i < SG; i += blockDim.x)
-        s_w[i] = s_l[i] != 0.0f ? expf(s_w[i] - s_M[i % P.gs]) : 0.0f;
-      __syncthreads();
-      // (4) normalisers, and the weighted o sums with 8-byte loads, four
-      //     independent accumulators per thread so many loads are in flight
-      for (int h = threadIdx.x; h < P.gs; h += blockDim.x) {
-        float L = 0.0f;
-        for (int s = 0; s < P.S; ++s) L = __fadd_rn(L, __fmul_rn(s_l[s * P.gs + h], s_w[s * P.gs + h]));
-        s_L[h] = L;
-      }
-      const int pairs = P.gs * (d / 2);
-      for (int pi = threadIdx.x; pi < pairs; pi += blockDim.x) {
-        const int h = pi / (d / 2), e = 2 * (pi % (d / 2));
-        float2 acc[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) acc[u] = make_float2(0.f, 0.f);
-        int s = 0;
-        for (; s + 4 <= P.S; s += 4) {
-          float2 v[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            v[u] = __ldcg(reinterpret_cast<const float2*>(grp + (size_t(s + u) * P.gs + h) * row_len + 2 + e));
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float w = s_w[(s + u) * P.gs + h];
-            acc[u].x = __fadd_rn(acc[u].x, __fmul_rn(v[u].x, w));
-            acc[u].y = __fadd_rn(acc[u].y, __fmul_rn(v[u].y, w));
-          }
-        }
-        for (; s < P.S; ++s) {
-          const float2 v = __ldcg(reinterpret_cast<const float2*>(grp + (size_t(s) * P.gs + h) * row_len + 2 + e));
-          const float w = s_w[s * P.gs + h];
-          acc[0].x = __fadd_rn(acc[0].x, __fmul_rn(v.x, w));
-          acc[0].y = __fadd_rn(acc[0].y, __fmul_rn(v.y, w));
-        }
-        put(h, 2 + e, __fadd_rn(__fadd_rn(acc[0].x, acc[1].x), __fadd_rn(acc[2].x, acc[3].x)));
-        put(h, 3 + e, __fadd_rn(__fadd_rn(acc[0].y, acc[1].y), __fadd_rn(acc[2].y, acc[3].y)));
-      }
-      __syncthreads();
-      for (int h = threadIdx.x; h < P.gs; h += blockDim.x) {
-        put(h, 0, s_M[h]);
-        put(h, 1, s_L[h]);
-      }
+    if (!ticket(c, cn)) continue;
+    stamp(2);
+    if (nch > 1) {
+      if (cn > 1) fold_ws(P, lr, g, grp, c0, 1, cn, /*to_wire=*/0, s_M, s_L, s_w, s_l);
+      stamp(8);
+      if (!ticket(nch, nch)) continue;
+      stamp(9);
+      fold_ws(P, lr, g, grp, 0, kChunk, nch, /*to_wire=*/1, s_M, s_L, s_w, s_l);
     } else {
-      // Large S x gs: per-head scalar fold (weights recomputed).
-      for (int h = threadIdx.x; h < P.gs; h += blockDim.x) {
-        float M = -INFINITY;
-        for (int s = 0; s < P.S; ++s) {
-          const float* row = grp + (size_t(s) * P.gs + h) * row_len;
-          if (__ldcg(row + 1) != 0.0f) M = fmaxf(M, __ldcg(row));
-        }
-        float L = 0.0f;
-        for (int s = 0; s < P.S; ++s) {
-          const float* row = grp + (size_t(s) * P.gs + h) * row_len;
-          const float l = __ldcg(row + 1);
-          L = __fadd_rn(L, __fmul_rn(l, l != 0.0f ? expf(__ldcg(row) - M) : 0.0f));
-        }
-        s_M[h] = M;
-        s_L[h] = L;
-      }
+      fold_ws(P, lr, g, grp, 0, 1, P.S, /*to_wire=*/1, s_M, s_L, s_w, s_l);
+    }
+    const FdRank& R = P.r[lr];
+    if (P.push) {
+      // bar.sync makes every thread's row stores visible to the releasing
+      // threads; the release (gpu scope for same-device inboxes, sys scope
+      // across NVLink) is cumulative over them -- no separate fence.
       __syncthreads();
-      for (int idx = threadIdx.x; idx < P.gs * (d + 2); idx += blockDim.x) {
-        const int h = idx / (d + 2), e = idx % (d + 2);
-        float val;
-        if (e == 0) {
-          val = s_M[h];
-        } else if (e == 1) {
-          val = s_L[h];
-        } else {
-          float o = 0.0f;
-          for (int s = 0; s < P.S; ++s) {
-            const float* row = grp + (size_t(s) * P.gs + h) * row_len;
-            const float w = __ldcg(row + 1) != 0.0f ? expf(__ldcg(row) - s_M[h]) : 0.0f;
-            if (w != 0.0f) o = __fadd_rn(o, __fmul_rn(__ldcg(row + e), w));
-          }
-          val = o;
-        }
-        put(h, e, val);
+      stamp(7);
+      if (threadIdx.x < P.W) {
+        uint64_t* f = P.flags_all[threadIdx.x] + size_t(R.rank) * G + g;
+        if ((P.local_dst >> threadIdx.x) & 1ull) red_release_gpu(f, 1);
+        else red_release_sys(f, 1);
       }
     }
-    if (P.push) {
+    stamp(3);
+    if (P.fold_inline && !P.direct) {
+      // Early fold: when every source of this group has already landed
+      // (always at W = 1; the last rank to push otherwise) fold it here
+      // instead of handing it to the fold phase.  Non-blocking check, so
+      // the compute phase still never waits.
       __syncthreads();
-      if (threadIdx.x < P.W) {
-        fence_sys();
-        red_release_sys(P.flags_all[threadIdx.x] + size_t(R.rank) * G + g, 1);
+      if (threadIdx.x == 0) {
+        bool all = true;
+        for (int i = 0; i < P.W && all; ++i) all = ld_acquire_sys(R.flags + size_t(i) * G + g) >= P.flag_epoch;
+        s_src = all && atomicMax(&P.claim[size_t(lr) * G + g], (unsigned long long)P.epoch) < P.epoch;
       }
+      __syncthreads();
+      const int mine = s_src;
+      __syncthreads();
+      if (mine) fold_group(P, lr, g, s_src);
     }
   }
-  if (P.fold_inline) {
+  stamp(4);
+  if (P.fold_inline && !P.direct) {
     // Fold phase: every compute item has been claimed by a CTA that never
     // blocks before pushing, so these waits always complete.
     const unsigned nfold = unsigned(P.nlocal) * G;
     for (;;) {
       __syncthreads();
-      if (threadIdx.x == 0) s_item = atomicAdd(&P.ctr[1], 1u);
+      if (threadIdx.x == 0) {
+        s_item = atomicAdd(&P.ctr[1], 1u);
+        s_src = s_item < nfold && atomicMax(&P.claim[s_item], (unsigned long long)P.epoch) < P.epoch;
+      }
       __syncthreads();
       const unsigned item = s_item;
+      const int mine = s_src;
+      __syncthreads();
       if (item >= nfold) break;
-      const int g = item % G, lr = item / G;
-      const FdRank& R = P.r[lr];
-      const int b = g / P.Hkv, kvh = g % P.Hkv;
-      // Per-source waits right before each fold (flash_decode.hpp:409-418):
-      // ascending source order, or -- FdOptions::fold_by_arrival
-      // (:377-408) -- whichever source has landed first.
-      constexpr int MAXH = 4;  // heads per warp (gs <= 32, 8 warps)
-      float am[MAXH], al[MAXH], ao[MAXH][8];
-#pragma unroll
-      for (int j = 0; j < MAXH; ++j) {
-        am[j] = -INFINITY;
-        al[j] = 0.0f;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) ao[j][i] = 0.0f;
-      }
-      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-      uint64_t folded = 0;
-      bool ok = true;
-      for (int i = 0; i < P.W && ok; ++i) {
-        if (threadIdx.x == 0) {
-          int src = -1;
-          if (!P.by_arrival) {
-            if (wait_geq(R.flags + size_t(i) * G + g, P.flag_epoch, P.watchdog_ns, P.err, kWaitSignal,
-                         R.rank, P.board, i, g, 0))
-              src = i;
-          } else {
-            const uint64_t t0 = globaltimer_ns();
-            for (unsigned polls = 0; src < 0; ++polls) {
-              for (int s = 0; s < P.W; ++s)
-                if (!((folded >> s) & 1ull) && ld_acquire_sys(R.flags + size_t(s) * G + g) >= P.flag_epoch) {
-                  src = s;
-                  break;
-                }
-              if (src < 0 && (polls & 63u) == 63u) {
-                if (err_raised(P.err)) break;
-                if (globaltimer_ns() - t0 > P.watchdog_ns) {
-                  raise_err(P.err, TF_ERR_DEADLOCK, kWaitSignal, R.rank, P.board, -1, g, P.flag_epoch, 0, 0);
-                  break;
-                }
-              }
-            }
-          }
-          s_last = src;
-        }
-        __syncthreads();
-        const int src = s_last;
-        __syncthreads();
-        if (src < 0) {
-          ok = false;
-          break;
-        }
-        folded |= 1ull << src;
-        const float* base = R.inbox + size_t(src) * P.B * P.Hq * row_len;
-#pragma unroll
-        for (int j = 0; j < MAXH; ++j) {
-          const int h = warp + j * nw;
-          if (h < P.gs)
-            fold_row<8>(am[j], al[j], ao[j], base + (size_t(b) * P.Hq + kvh * P.gs + h) * row_len, d, lane, 32);
-        }
-      }
-      if (!ok) break;
-#pragma unroll
-      for (int j = 0; j < MAXH; ++j) {
-        const int h = warp + j * nw;
-        if (h >= P.gs) continue;
-        const int hq = kvh * P.gs + h;
-        if (al[j] == 0.0f) {
-          if (lane == 0)
-            raise_err(P.err, TF_ERR_EMPTY_ATTENTION, kEmpty, R.rank, -1, 0, 0, 0, 0, uint64_t(hq));
-          continue;
-        }
-        const size_t ooff = (size_t(b) * P.Hq + hq) * d;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int e = lane + 32 * i;
-          if (e < d) store_out(R.out, ooff + e, ao[j][i] / al[j], P.out_bf16);
-        }
-      }
+      if (!mine) continue;  // folded early by its group's last CTA
+      stamp(5);
+      if (!fold_group(P, item / G, item % G, s_src)) break;
     }
   }
+  stamp(6);
   // Last CTA out resets the work counters for the next launch.
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -861,10 +991,10 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   TFB_CHECK(heap_get(w, "fd.inbox" + geo, sizeof(float) * W * row_floats * 2, &inbox_off));
   TFB_CHECK(heap_get(w, "fd.partials" + geo, sizeof(float) * row_floats, &pub_off));
   const int nlocal_max = std::min(w->n_local, kMaxLocal);
-  const size_t ws_floats = size_t(nlocal_max) * G * S_eff * gs * (d + 2);
+  const size_t ws_floats = size_t(nlocal_max) * G * S_eff * gs * ws_row(d);
   TFB_CHECK(heap_get(w, "fd.ws[" + std::to_string(ws_floats) + "]", sizeof(float) * ws_floats, &ws_off));
   TFB_CHECK(heap_get(w, "fd.tickets[" + std::to_string(G) + "x" + std::to_string(S_eff) + "]",
-                     sizeof(unsigned long long) * nlocal_max * G, &tick_off));
+                     sizeof(unsigned long long) * nlocal_max * G * (S_eff / kChunk + 3), &tick_off));  // tickets | claims
   TFB_CHECK(heap_get(w, "fd.ctr", 64, &ctr_off));
   // Tickets are epoch-valued per (group, split-count) geometry.
   const uint64_t tepoch = ++w->epochs["fd.tickets@" + std::to_string(tick_off)];
@@ -920,10 +1050,20 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
         }
         Q.err = w->err_of(lead);
         Q.ws = reinterpret_cast<float*>(w->ptr(lead, ws_off));
+        if (std::getenv("TFB_TRACE")) {
+          size_t toff;
+          TFB_CHECK(heap_get(w, "fd.trace", sizeof(unsigned long long) * 16 * 4096, &toff));
+          Q.trace = reinterpret_cast<unsigned long long*>(w->ptr(lead, toff));
+        }
         Q.ticket = reinterpret_cast<unsigned long long*>(w->ptr(lead, tick_off));
+        Q.claim = Q.ticket + size_t(nlocal_max) * G * ((S_eff + kChunk - 1) / kChunk + 1);
+        Q.local_dst = 0;
+        for (int r = 0; r < W; ++r)
+          if (w->ranks[r].local && w->ranks[r].device == kv.first) Q.local_dst |= 1ull << r;
         Q.ctr = reinterpret_cast<unsigned int*>(w->ptr(lead, ctr_off));
         Q.push = push;
         Q.fold_inline = fold_inline;
+        Q.direct = fold_inline && W == 1;
         Q.by_arrival = variant == TF_FD_FUSED_BY_ARRIVAL;
         cudaSetDevice(kv.first);
         const unsigned items = unsigned(Q.nlocal) * G * S_eff;

@@ -1,0 +1,29 @@
+"""Host-side cost of one async C-ABI call (FD fused, AG pull) vs its GPU time."""
+import ctypes as C, os, sys, time
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2511_02168_b200 as tf
+from paper_2511_02168_b200 import _abi
+Bt, Hq, Hkv, d, L = 1, 64, 8, 128, 8192
+with tf.World(1, [0], 512 << 20) as w:
+    q = (torch.rand(Bt, Hq, d, device="cuda") * 2 - 1).bfloat16()
+    k = (torch.rand(Bt, Hkv, L, d, device="cuda") * 2 - 1).bfloat16()
+    v = (torch.rand(Bt, Hkv, L, d, device="cuda") * 2 - 1).bfloat16()
+    out = torch.empty(Bt, Hq, d, device="cuda", dtype=torch.bfloat16)
+    shape = _abi.FdShape(Bt, Hq, Hkv, d, L, d ** -0.5, 1, 1)
+    args = (w.handle, 3, C.byref(shape), _abi.ptr_array([q.data_ptr()]), _abi.ptr_array([k.data_ptr()]),
+            _abi.ptr_array([v.data_ptr()]), _abi.ptr_array([out.data_ptr()]), None, None)
+    _abi.check(w.lib.tf_flash_decode(*args))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(200):
+        w.lib.tf_flash_decode_async(*args)
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    print(f"FD host per call {(t1-t0)/200*1e6:.1f} us, wall per call incl. GPU {(t2-t0)/200*1e6:.1f} us")
+    f = w.lib.tf_launch_count
+    t0 = time.perf_counter()
+    for _ in range(2000):
+        f(w.handle)
+    print(f"bare ctypes call {(time.perf_counter()-t0)/2000*1e6:.2f} us")
