@@ -233,9 +233,10 @@ uint64_t tf_launch_count(const tf_world* w);
  * kernel launches (launch tax), acquire waits on signal boards and their
  * spin time (wait_idle), device-barrier waits and their time (bulk-sync
  * tax), bytes stored into staging/inbox tensors (staged_bytes, the
- * inter-kernel locality proxy).  Wait counters are accumulated per device by
- * every spinning thread (%globaltimer); in a loopback world all ranks share
- * one device's counters.  tf_tax_reset zeroes them. */
+ * inter-kernel locality proxy).  Wait counters are accumulated on the
+ * device by every spinning thread (%globaltimer) and reported for the
+ * waiting rank (loopback ranks sharing a device are kept apart); launches
+ * and staged bytes are host-side counts.  tf_tax_reset zeroes them. */
 typedef struct {
   uint64_t launches;
   uint64_t signal_waits, wait_idle_ns;
@@ -243,6 +244,11 @@ typedef struct {
   uint64_t staged_bytes;
 } tf_taxes;
 tf_status tf_tax_report(tf_world* w, int rank, tf_taxes* out);
+
+/* Straggler injection (WorldConfig::skew / inject_skew, fabric.hpp:59-62,
+ * 100-110): every later run delays `rank`'s first compute stage by
+ * delay_ns (0 clears it).  TF_ERR_CONFIG for a rank outside [0, W). */
+tf_status tf_world_set_skew(tf_world* w, int rank, uint64_t delay_ns);
 tf_status tf_tax_reset(tf_world* w);
 
 #ifdef __cplusplus

@@ -5,10 +5,12 @@
 // switches by including this header instead: the namespaces, problem/run
 // structs, make_problem generators, run_* entry points and exception classes
 // keep their names and meaning.  Differences (all documented in DESIGN.md):
-//   * WorldConfig keeps world_size/watchdog/seed; launch_cost, skew and
+//   * WorldConfig keeps world_size/watchdog/seed/skew (inject_skew delays the
+//     rank's first compute stage on the device); launch_cost and
 //     spin_yield_every were CPU-simulation devices and are accepted but unused.
-//   * AgGemmRun / FdRun carry results and flag counts; the CPU event log and
-//     TaxReport are not produced (the GPU measures real time instead).
+//   * AgGemmRun / FdRun carry results, flag counts and the per-rank Three
+//     Taxes measured on the device (tf_taxes); the CPU event log is not
+//     produced (the GPU measures real time instead).
 //   * dtype selects the fp32 exact-order path (bitwise == reference) or the
 //     bf16 tensor-core path; DecodeProblem gains batch and kv_heads (GQA).
 // Link: -ltilefabric_b200 (paper_2511_02168_b200/libtilefabric_b200.so).
@@ -16,7 +18,9 @@
 
 #include <cmath>
 #include <cstdint>
+#include <chrono>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <random>
 #include <stdexcept>
@@ -96,6 +100,15 @@ struct World {
     return p;
   }
   void put(void* dst, const void* src, size_t bytes) { check(tf_memcpy(w, dst, src, bytes)); }
+  template <class Cfg>
+  void apply(const Cfg& cfg) {
+    for (const auto& [rank, delay] : cfg.skew) check(tf_world_set_skew(w, rank, uint64_t(delay.count())));
+  }
+  std::vector<tf_taxes> taxes() {
+    std::vector<tf_taxes> t(tf_world_size(w));
+    for (int r = 0; r < int(t.size()); ++r) check(tf_tax_report(w, r, &t[r]));
+    return t;
+  }
 };
 }  // namespace b200
 
@@ -107,20 +120,43 @@ inline std::vector<float> uniform_reals(std::uint64_t seed, std::size_t n) {
 }
 
 // ---- fabric.hpp:46-96 (the GPU-meaningful fields) ---------------------------
-struct WorldConfig {
+using Duration = std::chrono::nanoseconds;
+
+struct WorldConfig {  // fabric.hpp:46-96
   int world_size = 1;
   double watchdog_secs = 0.0;      // 0 -> TILEFABRIC_WATCHDOG_SECS or 10 s
   std::uint64_t seed = 0;
   std::vector<int> devices;        // empty -> all ranks on GPU 0 (loopback world)
   std::size_t heap_bytes = 0;      // 0 -> sized from the problem
+  std::map<int, Duration> skew;    // straggler delay of a rank's first compute stage
+  Duration launch_cost{0};         // CPU-simulation knob: accepted, unused
+  int spin_yield_every = 64;       // CPU-simulation knob: accepted, unused
   void validate() const {
     if (world_size < 1 || world_size > 64)
       throw ConfigError("world_size must be in [1, 64], got " + std::to_string(world_size));
+    if (launch_cost < Duration::zero()) throw ConfigError("launch_cost must be >= 0");
+    if (spin_yield_every < 1) throw ConfigError("spin_yield_every must be >= 1");
+    for (const auto& [rank, delay] : skew) {
+      if (rank < 0 || rank >= world_size)
+        throw ConfigError("skew rank " + std::to_string(rank) + " out of range for world_size " +
+                          std::to_string(world_size));
+      if (delay < Duration::zero()) throw ConfigError("skew delay must be >= 0");
+    }
   }
   std::vector<int> device_list() const {
     return devices.empty() ? std::vector<int>(std::size_t(world_size), 0) : devices;
   }
 };
+
+// fabric.hpp:100-110: validates eagerly, accumulates per rank.
+template <class Rep, class Period>
+inline void inject_skew(WorldConfig& cfg, int rank, std::chrono::duration<Rep, Period> delay) {
+  if (rank < 0 || rank >= cfg.world_size)
+    throw ConfigError("inject_skew: rank " + std::to_string(rank) + " out of range for world_size " +
+                      std::to_string(cfg.world_size));
+  if (delay < delay.zero()) throw ConfigError("inject_skew: delay must be >= 0");
+  cfg.skew[rank] += std::chrono::duration_cast<Duration>(delay);
+}
 
 // ---- tilemath.hpp:78-88 ------------------------------------------------------
 struct TileSpec {
@@ -169,6 +205,7 @@ struct AgGemmRun {  // ag_gemm.hpp:85-92
   std::vector<std::vector<std::uint64_t>> flag_counts;  // push only
   std::vector<std::vector<float>> gathered;          // per rank, m x k (baseline/push)
   std::uint64_t launches = 0;                        // kernels this run launched
+  std::vector<tf_taxes> taxes;                       // per rank, measured on the device
 };
 
 namespace detail {
@@ -182,6 +219,7 @@ inline AgGemmRun run(tf_ag_variant variant, const AgGemmProblem& p, const WorldC
   const std::size_t heap = cfg.heap_bytes ? cfg.heap_bytes
                                           : esz * (p.m * kw + 5 * p.m * p.k) + (16u << 20);
   b200::World w(W, cfg.device_list(), heap, cfg.watchdog_secs);
+  w.apply(cfg);
   auto shards = w.heap("ag.a", esz * p.m * kw);
   auto gathered = w.heap("ag.gathered", esz * p.m * p.k);
   std::vector<void*> B(W), C(W);
@@ -211,6 +249,7 @@ inline AgGemmRun run(tf_ag_variant variant, const AgGemmProblem& p, const WorldC
                          C.data(), variant == TF_AG_PULL ? nullptr : gathered.data(), nullptr));
   AgGemmRun out;
   out.launches = tf_launch_count(w.w) - l0;
+  out.taxes = w.taxes();
   auto unpack = [&](const void* dev, std::size_t n) {
     std::vector<uint8_t> raw(n * esz);
     w.put(raw.data(), dev, raw.size());
@@ -313,6 +352,7 @@ struct FdRun {  // :116-123
   std::vector<std::vector<std::uint64_t>> flag_counts;   // push-style variants
   std::vector<std::vector<float>> inbox;                 // per rank, W x batch x heads x (d+2)
   std::uint64_t launches = 0;
+  std::vector<tf_taxes> taxes;                           // per rank, measured on the device
 };
 
 inline FdRun run_fd(const DecodeProblem& p, Variant variant, const WorldConfig& cfg,
@@ -332,6 +372,7 @@ inline FdRun run_fd(const DecodeProblem& p, Variant variant, const WorldConfig& 
   const std::size_t heap = cfg.heap_bytes ? cfg.heap_bytes
                                           : 4 * W * row * 6 + 4 * std::size_t(B) * Hkv * 4096 * (d + 2) * 8 + (16u << 20);
   b200::World w(W, cfg.device_list(), heap, cfg.watchdog_secs);
+  w.apply(cfg);
   auto inbox = w.heap("fd.inbox.user", 4 * W * row);
   auto pack = [&](const float* src, std::size_t n) {
     std::vector<uint8_t> out(n * esz);
@@ -366,6 +407,7 @@ inline FdRun run_fd(const DecodeProblem& p, Variant variant, const WorldConfig& 
                               const_cast<const void* const*>(V.data()), O.data(), inbox.data(), nullptr));
   FdRun out;
   out.launches = tf_launch_count(w.w) - l0;
+  out.taxes = w.taxes();
   for (int r = 0; r < W; ++r) {
     std::vector<uint8_t> raw(esz * std::size_t(B) * H * d);
     w.put(raw.data(), O[r], raw.size());

@@ -7,6 +7,6 @@ ctypes binding (``_abi``) and a Python mirror of the reference API
 (``tilefabric``); the C++ mirror is include/tilefabric_b200/tilefabric.hpp.
 """
 from ._abi import lib, build  # noqa: F401
-from .tilefabric import (TileSpec, World, WorldConfig, ag, fd, uniform_reals,  # noqa: F401
+from .tilefabric import (TileSpec, World, WorldConfig, ag, fd, uniform_reals, inject_skew,  # noqa: F401
                          ConfigError, BoundsError, ShapeError, DeadlockError, WorldError,
                          EmptyAttentionError, NumericError, CudaError, Error)

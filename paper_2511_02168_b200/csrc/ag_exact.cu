@@ -144,6 +144,7 @@ tf_status ag_exact_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh,
     for (int r = 0; r < W; ++r) {
       if (!w->ranks[r].local) continue;
       cudaSetDevice(w->ranks[r].device);
+      TFB_CHECK(launch_skew(w, r, streams[r]));
       exact_gemm_kernel<<<grid, 256, 0, streams[r]>>>(
           shards, W, kw, kw, static_cast<const float*>(b[r]), static_cast<float*>(c[r]), m, n,
           bk, nullptr, 0, 0, w->watchdog_ns, w->err_of(r), r, -1);
@@ -191,6 +192,7 @@ tf_status ag_exact_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh,
       cudaSetDevice(w->ranks[r].device);
       SrcTable st{};
       st.p[0] = stage[r];
+      TFB_CHECK(launch_skew(w, r, streams[r]));
       exact_gemm_kernel<<<grid, 256, 0, streams[r]>>>(
           st, 1, k, k, static_cast<const float*>(b[r]), static_cast<float*>(c[r]), m, n, bk,
           nullptr, 0, 0, w->watchdog_ns, w->err_of(r), r, -1);
@@ -231,6 +233,7 @@ tf_status ag_exact_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh,
     cudaSetDevice(w->ranks[r].device);
     SrcTable st{};
     for (int s = 0; s < W; ++s) st.p[s] = stage[r] + size_t(s) * kw;
+    TFB_CHECK(launch_skew(w, r, streams[r]));
     exact_gemm_kernel<<<grid, 256, 0, streams[r]>>>(
         st, W, kw, k, static_cast<const float*>(b[r]), static_cast<float*>(c[r]), m, n, bk,
         reinterpret_cast<const uint64_t*>(w->ptr(r, fb.offset)), n_kb, epoch, w->watchdog_ns,

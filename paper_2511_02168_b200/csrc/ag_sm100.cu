@@ -765,6 +765,7 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
     // No exchange: the fused kernel degenerates to the GEMM over the shard.
     if (!w->ranks[0].local) return TF_OK;
     AgTcParams proto{};
+    TFB_CHECK(launch_skew(w, 0, streams[0]));
     TFB_CHECK(launch_gemm(w, 0, sh, a_shard[0], nullptr, b[0], c[0], nullptr, 0, 0, 0, proto,
                           streams[0], -1, sms));
     if (gathered && gathered[0])
@@ -813,6 +814,7 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
     for (int r = 0; r < W; ++r) {
       if (!w->ranks[r].local) continue;
       AgTcParams proto{};
+      TFB_CHECK(launch_skew(w, r, streams[r]));
       TFB_CHECK(launch_gemm(w, r, sh, nullptr, inbox_of(r), b[r], c[r], nullptr, 0, -1, 0, proto,
                             streams[r], -1, sms));
     }
@@ -827,6 +829,7 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
       proto.inbox = inbox_of(r);
       proto.ready_w = ready_of(r);
       proto.ctr = ctr_of(r, 0);
+      TFB_CHECK(launch_skew(w, r, streams[r]));
       TFB_CHECK(launch_gemm(w, r, sh, a_shard[r], inbox_of(r), b[r], c[r], ready_of(r), rb.epoch, r,
                             1, proto, streams[r], rb.id, sms));
     }
@@ -864,6 +867,7 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
   for (int r = 0; r < W; ++r) {
     if (!w->ranks[r].local) continue;
     AgTcParams proto{};
+    TFB_CHECK(launch_skew(w, r, streams[r]));
     TFB_CHECK(launch_gemm(w, r, sh, a_shard[r], inbox_of(r), b[r], c[r], ready_of(r), rb.epoch, r, 0,
                           proto, streams[r], rb.id, sms > push_ctas ? sms - push_ctas : 1));
     cudaEvent_t ev;

@@ -27,6 +27,8 @@ struct DevErr {
   // Three-Tax meter (taxmeter.hpp:45-63 on the device): every acquire wait
   // adds its spin time; barrier waits are kept apart (bulk-sync tax).
   unsigned long long waits, wait_ns, barriers, barrier_ns;
+  // The same, per waiting rank (a loopback device hosts several ranks).
+  unsigned long long rank_waits[64], rank_wait_ns[64], rank_barriers[64], rank_barrier_ns[64];
 };
 
 enum : int { kWaitSignal = 0, kWaitBarrier = 1, kNumeric = 2, kEmpty = 3 };
@@ -117,8 +119,10 @@ static __device__ __noinline__ bool wait_geq(const uint64_t* cell, uint64_t expe
                                       uint64_t aux) {
   const bool barrier = kind == kWaitBarrier;
   uint64_t seen = ld_acquire_sys(cell);
+  const int rk = rank & 63;
   if (seen >= expected) {
     atomicAdd(barrier ? &err->barriers : &err->waits, 1ull);
+    atomicAdd(barrier ? &err->rank_barriers[rk] : &err->rank_waits[rk], 1ull);
     return true;
   }
   const uint64_t t0 = globaltimer_ns();
@@ -144,6 +148,8 @@ static __device__ __noinline__ bool wait_geq(const uint64_t* cell, uint64_t expe
   const unsigned long long dt = globaltimer_ns() - t0;
   atomicAdd(barrier ? &err->barriers : &err->waits, 1ull);
   atomicAdd(barrier ? &err->barrier_ns : &err->wait_ns, dt);
+  atomicAdd(barrier ? &err->rank_barriers[rk] : &err->rank_waits[rk], 1ull);
+  atomicAdd(barrier ? &err->rank_barrier_ns[rk] : &err->rank_wait_ns[rk], dt);
   return ok;
 }
 

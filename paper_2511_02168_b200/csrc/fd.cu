@@ -65,6 +65,7 @@ struct FdRank {
   float* inbox;      // [W][B][Hq][d+2] local inbox (fold source)
   uint64_t* flags;   // [W][G] local flag board
   int rank;          // global rank id
+  uint64_t skew_ns;  // straggler delay before this rank's compute (fabric.hpp:59-62)
 };
 
 struct FdParams {
@@ -729,6 +730,8 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
     if (tr && threadIdx.x == 0) tr[i] = globaltimer_ns();
   };
   stamp(0);
+  __shared__ unsigned long long s_t0;  // CTA entry time (straggler model)
+  if (threadIdx.x == 0) s_t0 = globaltimer_ns();
   if (tr && threadIdx.x == 0)
     for (int i = 1; i < 16; ++i)
       if (i != 12 && i != 13) tr[i] = 0;
@@ -741,6 +744,11 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
     const int sp = item % P.S;
     const int g = (item / P.S) % G;
     const int lr = item / (unsigned(P.S) * G);
+    if (P.r[lr].skew_ns) {  // straggler model: this rank's compute starts late
+      if (threadIdx.x == 0)
+        while (globaltimer_ns() - s_t0 < P.r[lr].skew_ns) __nanosleep(1000);
+      __syncthreads();
+    }
     float* grp = P.ws + ((size_t(lr) * G + g) * P.S) * P.gs * wrl;
     float* wsrow = grp + size_t(sp) * P.gs * wrl;
     if (FAST) fast_split(P, lr, g, sp, wsrow, fsm);
@@ -1046,7 +1054,7 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
           const int r = rs[c0 + i];
           Q.r[i] = FdRank{q[r], k_shard[r], v_shard[r], out[r],
                           reinterpret_cast<float*>(w->ptr(r, pub_off)), inbox_of(r),
-                          reinterpret_cast<uint64_t*>(w->ptr(r, fb.offset)), r};
+                          reinterpret_cast<uint64_t*>(w->ptr(r, fb.offset)), r, w->skew_of(r)};
         }
         Q.err = w->err_of(lead);
         Q.ws = reinterpret_cast<float*>(w->ptr(lead, ws_off));

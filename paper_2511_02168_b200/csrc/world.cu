@@ -320,6 +320,20 @@ static tf_status check_device(int dev) {
   return TF_OK;
 }
 
+__global__ void skew_kernel(uint64_t ns) {
+  const uint64_t t0 = globaltimer_ns();
+  while (globaltimer_ns() - t0 < ns) __nanosleep(1000);
+}
+
+tf_status launch_skew(World* w, int r, cudaStream_t s) {
+  const uint64_t ns = w->skew_of(r);
+  if (!ns) return TF_OK;
+  cudaSetDevice(w->ranks[r].device);
+  skew_kernel<<<1, 1, 0, s>>>(ns);
+  TFB_CUDA(cudaGetLastError());
+  return TF_OK;
+}
+
 }  // namespace tfb
 
 using namespace tfb;
@@ -701,6 +715,17 @@ tf_status tf_world_barrier(tf_world* tw, int only_rank) {
   return s;
 }
 
+tf_status tf_world_set_skew(tf_world* tw, int rank, uint64_t delay_ns) {
+  if (!tw) return set_error(TF_ERR_CONFIG, "NULL world");
+  World* w = &tw->impl;
+  if (rank < 0 || rank >= w->W)  // fabric.hpp:100-105
+    return set_error(TF_ERR_CONFIG, "inject_skew: rank " + std::to_string(rank) +
+                                        " out of range for world_size " + std::to_string(w->W));
+  if (w->skew_ns.size() != size_t(w->W)) w->skew_ns.assign(w->W, 0);
+  w->skew_ns[rank] = delay_ns;
+  return TF_OK;
+}
+
 tf_status tf_tax_report(tf_world* tw, int rank, tf_taxes* out) {
   if (!tw || !out) return set_error(TF_ERR_CONFIG, "tf_tax_report: NULL argument");
   World* w = &tw->impl;
@@ -710,10 +735,12 @@ tf_status tf_tax_report(tf_world* tw, int rank, tf_taxes* out) {
   cudaSetDevice(w->ranks[rank].device);
   TFB_CUDA(cudaMemcpy(&rec, w->err_of(rank), sizeof(DevErr), cudaMemcpyDeviceToHost));
   out->launches = w->launches - w->tax_launch_base;
-  out->signal_waits = rec.waits;
-  out->wait_idle_ns = rec.wait_ns;
-  out->barrier_waits = rec.barriers;
-  out->bulk_sync_ns = rec.barrier_ns;
+  // This rank's own waits (a loopback device's record also keeps per-rank
+  // rows, so ranks sharing a device are still told apart).
+  out->signal_waits = rec.rank_waits[rank & 63];
+  out->wait_idle_ns = rec.rank_wait_ns[rank & 63];
+  out->barrier_waits = rec.rank_barriers[rank & 63];
+  out->bulk_sync_ns = rec.rank_barrier_ns[rank & 63];
   out->staged_bytes = w->staged_bytes.empty() ? 0 : w->staged_bytes[rank];
   return TF_OK;
 }

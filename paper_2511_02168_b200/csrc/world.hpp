@@ -65,6 +65,10 @@ struct World {
   uint64_t launches = 0;
   uint64_t tax_launch_base = 0;        // tf_tax_reset point
   std::vector<uint64_t> staged_bytes;  // per rank: bytes landed in staging/inbox tensors
+  // Straggler model (WorldConfig::skew, fabric.hpp:59-62, 100-110): extra
+  // delay at the start of the rank's first compute stage of every run.
+  std::vector<uint64_t> skew_ns;
+  uint64_t skew_of(int r) const { return skew_ns.empty() ? 0 : skew_ns[r]; }
   void stage(int r, uint64_t bytes) {
     if (staged_bytes.size() != size_t(W)) staged_bytes.assign(W, 0);
     staged_bytes[r] += bytes;
@@ -98,6 +102,12 @@ tf_status cuda_status(cudaError_t e, const char* what);
     tf_status _s = (call);                   \
     if (_s != TF_OK) return _s;              \
   } while (0)
+
+// Straggler delay (world.skew_ns[r] > 0): a one-thread %globaltimer sleep
+// kernel ahead of rank r's compute on stream s.  Not counted as a launch:
+// it stands in for the reference's precise_sleep inside ComputeScope
+// (fabric.hpp:695-706).
+tf_status launch_skew(World* w, int r, cudaStream_t s);
 
 // Heap/board helpers used by the pattern implementations.
 tf_status heap_get(World* w, const std::string& name, size_t bytes, size_t* offset);

@@ -62,10 +62,16 @@ class WorldConfig:
     watchdog: float = 0.0            # seconds; 0 -> TILEFABRIC_WATCHDOG_SECS or 10 s
     devices: Optional[Sequence[int]] = None  # None -> distinct GPUs if available, else loopback
     heap_bytes: int = 0              # 0 -> sized from the problem
+    skew: dict = field(default_factory=dict)  # rank -> seconds of straggler delay (fabric.hpp:59-62)
 
     def validate(self) -> None:
         if self.world_size < 1 or self.world_size > 64:
             raise ConfigError(f"world_size must be in [1, 64], got {self.world_size}")
+        for rank, delay in self.skew.items():
+            if rank < 0 or rank >= self.world_size:
+                raise ConfigError(f"skew rank {rank} out of range for world_size {self.world_size}")
+            if delay < 0:
+                raise ConfigError("skew delay must be >= 0")
 
     def device_list(self) -> List[int]:
         if self.devices is not None:
@@ -75,6 +81,15 @@ class WorldConfig:
         if n >= self.world_size and not loop:
             return list(range(self.world_size))
         return [0] * self.world_size
+
+
+def inject_skew(cfg: WorldConfig, rank: int, delay: float) -> None:
+    """fabric.hpp:100-110: add `delay` seconds to `rank`'s first compute stage."""
+    if rank < 0 or rank >= cfg.world_size:
+        raise ConfigError(f"inject_skew: rank {rank} out of range for world_size {cfg.world_size}")
+    if delay < 0:
+        raise ConfigError("inject_skew: delay must be >= 0")
+    cfg.skew[rank] = cfg.skew.get(rank, 0.0) + delay
 
 
 class World:
@@ -93,7 +108,10 @@ class World:
     @classmethod
     def from_config(cls, cfg: WorldConfig, heap_bytes: int) -> "World":
         cfg.validate()
-        return cls(cfg.world_size, cfg.device_list(), cfg.heap_bytes or heap_bytes, cfg.watchdog)
+        w = cls(cfg.world_size, cfg.device_list(), cfg.heap_bytes or heap_bytes, cfg.watchdog)
+        for rank, delay in cfg.skew.items():
+            w.set_skew(rank, delay)
+        return w
 
     def close(self) -> None:
         if self.handle:
@@ -139,6 +157,10 @@ class World:
         t = _abi.Taxes()
         _abi.check(self.lib.tf_tax_report(self.handle, rank, C.byref(t)))
         return t.as_dict()
+
+    def set_skew(self, rank: int, seconds: float) -> None:
+        """Straggler delay before `rank`'s first compute stage of every run."""
+        _abi.check(self.lib.tf_world_set_skew(self.handle, rank, int(round(seconds * 1e9))))
 
     def tax_reset(self) -> None:
         _abi.check(self.lib.tf_tax_reset(self.handle))

@@ -5,6 +5,7 @@
 // acceptance_test.cpp (cited per test).  The checker is the CPU oracle
 // (oracle/tf_oracle.c, pinned to the reference by tests/test_oracle_golden.py).
 // Built by __graft_entry__.build(); run by tests/test_cpp_shim_gpu.py.
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -233,6 +234,33 @@ int main() {
         for (auto c : counts) EXPECT_TRUE(c == 1);
     }
     EXPECT_THROW(fd::run_fd(p, fd::Variant::kBsp, quick_config(2), o), ConfigError);
+  });
+  // flash_decode_test.cpp:250-286: a 50 ms straggler; rank 0 pays it as a
+  // signal wait on source 1, nobody pays a barrier, the straggler barely waits.
+  run_test("FlashDecode.FusedWaitsTargetTheStraggler", [] {
+    auto cfg = quick_config(2);
+    inject_skew(cfg, 1, std::chrono::milliseconds(50));
+    const auto p = fd::make_problem(14, 2, 4, 64);
+    const auto run = fd::run_fused(p, cfg);
+    EXPECT_TRUE(run.taxes.size() == 2);
+    EXPECT_TRUE(run.taxes[0].wait_idle_ns >= 45000000ull);
+    EXPECT_TRUE(run.taxes[1].wait_idle_ns < 25000000ull);
+    for (const auto& t : run.taxes) EXPECT_TRUE(t.bulk_sync_ns == 0 && t.barrier_waits == 0);
+    EXPECT_THROW(inject_skew(cfg, 2, std::chrono::milliseconds(1)), ConfigError);
+    EXPECT_THROW(inject_skew(cfg, 0, std::chrono::milliseconds(-1)), ConfigError);
+  });
+  // acceptance_test.cpp:207-243: barriers per rank -- bsp 2, fused 0.
+  run_test("Acceptance.StructuralTaxCounts", [] {
+    const auto p = fd::make_problem(7, 2, 8, 64);
+    const auto bsp = fd::run_bsp(p, quick_config(4));
+    const auto fused = fd::run_fused(p, quick_config(4));
+    for (int r = 0; r < 4; ++r) {
+      EXPECT_TRUE(bsp.taxes[r].barrier_waits == 2);
+      EXPECT_TRUE(fused.taxes[r].barrier_waits == 0);
+    }
+    const auto agp = ag::make_problem(7, 8, 8, 16);
+    for (const auto& t : ag::run_pull(agp, quick_config(4)).taxes)
+      EXPECT_TRUE(t.barrier_waits == 0 && t.staged_bytes == 0);
   });
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;

@@ -75,3 +75,21 @@ def test_python_mirror_validation():
     f2.scale = float("inf")
     with pytest.raises(tf.ConfigError):
         f2.validate(4)
+
+
+def test_world_config_skew_and_devices():
+    # fabric_test.cpp:62-73: inject_skew validates eagerly and accumulates.
+    import pytest
+    import paper_2511_02168_b200 as tf
+    cfg = tf.WorldConfig(world_size=4, devices=[0, 0, 0, 0])
+    tf.inject_skew(cfg, 1, 0.010)
+    tf.inject_skew(cfg, 1, 0.005)
+    assert abs(cfg.skew[1] - 0.015) < 1e-12
+    cfg.validate()
+    assert cfg.device_list() == [0, 0, 0, 0]
+    for rank, delay in ((4, 0.001), (-1, 0.001), (0, -0.001)):
+        with pytest.raises(tf.ConfigError):
+            tf.inject_skew(cfg, rank, delay)
+    cfg.skew[7] = 0.001
+    with pytest.raises(tf.ConfigError):
+        cfg.validate()

@@ -98,6 +98,6 @@ def test_three_taxes_structure():
     base = tf.ag.run_baseline(p, tf.WorldConfig(world_size=w))
     assert pull.taxes[0]["barrier_waits"] == 0 and pull.taxes[0]["staged_bytes"] == 0
     assert push.taxes[0]["barrier_waits"] == 0
-    assert base.taxes[0]["barrier_waits"] == 2 * w
+    assert [t["barrier_waits"] for t in base.taxes] == [2] * w  # per rank
     for t in push.taxes + base.taxes:
         assert t["staged_bytes"] == p.m * p.k * 4

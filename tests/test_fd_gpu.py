@@ -170,11 +170,31 @@ def test_three_taxes_measured_on_device():
     bsp = tf.fd.run_bsp(p, tf.WorldConfig(world_size=w))
     assert fused.taxes[0]["barrier_waits"] == 0
     assert fused.launches == 1
-    # loopback: the W ranks share one device's counters
-    assert bsp.taxes[0]["barrier_waits"] == 2 * w
+    # per rank, even though the loopback ranks share one device
+    assert [t["barrier_waits"] for t in bsp.taxes] == [2] * w
     for t in fused.taxes + bsp.taxes:
         assert t["staged_bytes"] == w * wire_bytes
-    assert fused.taxes[0]["signal_waits"] >= w  # one fold wait per source (per group)
+    for t in fused.taxes:
+        assert t["signal_waits"] >= w  # one fold wait per source (per group)
+
+
+def test_fused_waits_target_the_straggler():
+    # flash_decode_test.cpp:250-286: with rank 1 delayed 50 ms, rank 0 pays
+    # about the delay waiting for source 1, nobody pays a barrier, and the
+    # straggler itself barely waits (every other row landed long ago).
+    delay = 0.05
+    cfg = tf.WorldConfig(world_size=2)
+    tf.inject_skew(cfg, 1, delay)
+    p = tf.fd.make_problem(14, 2, 4, 64)
+    run = tf.fd.run_fused(p, cfg)
+    eps = 0.005
+    assert run.taxes[0]["wait_idle_ns"] >= (delay - eps) * 1e9
+    assert run.taxes[1]["wait_idle_ns"] < delay / 2 * 1e9
+    assert all(t["barrier_waits"] == 0 and t["bulk_sync_ns"] == 0 for t in run.taxes)
+    with pytest.raises(tf.ConfigError):
+        tf.inject_skew(cfg, 2, delay)
+    with pytest.raises(tf.ConfigError):
+        tf.inject_skew(cfg, 0, -1.0)
 
 
 def test_fold_by_arrival_option(oracle):

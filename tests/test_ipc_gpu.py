@@ -126,6 +126,27 @@ def _worker(rank, world, port, q):
             dist.all_gather_object(outs, o.tobytes())
             out.setdefault("fd_ranks_equal", []).append(all(x == outs[0] for x in outs))
             dist.barrier()
+
+        # ---- straggler (acceptance_test.cpp:246-281): rank 1 starts its
+        # compute 50 ms late; BSP makes rank 0 pay it at a barrier, fused
+        # has no barrier (rank 0 waits on source 1's flag instead) ----
+        _abi.check(L.tf_world_set_skew(h, 1, 50_000_000))
+        strag = {}
+        for name, variant in (("bsp", _abi.TF_FD_BSP), ("fused", _abi.TF_FD_FUSED)):
+            torch.cuda.synchronize()
+            dist.barrier()
+            _abi.check(L.tf_tax_reset(h))
+            dist.barrier()
+            _abi.check(L.tf_flash_decode(h, variant, C.byref(fshape), tbl(qd.data_ptr()), tbl(kd.data_ptr()),
+                                         tbl(vd.data_ptr()), tbl(od.data_ptr()), None, None))
+            t = _abi.Taxes()
+            _abi.check(L.tf_tax_report(h, rank, C.byref(t)))
+            strag[name] = t.as_dict()
+            out.setdefault("fd_err", []).append(O.head_rel_err(od.cpu().numpy(), want_fd))
+        _abi.check(L.tf_world_set_skew(h, 1, 0))
+        out["straggler"] = strag
+        out["rank"] = rank
+        dist.barrier()
         L.tf_world_destroy(h)
     except Exception as e:  # surface the failure to the parent
         out["error"] = repr(e)
@@ -151,3 +172,10 @@ def test_two_process_ipc_world_on_one_gpu():
             assert err <= 4e-3, (name, err)
         assert all(e <= 1e-5 for e in r["fd_err"]), r
         assert all(r["fd_ranks_equal"]), r
+        st = r["straggler"]
+        assert st["fused"]["barrier_waits"] == 0 and st["fused"]["bulk_sync_ns"] == 0, st
+        if r["rank"] == 0:
+            assert st["bsp"]["bulk_sync_ns"] >= 40e6, st   # paid the 50 ms at a barrier
+            assert st["fused"]["wait_idle_ns"] >= 40e6, st  # waited on source 1's flag instead
+        else:
+            assert st["fused"]["wait_idle_ns"] < 25e6, st   # the straggler barely waits
