@@ -225,6 +225,9 @@ tf_status tf_uniform_reals(uint64_t seed, size_t n, float* out);
  * error record (watchdog, NumericError, EmptyAttentionError). */
 tf_status tf_world_sync(tf_world* w);
 
+/* GPUs visible to this process (0 without a driver/GPU; never fails). */
+int tf_device_count(void);
+
 /* Number of kernels this library launched since world creation (bench.py's
  * gpu_launches evidence). */
 uint64_t tf_launch_count(const tf_world* w);

@@ -123,6 +123,7 @@ SIGNATURES = {
     "tf_tax_report": (C.c_int, [_P, C.c_int, C.POINTER(Taxes)]),
     "tf_tax_reset": (C.c_int, [_P]),
     "tf_world_set_skew": (C.c_int, [_P, C.c_int, C.c_uint64]),
+    "tf_device_count": (C.c_int, []),
 }
 
 _lib = None

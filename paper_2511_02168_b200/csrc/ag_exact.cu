@@ -250,4 +250,13 @@ tf_status ag_exact_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh,
   return TF_OK;
 }
 
+// Force-load this file's kernels on the current device (lazy module loading
+// would otherwise load them inside the first schedule, serializing streams).
+void ag_exact_preload() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, exact_gemm_kernel);
+  cudaFuncGetAttributes(&a, exact_gather_kernel);
+  cudaFuncGetAttributes(&a, exact_push_kernel);
+}
+
 }  // namespace tfb

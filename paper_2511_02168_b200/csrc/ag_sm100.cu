@@ -879,4 +879,12 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
   return TF_OK;
 }
 
+void ag_sm100_preload() {  // see ag_exact_preload
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, ag_gemm_sm100_kernel<1>);
+  cudaFuncGetAttributes(&a, ag_gemm_sm100_kernel<2>);
+  cudaFuncGetAttributes(&a, ag_push_kernel);
+  cudaFuncGetAttributes(&a, splitk_reduce_kernel);
+}
+
 }  // namespace tfb

@@ -278,6 +278,7 @@ __device__ __forceinline__ int fast_d(int i, int j, int r) {
 
 // One warp: keys [kb, ke) of the group's stream; leaves its log2-domain
 // partial for the 8 heads in smem (m2[8], l[8], o[8][128]).
+template <bool HILO>
 __device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
                                 const __nv_bfloat16* V, const __nv_bfloat16* Q, size_t kb,
                                 size_t ke, float* sm_m, float* sm_l, float* sm_o, int* bad) {
@@ -340,11 +341,25 @@ __device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
     const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);
     m0 = mn0;
     m1 = mn1;
-    const __nv_bfloat162 p01 = __floats2bfloat162_rn(exp2f(x0 - mn0), exp2f(x1 - mn1));
-    const __nv_bfloat162 p23 = __floats2bfloat162_rn(exp2f(x2 - mn0), exp2f(x3 - mn1));
-    // Normalizer from the same rounded weights the PV product uses.
-    l0 = l0 * al0 + (__low2float(p01) + __low2float(p23));
-    l1 = l1 * al1 + (__high2float(p01) + __high2float(p23));
+    // HILO (fp32 output requested): the weights reach the tensor core as a
+    // bf16 hi + lo pair (P = P_hi + P_lo to ~2^-16 relative) at one extra
+    // MMA per PV step, which gives fp32-grade attention on bf16 K/V.  Else
+    // (bf16 output, whose own rounding is 2^-9) a single bf16 P, with the
+    // normalizer taken from the same rounded weights.
+    const float e0 = exp2f(x0 - mn0), e1 = exp2f(x1 - mn1);
+    const float e2 = exp2f(x2 - mn0), e3 = exp2f(x3 - mn1);
+    const __nv_bfloat162 p01 = __floats2bfloat162_rn(e0, e1);
+    const __nv_bfloat162 p23 = __floats2bfloat162_rn(e2, e3);
+    __nv_bfloat162 r01, r23;
+    if (HILO) {
+      r01 = __floats2bfloat162_rn(e0 - __low2float(p01), e1 - __high2float(p01));
+      r23 = __floats2bfloat162_rn(e2 - __low2float(p23), e3 - __high2float(p23));
+      l0 = l0 * al0 + (e0 + e2);
+      l1 = l1 * al1 + (e1 + e3);
+    } else {
+      l0 = l0 * al0 + (__low2float(p01) + __low2float(p23));
+      l1 = l1 * al1 + (__high2float(p01) + __high2float(p23));
+    }
 #pragma unroll
     for (int x = 0; x < 8; ++x) {
       o[x][0] *= al0;
@@ -354,6 +369,11 @@ __device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
     }
     const uint32_t pb0 = movtrans(*reinterpret_cast<const uint32_t*>(&p01));
     const uint32_t pb1 = movtrans(*reinterpret_cast<const uint32_t*>(&p23));
+    uint32_t rb0 = 0, rb1 = 0;
+    if (HILO) {
+      rb0 = movtrans(*reinterpret_cast<const uint32_t*>(&r01));
+      rb1 = movtrans(*reinterpret_cast<const uint32_t*>(&r23));
+    }
     // O^T += V^T . P^T: tile (i, jp) covers d rows fast_d(i, 2jp, .) and
     // fast_d(i, 2jp+1, .).
 #pragma unroll
@@ -365,6 +385,7 @@ __device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
         const uint32_t a2 = movtrans(w4(v_b[i], 2 * jp));
         const uint32_t a3 = movtrans(w4(v_b[i], 2 * jp + 1));
         mma_bf16(o[2 * i + jp], a0, a1, a2, a3, pb0, pb1);
+        if (HILO) mma_bf16(o[2 * i + jp], a0, a1, a2, a3, rb0, rb1);
       }
     }
   }
@@ -403,6 +424,7 @@ struct FastSmem {
   int bad;
 };
 
+template <bool HILO>
 __device__ void fast_split(const FdParams& P, int lr, int g, int sp, float* wsrow,
                            FastSmem& sm) {
   const FdRank& R = P.r[lr];
@@ -419,7 +441,7 @@ __device__ void fast_split(const FdParams& P, int lr, int g, int sp, float* wsro
   for (int i = threadIdx.x; i < 8 * 16; i += blockDim.x) sm.q[i] = reinterpret_cast<const uint4*>(Q)[i];
   __syncthreads();
   trace_at(P, 12);
-  fast_warp_range(P, K, V, reinterpret_cast<const __nv_bfloat16*>(sm.q), wb, we, sm.m[warp], sm.l[warp],
+  fast_warp_range<HILO>(P, K, V, reinterpret_cast<const __nv_bfloat16*>(sm.q), wb, we, sm.m[warp], sm.l[warp],
                   sm.o[warp], &sm.bad);
   __syncthreads();
   trace_at(P, 13);
@@ -716,7 +738,8 @@ __device__ __noinline__ void fold_ws(const FdParams& P, int lr, int g, float* gr
 }
 
 // ---- the persistent kernel ------------------------------------------------
-template <bool FAST>
+// MODE: 0 generic split, 1 fast split with bf16 P, 2 fast split with hi/lo P.
+template <int MODE>
 __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __grid_constant__ FdParams P) {
   __shared__ unsigned int s_item;
   __shared__ int s_last, s_src;
@@ -751,7 +774,8 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
     }
     float* grp = P.ws + ((size_t(lr) * G + g) * P.S) * P.gs * wrl;
     float* wsrow = grp + size_t(sp) * P.gs * wrl;
-    if (FAST) fast_split(P, lr, g, sp, wsrow, fsm);
+    if (MODE == 2) fast_split<true>(P, lr, g, sp, wsrow, fsm);
+    else if (MODE == 1) fast_split<false>(P, lr, g, sp, wsrow, fsm);
     else generic_split(P, lr, g, sp, wsrow);
     stamp(1);
     // Two-level ticketed fold.  Level 1: the last split of each chunk of
@@ -954,6 +978,16 @@ static tf_status fd_validate(World* w, const tf_fd_shape* s, const void* const* 
   return TF_OK;
 }
 
+void fd_preload() {  // see ag_exact_preload
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, fd_attention_kernel<0>);
+  cudaFuncGetAttributes(&a, fd_attention_kernel<1>);
+  cudaFuncGetAttributes(&a, fd_attention_kernel<2>);
+  cudaFuncGetAttributes(&a, fd_push_kernel);
+  cudaFuncGetAttributes(&a, fd_gather_kernel);
+  cudaFuncGetAttributes(&a, fd_fold_kernel);
+}
+
 }  // namespace tfb
 
 using namespace tfb;
@@ -1043,12 +1077,17 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   P.flag_epoch = fb.epoch;
   // One attention launch per device (a loopback device runs all its ranks
   // in one persistent grid, so the fused waits can never starve a producer).
+  // The fused schedule shares one launch per device (its waits need every
+  // local producer resident); the others never wait inside the attention
+  // kernel, so each rank gets its own launch on its own stream, as in the
+  // reference (a straggling rank then delays only its own stage).
   auto launch_attention = [&](int push, int fold_inline) -> tf_status {
+    const size_t per_launch = fold_inline ? size_t(kMaxLocal) : 1;
     for (auto& kv : by_dev) {
       const std::vector<int>& rs = kv.second;
-      for (size_t c0 = 0; c0 < rs.size(); c0 += kMaxLocal) {
+      for (size_t c0 = 0; c0 < rs.size(); c0 += per_launch) {
         FdParams Q = P;
-        Q.nlocal = int(std::min(rs.size() - c0, size_t(kMaxLocal)));
+        Q.nlocal = int(std::min(rs.size() - c0, per_launch));
         const int lead = rs[c0];
         for (int i = 0; i < Q.nlocal; ++i) {
           const int r = rs[c0 + i];
@@ -1075,17 +1114,19 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
         Q.by_arrival = variant == TF_FD_FUSED_BY_ARRIVAL;
         cudaSetDevice(kv.first);
         const unsigned items = unsigned(Q.nlocal) * G * S_eff;
+        // Tensor-core split with bf16 P for bf16 output, hi/lo P when the
+        // caller asked for fp32 output; the generic split otherwise.
+        const int mode = !fast ? 0 : (sh.out_dtype == TF_F32 ? 2 : 1);
+        const void* kfn = mode == 0 ? reinterpret_cast<const void*>(fd_attention_kernel<0>)
+                        : mode == 1 ? reinterpret_cast<const void*>(fd_attention_kernel<1>)
+                                    : reinterpret_cast<const void*>(fd_attention_kernel<2>);
         int per_sm = 1;
-        if (fast)
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fd_attention_kernel<true>,
-                                                        kFastThreads, 0);
-        else
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fd_attention_kernel<false>,
-                                                        kFastThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kFastThreads, 0);
         const unsigned grid =
             std::max(1u, std::min(items, unsigned(std::max(per_sm, 1) * w->sm_count)));
-        if (fast) fd_attention_kernel<true><<<grid, kFastThreads, 0, st[lead]>>>(Q);
-        else fd_attention_kernel<false><<<grid, kFastThreads, 0, st[lead]>>>(Q);
+        if (mode == 0) fd_attention_kernel<0><<<grid, kFastThreads, 0, st[lead]>>>(Q);
+        else if (mode == 1) fd_attention_kernel<1><<<grid, kFastThreads, 0, st[lead]>>>(Q);
+        else fd_attention_kernel<2><<<grid, kFastThreads, 0, st[lead]>>>(Q);
         TFB_CUDA(cudaGetLastError());
         ++w->launches;
         // Ranks sharing the launch are complete when it is: order their streams.
@@ -1108,6 +1149,11 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   for (int r = 0; r < W; ++r)
     if (w->ranks[r].local) w->stage(r, sizeof(float) * W * row_floats);
   if (fused) return launch_attention(/*push=*/1, /*fold_inline=*/1);
+  // Everything the later stages allocate exists before the first launch.
+  TFB_CHECK(ensure_barrier(w));
+  size_t stage_off = 0;
+  if (variant == TF_FD_BSP)
+    TFB_CHECK(heap_get(w, "fd.stage" + geo, sizeof(float) * W * row_floats, &stage_off));
   TFB_CHECK(launch_attention(0, 0));
   TFB_CHECK(world_barrier(w, st));
   FdParams PP = P;
@@ -1117,8 +1163,6 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
     return x;
   };
   if (variant == TF_FD_BSP) {
-    size_t stage_off;
-    TFB_CHECK(heap_get(w, "fd.stage" + geo, sizeof(float) * W * row_floats, &stage_off));
     FdParams G2 = PP;
     for (int r = 0; r < W; ++r) G2.inbox_all[r] = reinterpret_cast<float*>(w->ptr(r, pub_off));
     for (int r = 0; r < W; ++r) {

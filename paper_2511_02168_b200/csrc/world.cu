@@ -266,27 +266,39 @@ __global__ void soak_kernel(uint32_t* const* mail, uint64_t* const* flags,
   }
 }
 
-tf_status world_barrier(World* w, const std::vector<cudaStream_t>& streams, int only_rank) {
+tf_status ensure_barrier(World* w) {
+  if (w->barrier_ready) return TF_OK;
   BoardEntry b;
   TFB_CHECK(board_get(w, "tf.barrier", 1, 1, &b));
-  const uint64_t epoch = ++w->barrier_epoch;
   std::vector<uint64_t*> cells(w->W);
   for (int r = 0; r < w->W; ++r) cells[r] = reinterpret_cast<uint64_t*>(w->ptr(r, b.offset));
-  size_t off;
-  TFB_CHECK(heap_get(w, "tf.barrier.table", sizeof(uint64_t*) * 64, &off));
+  TFB_CHECK(heap_get(w, "tf.barrier.table", sizeof(uint64_t*) * 64, &w->barrier_table_off));
+  for (int r = 0; r < w->W; ++r) {
+    if (!w->ranks[r].local) continue;
+    TFB_CUDA(cudaSetDevice(w->ranks[r].device));
+    TFB_CUDA(cudaMemcpy(w->ptr(r, w->barrier_table_off), cells.data(), sizeof(uint64_t*) * w->W,
+                        cudaMemcpyHostToDevice));
+  }
+  w->barrier_ready = true;
+  return TF_OK;
+}
+
+tf_status world_barrier(World* w, const std::vector<cudaStream_t>& streams, int only_rank) {
+  TFB_CHECK(ensure_barrier(w));
+  const int board = w->boards["tf.barrier"].id;
+  const uint64_t epoch = ++w->barrier_epoch;
   for (int r = 0; r < w->W; ++r) {
     if (!w->ranks[r].local || (only_rank >= 0 && r != only_rank)) continue;
     cudaSetDevice(w->ranks[r].device);
-    uint64_t** table = reinterpret_cast<uint64_t**>(w->ptr(r, off));
-    TFB_CUDA(cudaMemcpyAsync(table, cells.data(), sizeof(uint64_t*) * w->W,
-                             cudaMemcpyHostToDevice, streams[r]));
-    barrier_kernel<<<1, 32, 0, streams[r]>>>(table, r, w->W, epoch, w->watchdog_ns, w->err_of(r),
-                                             b.id);
+    uint64_t** table = reinterpret_cast<uint64_t**>(w->ptr(r, w->barrier_table_off));
+    barrier_kernel<<<1, 32, 0, streams[r]>>>(table, r, w->W, epoch, w->watchdog_ns, w->err_of(r), board);
     TFB_CUDA(cudaGetLastError());
     ++w->launches;
   }
   return TF_OK;
 }
+
+__global__ void skew_kernel(uint64_t ns);
 
 static tf_status world_init_common(World* w) {
   for (const RankRes& rr : w->ranks) {
@@ -296,6 +308,17 @@ static tf_status world_init_common(World* w) {
     TFB_CUDA(cudaMalloc(reinterpret_cast<void**>(&e), sizeof(DevErr)));
     TFB_CUDA(cudaMemset(e, 0, sizeof(DevErr)));
     w->errs[rr.device] = e;
+    // Load every kernel now, not lazily inside a schedule's first call.
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, barrier_kernel);
+    cudaFuncGetAttributes(&a, signal_kernel);
+    cudaFuncGetAttributes(&a, wait_kernel);
+    cudaFuncGetAttributes(&a, soak_kernel);
+    cudaFuncGetAttributes(&a, skew_kernel);
+    ag_exact_preload();
+    ag_sm100_preload();
+    fd_preload();
+    TFB_CUDA(cudaGetLastError());
   }
   // Heap/record memsets ran on the legacy stream; the world's non-blocking
   // streams must not overtake them.
@@ -482,6 +505,7 @@ tf_status tf_world_ipc_import(tf_world* tw, const void* all_handles) {
     w->ranks[r].heap = static_cast<char*>(p);
     w->ranks[r].device = -1;
   }
+  w->barrier_ready = false;  // the cell table needs the peers' heaps
   return TF_OK;
 }
 
@@ -536,6 +560,7 @@ tf_status tf_world_reset_heap(tf_world* tw) {
   w->board_names.clear();
   w->heap_used = 0;
   w->barrier_epoch = w->ag_epoch = w->fd_epoch = 0;
+  w->barrier_ready = false;
   w->ag_flags = FlagSnapshot{};
   w->fd_flags = FlagSnapshot{};
   for (int r = 0; r < w->W; ++r) {
@@ -713,6 +738,15 @@ tf_status tf_world_barrier(tf_world* tw, int only_rank) {
     set_error(s, msg);
   }
   return s;
+}
+
+int tf_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
 }
 
 tf_status tf_world_set_skew(tf_world* tw, int rank, uint64_t delay_ns) {

@@ -74,6 +74,8 @@ struct World {
     staged_bytes[r] += bytes;
   }
   uint64_t barrier_epoch = 0;
+  bool barrier_ready = false;     // tf.barrier board + its device pointer table written
+  size_t barrier_table_off = 0;
   uint64_t ag_epoch = 0;
   uint64_t fd_epoch = 0;
   FlagSnapshot ag_flags, fd_flags;
@@ -108,6 +110,17 @@ tf_status cuda_status(cudaError_t e, const char* what);
 // it stands in for the reference's precise_sleep inside ComputeScope
 // (fabric.hpp:695-706).
 tf_status launch_skew(World* w, int r, cudaStream_t s);
+
+// Allocate the world barrier's board and per-rank cell table once, with
+// synchronous copies, before a schedule launches anything: a first-call
+// allocation (device sync / pageable copy) inside a schedule would
+// serialize the ranks' streams and hide the barrier waits being measured.
+tf_status ensure_barrier(World* w);
+
+// Per-file kernel preloads, run for every local device at world creation.
+void ag_exact_preload();
+void ag_sm100_preload();
+void fd_preload();
 
 // Heap/board helpers used by the pattern implementations.
 tf_status heap_get(World* w, const std::string& name, size_t bytes, size_t* offset);

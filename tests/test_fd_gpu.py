@@ -107,9 +107,15 @@ def test_gqa_bf16_fast_path_vs_oracle(oracle):
                 np.repeat(kb[b, g:g + 1], gs, 0), np.repeat(vb[b, g:g + 1], gs, 0), p.scale)
     for w in (1, 2, 4):
         for variant in (V.kFused, V.kBsp):
+            # fp32 output: the tensor-core split feeds P as a bf16 hi + lo
+            # pair, so bf16 K/V decode is fp32-grade against the oracle.
             run = tf.fd.run_fd(p, variant, tf.WorldConfig(world_size=w), dtype=1, out_dtype=0)
             err = oracle.head_rel_err(run.out[0].reshape(B * Hq, d), want.reshape(B * Hq, d))
-            assert err <= 2e-3, (w, variant, err)
+            assert err <= 1e-4, (w, variant, err)
+            # bf16 output: single bf16 P; output rounding (2^-9) dominates.
+            run = tf.fd.run_fd(p, variant, tf.WorldConfig(world_size=w), dtype=1, out_dtype=1)
+            err = oracle.head_rel_err(run.out[0].reshape(B * Hq, d).astype(np.float32), want.reshape(B * Hq, d))
+            assert err <= 8e-3, (w, variant, err)
 
 
 def test_rejects_bad_shapes():
@@ -152,7 +158,7 @@ def test_gqa_bf16_eight_rank_loopback(oracle):
                                             np.repeat(kb[0, g:g + 1], gs, 0), np.repeat(vb[0, g:g + 1], gs, 0),
                                             p.scale) for g in range(Hkv)])
     run = tf.fd.run_fused(p, tf.WorldConfig(world_size=8), dtype=1, out_dtype=0)
-    assert oracle.head_rel_err(run.out[0], want) <= 2e-3
+    assert oracle.head_rel_err(run.out[0], want) <= 1e-4
     for out in run.out[1:]:
         assert np.array_equal(out.view(np.uint32), run.out[0].view(np.uint32))
     for counts in run.flag_counts:
