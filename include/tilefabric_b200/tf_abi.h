@@ -167,6 +167,28 @@ tf_status tf_ag_gemm_async(tf_world* w, tf_ag_variant variant,
                            const tf_ag_shape* shape, void* const* a_shard,
                            const void* const* b, void* const* c,
                            void* const* gathered_opt, void* const* streams);
+/* Host-buffer All-Gather+GEMM: the reference's calling convention, where
+ * AgGemmProblem holds host vectors and AgGemmRun returns host C
+ * (ag_gemm.hpp:47-99, 134-305).  a_host[r]: rank r's m x kw shard, b_host[r]:
+ * k x n, c_host[r]: m x n output, all row-major host memory of `dtype`.  The
+ * shard is placed in the symmetric heap, B streams to the device in column
+ * slabs and each slab's GEMM starts as soon as it has landed (slab 0 runs
+ * the variant's exchange, later slabs reuse the gathered operand); C slabs
+ * stream back as their GEMMs retire -- H2D, compute and D2H overlap on three
+ * streams per rank.  Pinned host memory (cudaHostAlloc/cudaHostRegister)
+ * gives the full overlap; pageable memory is correct but the driver
+ * serialises it.  Results are bitwise those of tf_ag_gemm on the same
+ * operands (the GEMM of a column slab is the same per-tile computation).
+ * The _async form returns once the work is enqueued on the per-rank
+ * streams (the host buffers must stay valid until they are idle). */
+tf_status tf_ag_gemm_host(tf_world* w, tf_ag_variant variant, const tf_ag_shape* shape,
+                          const void* const* a_host, const void* const* b_host,
+                          void* const* c_host, void* const* streams);
+tf_status tf_ag_gemm_host_async(tf_world* w, tf_ag_variant variant,
+                                const tf_ag_shape* shape, const void* const* a_host,
+                                const void* const* b_host, void* const* c_host,
+                                void* const* streams);
+
 /* Flag snapshot after the last push run (ag_gemm.hpp:296-302): per rank,
  * `count` counters normalised so that one completed run reads 1.
  * *count receives the number of cells per rank. */

@@ -643,17 +643,18 @@ tf_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t ou
 static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void* shard,
                              const void* inbox, const void* b, void* c, const uint64_t* ready,
                              uint64_t epoch, int own, int gather, const AgTcParams& proto,
-                             cudaStream_t st, int board, unsigned grid_cap) {
+                             cudaStream_t st, int board, unsigned grid_cap, const AgLayout& lay) {
   const int W = w->W;
   const size_t kw = sh.k / W;
+  const size_t ldb = lay.ldb ? lay.ldb : sh.n, ldc = lay.ldc ? lay.ldc : sh.n;
   CUtensorMap mOwn{}, mInbox{}, mB{}, mC{};
   // C: 64-column x 32-row boxes, one per epilogue warp per store.
-  TFB_CHECK(make_map(&mC, c, sh.n, sh.m, sh.n, 64, 32));
+  TFB_CHECK(make_map(&mC, c, sh.n, sh.m, ldc, 64, 32));
   if (shard) TFB_CHECK(make_map(&mOwn, shard, kw, sh.m, kw, BK, BM));
   if (inbox) TFB_CHECK(make_map(&mInbox, inbox, sh.k, sh.m, sh.k, BK, BM));
   if (!shard) mOwn = mInbox;
   if (!inbox) mInbox = mOwn;
-  TFB_CHECK(make_map(&mB, b, sh.n, sh.k, sh.n, 64, BK));
+  TFB_CHECK(make_map(&mB, b, sh.n, sh.k, ldb, 64, BK));
   AgTcParams p = proto;
   p.M = int(sh.m);
   p.N = int(sh.n);
@@ -690,6 +691,7 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
     if (busy * 2 <= grid_cap) ks = int(std::min<unsigned>(grid_cap / busy, 16));
     ks = std::min(ks, std::max(1, p.kb_total / 4));  // >= 4 k-blocks per split
     if (const char* e = std::getenv("TFB_KSPLIT")) ks = std::max(1, std::atoi(e));
+    if (ldc != sh.n) ks = 1;  // slab of a wider C: the reduce writes dense rows
     p.kbs = (p.kb_total + ks - 1) / ks;
     p.ksplit = (p.kb_total + p.kbs - 1) / p.kbs;
   }
@@ -749,7 +751,7 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
 
 tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, void* const* a_shard,
                       const void* const* b, void* const* c, void* const* gathered,
-                      const std::vector<cudaStream_t>& streams) {
+                      const std::vector<cudaStream_t>& streams, const AgLayout& lay) {
   const int W = w->W;
   const size_t m = sh.m, n = sh.n, k = sh.k, kw = k / W;
   if (kw % BK != 0)
@@ -767,7 +769,7 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
     AgTcParams proto{};
     TFB_CHECK(launch_skew(w, 0, streams[0]));
     TFB_CHECK(launch_gemm(w, 0, sh, a_shard[0], nullptr, b[0], c[0], nullptr, 0, 0, 0, proto,
-                          streams[0], -1, sms));
+                          streams[0], -1, sms, lay));
     if (gathered && gathered[0])
       TFB_CUDA(cudaMemcpyAsync(gathered[0], a_shard[0], m * k * 2, cudaMemcpyDefault, streams[0]));
     return TF_OK;
@@ -781,7 +783,7 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
   BoardEntry rb;
   // Only the signalling schedules (pull, push) advance the ready board's
   // epoch; BASELINE never touches it (every rank/process must agree on e).
-  if (variant == TF_AG_BASELINE) {
+  if (variant == TF_AG_BASELINE || lay.inbox_complete) {
     const std::string bname = "ag.ready[" + std::to_string(num_m) + "x" + std::to_string(W) + "]";
     TFB_CHECK(board_get(w, bname, num_m, W, &rb));
     rb.epoch = w->boards[bname].epoch;
@@ -798,6 +800,20 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
   auto ctr_of = [&](int r, int slot) { return reinterpret_cast<unsigned int*>(w->ptr(r, ctr_off)) + slot * 4; };
   // Every schedule lands the gathered operand in HBM once per rank (PULL via
   // the gather warps; the reference's pull re-fetches tiles instead).
+  if (lay.inbox_complete) {
+    // The inbox already holds the gathered A (an earlier run on these
+    // streams): the GEMM alone, ungated, own k-range from the shard.
+    for (int r = 0; r < W; ++r) {
+      if (!w->ranks[r].local) continue;
+      AgTcParams proto{};
+      // Same k order as the schedule that gathered (BASELINE: ascending,
+      // pull/push: own shard first), so every slab matches a one-shot run.
+      const int own = variant == TF_AG_BASELINE ? -1 : r;
+      TFB_CHECK(launch_gemm(w, r, sh, own < 0 ? nullptr : a_shard[r], inbox_of(r), b[r], c[r], nullptr, 0,
+                            own, 0, proto, streams[r], -1, sms, lay));
+    }
+    return TF_OK;
+  }
   for (int r = 0; r < W; ++r)
     if (w->ranks[r].local) w->stage(r, m * k * 2);
 
@@ -816,7 +832,7 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
       AgTcParams proto{};
       TFB_CHECK(launch_skew(w, r, streams[r]));
       TFB_CHECK(launch_gemm(w, r, sh, nullptr, inbox_of(r), b[r], c[r], nullptr, 0, -1, 0, proto,
-                            streams[r], -1, sms));
+                            streams[r], -1, sms, lay));
     }
     return TF_OK;
   }
@@ -831,7 +847,7 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
       proto.ctr = ctr_of(r, 0);
       TFB_CHECK(launch_skew(w, r, streams[r]));
       TFB_CHECK(launch_gemm(w, r, sh, a_shard[r], inbox_of(r), b[r], c[r], ready_of(r), rb.epoch, r,
-                            1, proto, streams[r], rb.id, sms));
+                            1, proto, streams[r], rb.id, sms, lay));
     }
     return TF_OK;
   }
@@ -869,7 +885,7 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
     AgTcParams proto{};
     TFB_CHECK(launch_skew(w, r, streams[r]));
     TFB_CHECK(launch_gemm(w, r, sh, a_shard[r], inbox_of(r), b[r], c[r], ready_of(r), rb.epoch, r, 0,
-                          proto, streams[r], rb.id, sms > push_ctas ? sms - push_ctas : 1));
+                          proto, streams[r], rb.id, sms > push_ctas ? sms - push_ctas : 1, lay));
     cudaEvent_t ev;
     TFB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     TFB_CUDA(cudaEventRecord(ev, w->ranks[r].side));

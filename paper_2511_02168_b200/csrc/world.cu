@@ -517,6 +517,10 @@ tf_status tf_world_destroy(tf_world* tw) {
     if (rr.local) cudaSetDevice(rr.device);
     if (rr.stream) cudaStreamSynchronize(rr.stream), cudaStreamDestroy(rr.stream);
     if (rr.side) cudaStreamSynchronize(rr.side), cudaStreamDestroy(rr.side);
+    if (rr.h2d) cudaStreamSynchronize(rr.h2d), cudaStreamDestroy(rr.h2d);
+    if (rr.d2h) cudaStreamSynchronize(rr.d2h), cudaStreamDestroy(rr.d2h);
+    for (void* p : rr.scratch)
+      if (p) cudaFree(p);
   }
   for (int r = 0; r < (int)w->ranks.size(); ++r) {
     RankRes& rr = w->ranks[r];

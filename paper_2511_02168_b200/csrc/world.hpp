@@ -24,6 +24,11 @@ struct RankRes {
   bool owns_heap = false;     // allocated (vs IPC-opened) here
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // producer stream (push variants)
+  // Host-buffer runs (ag_host.cu): copy-engine streams and device operand
+  // buffers, created on first use, grow-only.
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  void* scratch[2] = {nullptr, nullptr};
+  size_t scratch_bytes[2] = {0, 0};
 };
 
 struct HeapEntry {
