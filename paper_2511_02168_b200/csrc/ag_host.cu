@@ -19,6 +19,7 @@
 // flowing back early, the last ones shrink so the exposed tail (last GEMM +
 // last D2H) is short.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -62,6 +63,40 @@ tf_status join(cudaStream_t after, cudaStream_t before) {
   cudaEventDestroy(ev);  // released once the recorded work completes
   return TF_OK;
 }
+
+// TFB_HOST_TRACE=1: timing events after every copy / GEMM of rank 0,
+// printed by the blocking entry point (a profiling aid; nsys is absent).
+struct Trace {
+  bool on = false;
+  cudaEvent_t t0 = nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> ev;
+  void start(cudaStream_t s) {
+    on = std::getenv("TFB_HOST_TRACE") != nullptr;
+    if (!on) return;
+    cudaEventCreate(&t0);
+    cudaEventRecord(t0, s);
+  }
+  void mark(const std::string& what, cudaStream_t s) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.emplace_back(what, e);
+  }
+  void dump() {
+    if (!on) return;
+    for (auto& [what, e] : ev) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, t0, e);
+      std::fprintf(stderr, "[host-trace] %8.3f ms  %s\n", ms, what.c_str());
+      cudaEventDestroy(e);
+    }
+    cudaEventDestroy(t0);
+    ev.clear();
+    on = false;
+  }
+};
+Trace g_trace;
 
 }  // namespace
 
@@ -122,6 +157,8 @@ extern "C" tf_status tf_ag_gemm_host_async(tf_world* tw, tf_ag_variant variant, 
       return set_error(TF_ERR_CONFIG, "tf_ag_gemm_host: a/b/c for local rank " + std::to_string(r) +
                                           " is NULL");
   auto s = resolve_streams(w, streams);
+  g_trace.start(s[w->first_local]);
+  const int tr = w->first_local;
 
   // Shards live in the symmetric heap (peers pull them / push from them).
   size_t shard_off = 0;
@@ -139,6 +176,7 @@ extern "C" tf_status tf_ag_gemm_host_async(tf_world* tw, tf_ag_variant variant, 
     TFB_CHECK(join(rr.h2d, s[r]));
     TFB_CHECK(join(rr.d2h, s[r]));
     TFB_CUDA(cudaMemcpyAsync(shard[r], a_host[r], m * kw * esz, cudaMemcpyDefault, rr.h2d));
+    if (r == tr) g_trace.mark("h2d shard", rr.h2d);
   }
   const std::vector<size_t> slabs = ag_host_slabs(n, sh.dtype);
   auto put_b = [&](size_t off, size_t ns) -> tf_status {
@@ -149,6 +187,7 @@ extern "C" tf_status tf_ag_gemm_host_async(tf_world* tw, tf_ag_variant variant, 
       TFB_CUDA(cudaMemcpy2DAsync(static_cast<char*>(bdev[r]) + off * esz, n * esz,
                                  static_cast<const char*>(b_host[r]) + off * esz, n * esz, ns * esz, k,
                                  cudaMemcpyDefault, rr.h2d));
+      if (r == tr) g_trace.mark("h2d B cols " + std::to_string(off) + "+" + std::to_string(ns), rr.h2d);
       TFB_CHECK(join(s[r], rr.h2d));
     }
     return TF_OK;
@@ -179,6 +218,7 @@ extern "C" tf_status tf_ag_gemm_host_async(tf_world* tw, tf_ag_variant variant, 
       lay.inbox_complete = j > 0;
       TFB_CHECK(ag_bf16_run(w, variant, slab, shard.data(), bp.data(), cp.data(), nullptr, s, lay));
     }
+    g_trace.mark("gemm cols " + std::to_string(off) + "+" + std::to_string(ns), s[tr]);
     for (int r = 0; r < W; ++r) {
       if (!w->ranks[r].local) continue;
       RankRes& rr = w->ranks[r];
@@ -187,6 +227,7 @@ extern "C" tf_status tf_ag_gemm_host_async(tf_world* tw, tf_ag_variant variant, 
       TFB_CUDA(cudaMemcpy2DAsync(static_cast<char*>(c_host[r]) + off * esz, n * esz,
                                  static_cast<const char*>(cdev[r]) + off * esz, n * esz, ns * esz, m,
                                  cudaMemcpyDefault, rr.d2h));
+      if (r == tr) g_trace.mark("d2h C cols " + std::to_string(off) + "+" + std::to_string(ns), rr.d2h);
     }
     off += ns;
   }
@@ -200,5 +241,7 @@ extern "C" tf_status tf_ag_gemm_host(tf_world* tw, tf_ag_variant variant, const 
                                      const void* const* a_host, const void* const* b_host,
                                      void* const* c_host, void* const* streams) {
   TFB_CHECK(tf_ag_gemm_host_async(tw, variant, shape, a_host, b_host, c_host, streams));
-  return sync_and_check(&tw->impl, resolve_streams(&tw->impl, streams));
+  tf_status st = sync_and_check(&tw->impl, resolve_streams(&tw->impl, streams));
+  g_trace.dump();
+  return st;
 }

@@ -68,6 +68,8 @@ def host_api():
             _abi.ptr_array([hB.data_ptr()]), _abi.ptr_array([hC.data_ptr()]), None)
     with torch.cuda.stream(st):
         ms = timed(lambda: _abi.check(w.lib.tf_ag_gemm_host_async(*args)), reps=4)
+    if os.environ.get("TFB_HOST_TRACE"):
+        _abi.check(w.lib.tf_ag_gemm_host(*args))
     print(json.dumps({"host_api_ms": ms, "slab": os.environ.get("TFB_HOST_SLAB"),
                       "oneshot": os.environ.get("TFB_HOST_ONESHOT")}))
     w.close()
@@ -103,9 +105,10 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "api":
         host_api()
         sys.exit(0)
-    pcie()
-    copy2d()
-    for env in ({}, {"TFB_HOST_BIGFIRST": "1"}, {"TFB_HOST_SLAB": "2048"}, {"TFB_HOST_SLAB": "2560"},
+    if len(sys.argv) > 1 and sys.argv[1] == "all":
+        pcie()
+        copy2d()
+    for env in ({"TFB_HOST_TRACE": "1"}, {"TFB_HOST_BIGFIRST": "1"}, {"TFB_HOST_SLAB": "2048"}, {"TFB_HOST_SLAB": "2560"},
                 {"TFB_HOST_SLAB": "5120"}):
         subprocess.run([sys.executable, __file__, "api"], env={**os.environ, **env}, check=False)
 
