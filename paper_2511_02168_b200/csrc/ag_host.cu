@@ -216,6 +216,7 @@ extern "C" tf_status tf_ag_gemm_host_async(tf_world* tw, tf_ag_variant variant, 
       lay.ldb = n;
       lay.ldc = n;
       lay.inbox_complete = j > 0;
+      lay.split_k = false;
       TFB_CHECK(ag_bf16_run(w, variant, slab, shard.data(), bp.data(), cp.data(), nullptr, s, lay));
     }
     g_trace.mark("gemm cols " + std::to_string(off) + "+" + std::to_string(ns), s[tr]);

@@ -17,9 +17,12 @@ tf_status ag_exact_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh,
 // host-streaming entry, ag_host.cu).  inbox_complete: a previous run of the
 // same variant and shape already gathered A into the inbox (stream-ordered
 // before this one) -- skip the exchange and run the GEMM ungated from it.
+// split_k: allow the skinny-M split-K (off for slabs, so a slab's bits
+// never depend on how the columns were cut).
 struct AgLayout {
   size_t ldb = 0, ldc = 0;
   bool inbox_complete = false;
+  bool split_k = true;
 };
 
 // bf16 tcgen05 path (ag_sm100.cu).

@@ -42,6 +42,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -60,11 +61,11 @@ constexpr int GATHER_T = NUM_THREADS - 192;  // gather threads (PULL)
 constexpr int TMEM_COLS = 512;
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 
-template <int CG>
+template <int CG, int NH_>
 struct Cfg {
-  static constexpr int NH = CG == 2 ? 2 : 1;            // 256-column MMA halves per tile
+  static constexpr int NH = NH_;                        // 256-column MMA halves per tile
   static constexpr int BN_TILE = 256 * NH;              // tile width
-  static constexpr int ACC_BUFS = CG == 2 ? 1 : 2;      // accumulators in 512 TMEM columns
+  static constexpr int ACC_BUFS = NH == 2 ? 1 : 2;      // accumulators in 512 TMEM columns
   static constexpr int STAGES = 4;
   static constexpr int CPH = 4 / CG;                    // 64-column B chunks per half per CTA
   static constexpr int B_BYTES = NH * CPH * BK * 128;   // 32 KB
@@ -88,10 +89,9 @@ struct AgTcParams {
   uint64_t watchdog_ns;
   DevErr* err;
   int board;
-  int dbg;  // TFB_DEBUG knobs: 1 skip C stores, 2 skip MMAs, 8 force CG=1 (profiling aids)
-  int ksplit;  // > 1: skinny-M split-K, fp32 partials [ksplit][M][N] via tmP, then reduce
-  int kbs;     // k-blocks per split
-  int Mp;      // M rounded up to 128: row pitch between splits in the workspace
+  int dbg;  // TFB_DEBUG knobs: 1 skip C stores, 2 skip MMAs, 8 force CG=1, 16 skip the split-K reduce (profiling aids)
+  int ksplit;  // > 1: skinny-M split-K across a cluster of ksplit CTAs (pairs), reduced through DSMEM
+  int ldc;     // row pitch of C (elements)
   const __nv_bfloat16* peer_shard[64];
 };
 
@@ -165,15 +165,15 @@ __device__ __forceinline__ void mma_issue(uint32_t d_tmem, uint64_t a_desc, uint
     mma_bf16_ss(d_tmem, a_desc, b_desc, idesc, accumulate);
 }
 
-// tcgen05.commit: arrive on `bar` in every CTA of the pair once the issued
-// MMAs retired.
+// tcgen05.commit: arrive on `bar` in every CTA of the pair (cluster ranks in
+// pair_mask) once the issued MMAs retired.
 template <int CG>
-__device__ __forceinline__ void mma_commit_all(uint64_t* bar) {
+__device__ __forceinline__ void mma_commit_all(uint64_t* bar, uint16_t pair_mask) {
   if (CG == 2)
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
         "[%0], %1;" ::"r"(smem_u32(bar)),
-        "h"(uint16_t(3))
+        "h"(pair_mask)
         : "memory");
   else
     mma_commit(bar);
@@ -200,14 +200,13 @@ __device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr) {
     tmem_dealloc(taddr, TMEM_COLS);
 }
 
-template <int CG>
+template <int CG, int NH_>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     ag_gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA_own,
                          const __grid_constant__ CUtensorMap tmA_inbox,
                          const __grid_constant__ CUtensorMap tmB,
-                         const __grid_constant__ CUtensorMap tmC,
-                         const __grid_constant__ CUtensorMap tmP, const AgTcParams p) {
-  using K_ = Cfg<CG>;
+                         const __grid_constant__ CUtensorMap tmC, const AgTcParams p) {
+  using K_ = Cfg<CG, NH_>;
   constexpr int STAGES = K_::STAGES, NH = K_::NH, CPH = K_::CPH;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -221,18 +220,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;
-  const bool leader = crank == 0;
+  // Cluster = CG * ksplit CTAs: pairs (cta_group::2) at ranks (2j, 2j+1),
+  // split-K siblings of one tile at ranks prank + CG * ks.
+  const uint32_t crank = (CG == 2 || p.ksplit > 1) ? cluster_ctarank() : 0;
+  const uint32_t prank = CG == 2 ? (crank & 1u) : 0u;   // rank inside the CTA pair
+  const uint32_t lead = crank - prank;                  // the pair leader's cluster rank
+  const uint16_t pair_mask = uint16_t(3u << lead);
+  const bool leader = prank == 0;
   const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
   const int num_mt = (p.num_m + CG - 1) / CG;  // tile rows (BM * CG each)
   // Work items: (tile, k-split).  Split ks covers k-block slots
-  // [ks*kbs, min((ks+1)*kbs, kb_total)) of the rank's rotated k order.
+  // [ks*kb/S, (ks+1)*kb/S) of the rank's rotated k order (never empty:
+  // the host keeps kb_total >= 4 * ksplit).
   const int num_tiles = num_mt * p.num_n * p.ksplit;
   auto item_coords = [&](int t, int& mt, int& nb, int& i0, int& i1) {
     const int ks = t % p.ksplit;
     tile_coords(num_mt, p.num_n, t / p.ksplit, mt, nb);
-    i0 = ks * p.kbs;
-    i1 = min(p.kb_total, i0 + p.kbs);
+    i0 = ks * p.kb_total / p.ksplit;
+    i1 = (ks + 1) * p.kb_total / p.ksplit;
   };
 
   if (warp == 0 && lane == 0) {
@@ -240,7 +245,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tma_prefetch(&tmA_inbox);
     tma_prefetch(&tmB);
     tma_prefetch(&tmC);
-    tma_prefetch(&tmP);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], CG);  // one arrive per CTA of the pair (the leader's copy is used)
       mbar_init(&empty[s], 1);
@@ -253,7 +257,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   if (warp == 1) tmem_alloc_cg<CG>(tmem_slot);
   tc_fence_before();
-  if (CG == 2) cluster_sync();
+  if (CG == 2 || p.ksplit > 1) cluster_sync();
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int t = cid; t < num_tiles; t += ncl) {
         int mt, nb, i0, i1;
         item_coords(t, mt, nb, i0, i1);
-        const int mb = mt * CG + int(crank);  // this CTA's 128-row block
+        const int mb = mt * CG + int(prank);  // this CTA's 128-row block
         const int m0 = mb * BM, n0 = nb * K_::BN_TILE;
         uint64_t ready_mask = 0;
         for (int i = i0; i < i1; ++i) {
@@ -280,7 +284,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             fence_proxy_async_global();
             ready_mask |= 1ull << src;
           }
-          const uint32_t bar = CG == 2 ? mapa(&full[stage], 0) : smem_u32(&full[stage]);
+          const uint32_t bar = CG == 2 ? mapa(&full[stage], lead) : smem_u32(&full[stage]);
           if (leader) mbar_arrive_expect_tx(&full[stage], CG * K_::STAGE_BYTES);
           else mbar_arrive_cluster(bar);
           uint8_t* a_dst = smA + stage * A_BYTES;
@@ -292,7 +296,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int c = 0; c < CPH; ++c)
               tma_load<CG>(b_dst + (h * CPH + c) * (BK * 128), &tmB, bar,
-                           n0 + h * 256 + int(crank) * (256 / CG) + c * 64, kb * BK);
+                           n0 + h * 256 + int(prank) * (256 / CG) + c * 64, kb * BK);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -332,13 +336,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               }
             }
           }
-          mma_commit_all<CG>(&empty[stage]);
+          mma_commit_all<CG>(&empty[stage], pair_mask);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit_all<CG>(&tfull[acc]);
+        mma_commit_all<CG>(&tfull[acc], pair_mask);
         if (++acc == K_::ACC_BUFS) {
           acc = 0;
           aphase ^= 1;
@@ -350,55 +354,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int acc = 0;
     uint32_t aphase = 0;
-    const uint32_t tempty_leader0 = CG == 2 ? mapa(&tempty[0], 0) : smem_u32(&tempty[0]);
-    for (int t = cid; t < num_tiles; t += ncl) {
+    const uint32_t tempty_leader0 = CG == 2 ? mapa(&tempty[0], lead) : smem_u32(&tempty[0]);
+    // Split-K: one item per CTA, reduced after the role loops (below).
+    for (int t = p.ksplit > 1 ? num_tiles : cid; t < num_tiles; t += ncl) {
       int mt, nb;
       int i0_, i1_;
       item_coords(t, mt, nb, i0_, i1_);
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
-      if (p.ksplit > 1) {
-        // Split-K: this split's fp32 partial -> [ks][M][N] workspace, 32-col
-        // slabs (128-byte rows), same swizzled staging + TMA store.
-        const int ks = t % p.ksplit;
-        const int row0 = (mt * CG + int(crank)) * BM + 32 * q;
-        uint8_t* stg = smStage + q * (2 * 4096);
-#pragma unroll 1
-        for (int cc = 0; cc < NH * 8; ++cc) {
-          uint32_t r0[32];
-          tmem_ld_32x32b_x32(tmem_base + (uint32_t(32 * q) << 16) + uint32_t(acc * NH * 256 + 32 * cc), r0);
-          tmem_ld_wait();
-          uint8_t* buf = stg + (cc & 1) * 4096;
-          if (cc >= 2 && lane == 0) bulk_wait_read<1>();
-          __syncwarp();
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<uint4*>(buf + lane * 128 + ((j ^ (lane & 7)) * 16)) =
-                make_uint4(r0[4 * j], r0[4 * j + 1], r0[4 * j + 2], r0[4 * j + 3]);
-          fence_proxy_async_shared();
-          __syncwarp();
-          if (lane == 0 && row0 < p.M) {
-            tma_store_2d(&tmP, buf, nb * K_::BN_TILE + 32 * cc, ks * p.Mp + row0);
-            bulk_commit();
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (CG == 2) mbar_arrive_cluster(tempty_leader0 + uint32_t(acc) * 8);
-          else mbar_arrive(&tempty[acc]);
-        }
-        if (++acc == K_::ACC_BUFS) {
-          acc = 0;
-          aphase ^= 1;
-        }
-        continue;
-      }
       // 64-column slabs: two tcgen05.ld (32 columns each) -> bf16 -> a
       // SWIZZLE_128B smem box [32 rows][64 cols] (conflict-free: 16-byte
       // chunk j of row r sits at j ^ (r & 7)) -> one TMA store per warp per
       // slab, double-buffered so the next slab's TMEM reads overlap the store.
-      const int row0 = (mt * CG + int(crank)) * BM + 32 * q;
+      const int row0 = (mt * CG + int(prank)) * BM + 32 * q;
       uint8_t* stg = smStage + q * (2 * 4096);
 #pragma unroll 1
       for (int cc = 0; cc < NH * 4; ++cc) {
@@ -482,8 +450,89 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
 
+  if (p.ksplit > 1) {
+    // ===== split-K reduction through distributed shared memory =====
+    // Every CTA of the cluster holds a 128-row fp32 partial of the same tile
+    // (its k-range) in TMEM.  Per 256-column half: the epilogue warps dump it
+    // into this CTA's (drained) pipeline smem, the cluster syncs, then CTA ks
+    // sums rows [ks*128/S, (ks+1)*128/S) over the S siblings in ascending
+    // split order (deterministic) straight from their smem, and stores bf16
+    // C.  No workspace, no second launch.  (Measured: a push variant --
+    // remote st.shared::cluster into the owner's slots -- costs the same;
+    // DSMEM moves ~20 B/clk per SM either way.)
+    const int S = p.ksplit;
+    const int ks = int(crank) / CG;
+    const int rows_per = BM / S;
+    int mt, nb, i0_, i1_;
+    item_coords(cid, mt, nb, i0_, i1_);
+    float* R = reinterpret_cast<float*>(smem);  // [128][256] fp32, 16-byte chunks swizzled by row & 7
+    const int row_base = (mt * CG + int(prank)) * BM;
+    if (warp >= 2 && warp < 6) {
+      mbar_wait(&tfull[0], 0);
+      tc_fence_after();
+    }
+#pragma unroll 1
+    for (int h = 0; h < NH; ++h) {
+      if (warp >= 2 && warp < 6) {
+        const int row = 32 * (warp & 3) + lane;
+#pragma unroll 1
+        for (int cc = 0; cc < 8; ++cc) {
+          uint32_t r0[32];
+          tmem_ld_32x32b_x32(tmem_base + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(h * 256 + 32 * cc), r0);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c = cc * 8 + j;  // 16-byte chunk of the 256-column row
+            *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(R) + row * 1024 + ((c ^ (row & 7)) * 16)) =
+                make_uint4(r0[4 * j], r0[4 * j + 1], r0[4 * j + 2], r0[4 * j + 3]);
+          }
+        }
+      }
+      cluster_sync();
+      uint32_t src[8];
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2)
+        if (s2 < S) src[s2] = mapa(R, prank + uint32_t(CG * s2));
+      const int tasks = (p.dbg & 16) ? 0 : rows_per * 32;  // 8-column groups per row: 32
+      for (int e = threadIdx.x; e < tasks; e += NUM_THREADS) {
+        const int rl = ks * rows_per + e / 32, g = e % 32;
+        const int grow = row_base + rl, gcol = nb * K_::BN_TILE + h * 256 + g * 8;
+        const uint32_t off0 = uint32_t(rl * 1024 + (((2 * g) ^ (rl & 7)) * 16));
+        const uint32_t off1 = uint32_t(rl * 1024 + (((2 * g + 1) ^ (rl & 7)) * 16));
+        // All 2*S remote loads in flight first, then the ascending sum.
+        float4 x[8], y[8];
+#pragma unroll
+        for (int s2 = 0; s2 < 8; ++s2) {
+          if (s2 < S) {
+            asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(x[s2].x), "=f"(x[s2].y), "=f"(x[s2].z), "=f"(x[s2].w) : "r"(src[s2] + off0));
+            asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(y[s2].x), "=f"(y[s2].y), "=f"(y[s2].z), "=f"(y[s2].w) : "r"(src[s2] + off1));
+          }
+        }
+        float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int s2 = 0; s2 < 8; ++s2) {
+          if (s2 < S) {
+            a[0] += x[s2].x; a[1] += x[s2].y; a[2] += x[s2].z; a[3] += x[s2].w;
+            a[4] += y[s2].x; a[5] += y[s2].y; a[6] += y[s2].z; a[7] += y[s2].w;
+          }
+        }
+        if (grow < p.M && gcol < p.N && !(p.dbg & 1)) {
+          uint4 o;
+          o.x = pack_bf16x2(a[0], a[1]);
+          o.y = pack_bf16x2(a[2], a[3]);
+          o.z = pack_bf16x2(a[4], a[5]);
+          o.w = pack_bf16x2(a[6], a[7]);
+          *reinterpret_cast<uint4*>(p.C + size_t(grow) * p.ldc + gcol) = o;
+        }
+      }
+      cluster_sync();  // siblings done reading R before it is rewritten / released
+    }
+  }
+
   tc_fence_before();
-  if (CG == 2) cluster_sync();
+  if (CG == 2 || p.ksplit > 1) cluster_sync();
   else __syncthreads();
   if (warp == 1) {
     __syncwarp();
@@ -558,31 +607,6 @@ __global__ void __launch_bounds__(512) ag_push_kernel(const PushParams p) {
       p.ctr[1] = 0;
       __threadfence();
     }
-  }
-}
-
-// Split-K reduce: C = bf16(sum_ks P[ks]) in ascending ks (deterministic), 8
-// consecutive columns per thread (two 16-byte loads per split, one store).
-__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ P,
-                                                            __nv_bfloat16* __restrict__ C, int M, int N,
-                                                            int Mp, int ksplit) {
-  const size_t vecs = size_t(M) * N / 8;
-  const size_t split_stride = size_t(Mp) * N;
-  for (size_t v = blockIdx.x * size_t(blockDim.x) + threadIdx.x; v < vecs; v += size_t(gridDim.x) * blockDim.x) {
-    const size_t e = v * 8;
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int s = 0; s < ksplit; ++s) {
-      const float4 a = __ldcs(reinterpret_cast<const float4*>(P + s * split_stride + e));
-      const float4 b = __ldcs(reinterpret_cast<const float4*>(P + s * split_stride + e + 4));
-      acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
-      acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
-    }
-    uint4 o;
-    o.x = pack_bf16x2(acc[0], acc[1]);
-    o.y = pack_bf16x2(acc[2], acc[3]);
-    o.z = pack_bf16x2(acc[4], acc[5]);
-    o.w = pack_bf16x2(acc[6], acc[7]);
-    *reinterpret_cast<uint4*>(C + e) = o;
   }
 }
 
@@ -673,48 +697,102 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   p.err = w->err_of(r);
   p.board = board;
   if (const char* e = std::getenv("TFB_DEBUG")) p.dbg = std::atoi(e);
-  static bool attr_set[2][64] = {};
   const int dev = w->ranks[r].device;
   cudaSetDevice(dev);
-  // CTA pairs (cta_group::2, 256 x 512 tiles) whenever there are two 128-row
-  // blocks to pair; single CTAs (128 x 256) for skinny M.
-  const int CG = (p.num_m >= 2 && !(p.dbg & 8)) ? 2 : 1;
-  const int bn_tile = CG == 2 ? Cfg<2>::BN_TILE : Cfg<1>::BN_TILE;
-  p.num_n = int((sh.n + bn_tile - 1) / bn_tile);
-  p.num_tiles = ((p.num_m + CG - 1) / CG) * p.num_n;
-  // Skinny M: too few tiles to occupy the SMs -> split K across CTAs (fp32
-  // partials, deterministic ascending reduce).  BASELINE config 5's low end.
-  p.ksplit = 1;
-  {
-    const unsigned busy = unsigned(p.num_tiles) * CG;
-    int ks = 1;
-    if (busy * 2 <= grid_cap) ks = int(std::min<unsigned>(grid_cap / busy, 16));
-    ks = std::min(ks, std::max(1, p.kb_total / 4));  // >= 4 k-blocks per split
-    if (const char* e = std::getenv("TFB_KSPLIT")) ks = std::max(1, std::atoi(e));
-    if (ldc != sh.n) ks = 1;  // slab of a wider C: the reduce writes dense rows
-    p.kbs = (p.kb_total + ks - 1) / ks;
-    p.ksplit = (p.kb_total + p.kbs - 1) / p.kbs;
+  // Kernel shapes: CTA pairs (cta_group::2) with 256 x 512 tiles whenever
+  // there are two 128-row blocks to pair; 256 x 256 pair tiles when that
+  // fills the SMs better (skinny M); single CTAs (128 x 256) for M <= 128.
+  struct Shape {
+    int CG, NH;
+    void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, AgTcParams);
+    size_t smem;
+    int id;
+  };
+  const Shape shapes[3] = {
+      {1, 1, ag_gemm_sm100_kernel<1, 1>, Cfg<1, 1>::SMEM, 0},
+      {2, 2, ag_gemm_sm100_kernel<2, 2>, Cfg<2, 2>::SMEM, 1},
+      {2, 1, ag_gemm_sm100_kernel<2, 1>, Cfg<2, 1>::SMEM, 2},
+  };
+  // Skinny M: too few tiles to occupy the SMs -> split K across a cluster
+  // of S CTAs (pairs) per tile, reduced in-kernel through DSMEM in
+  // ascending split order.  S is a power of two (it divides the 128 rows a
+  // CTA reduces), CG * S <= 8 (portable cluster), >= 4 k-blocks per split,
+  // and every cluster resident in one wave (a cluster is co-scheduled
+  // inside one GPC).  BASELINE config 5's low end.
+  auto plan = [&](const Shape& shp, int& tiles, int& num_n, int& ks) -> tf_status {
+    num_n = int((sh.n + 256 * shp.NH - 1) / (256 * shp.NH));
+    tiles = ((p.num_m + shp.CG - 1) / shp.CG) * num_n;
+    const unsigned busy = unsigned(tiles) * shp.CG;
+    ks = 1;
+    if (busy * 2 <= grid_cap)
+      while (ks * 2 * busy <= grid_cap && ks * 2 * shp.CG <= 8 && ks * 2 * 4 <= p.kb_total) ks *= 2;
+    if (const char* e = std::getenv("TFB_KSPLIT")) {
+      const int want = std::max(1, std::atoi(e));
+      ks = 1;
+      while (ks * 2 <= want && ks * 2 * shp.CG <= 8 && ks * 2 * 4 <= p.kb_total) ks *= 2;
+    }
+    if (!lay.split_k) ks = 1;
+    while (ks > 1) {
+      static int max_active[3][9] = {};
+      int& ma = max_active[shp.id][ks];
+      if (ma == 0) {
+        TFB_CUDA(cudaFuncSetAttribute(shp.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shp.smem)));
+        cudaLaunchConfig_t qc{};
+        qc.gridDim = dim3(unsigned(shp.CG * ks));
+        qc.blockDim = dim3(NUM_THREADS);
+        qc.dynamicSmemBytes = shp.smem;
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = unsigned(shp.CG * ks);
+        qa[0].val.clusterDim.y = 1;
+        qa[0].val.clusterDim.z = 1;
+        qc.attrs = qa;
+        qc.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&ma, shp.kern, &qc) != cudaSuccess || ma < 1) {
+          cudaGetLastError();
+          ma = -1;
+        }
+      }
+      if (ma > 0 && unsigned(tiles) <= unsigned(ma)) break;
+      if (std::getenv("TFB_KSPLIT_FORCE")) break;
+      ks /= 2;
+    }
+    return TF_OK;
+  };
+  const Shape* shp = &shapes[(p.num_m >= 2 && !(p.dbg & 8)) ? 1 : 0];
+  int tiles = 0, num_n = 0, ks = 1;
+  TFB_CHECK(plan(*shp, tiles, num_n, ks));
+  if (shp->CG == 2 && !std::getenv("TFB_NO_NARROW")) {
+    int t2, n2, k2;
+    TFB_CHECK(plan(shapes[2], t2, n2, k2));
+    // Narrow pair tiles only when the wide ones leave a quarter of the SMs idle.
+    if (unsigned(tiles * ks * 2) * 4 < grid_cap * 3 && t2 * k2 > tiles * ks) {
+      shp = &shapes[2];
+      tiles = t2;
+      num_n = n2;
+      ks = k2;
+    }
   }
-  p.Mp = int((sh.m + BM - 1) / BM * BM);
-  CUtensorMap mP = mC;
-  float* partial = nullptr;
-  if (p.ksplit > 1) {
-    size_t off;
-    const size_t bytes = size_t(p.ksplit) * p.Mp * sh.n * 4;
-    TFB_CHECK(heap_get(w, "ag.splitk[" + std::to_string(bytes) + "]", bytes, &off));
-    partial = reinterpret_cast<float*>(w->ptr(r, off));
-    TFB_CHECK(make_map(&mP, partial, sh.n, size_t(p.ksplit) * p.Mp, sh.n, 32, 32, /*f32=*/true));
-  }
-  auto kern = CG == 2 ? ag_gemm_sm100_kernel<2> : ag_gemm_sm100_kernel<1>;
-  const size_t smem = CG == 2 ? Cfg<2>::SMEM : Cfg<1>::SMEM;
-  if (!attr_set[CG - 1][dev & 63]) {
+  const int CG = shp->CG;
+  p.num_n = num_n;
+  p.num_tiles = tiles;
+  p.ksplit = ks;
+  if (std::getenv("TFB_KSPLIT_VERBOSE"))
+    std::fprintf(stderr, "[ag] m=%zu n=%zu k=%zu CG=%d NH=%d tiles=%d ksplit=%d\n", sh.m, sh.n, sh.k, CG,
+                 shp->NH, tiles, ks);
+  p.ldc = int(ldc);
+  auto kern = shp->kern;
+  const size_t smem = shp->smem;
+  static bool attr_set[3][64] = {};
+  if (!attr_set[shp->id][dev & 63]) {
     TFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr_set[CG - 1][dev & 63] = true;
+    attr_set[shp->id][dev & 63] = true;
   }
   const unsigned pair_tiles = unsigned((p.num_m + CG - 1) / CG) * unsigned(p.num_n) * unsigned(p.ksplit);
   if (const char* e = std::getenv("TFB_GRID")) grid_cap = std::min(grid_cap, unsigned(std::atoi(e)));
   unsigned grid = std::min(pair_tiles * CG, grid_cap / CG * CG);
   grid = std::max(grid, unsigned(CG));
+  if (p.ksplit > 1) grid = pair_tiles * CG;  // exactly one item per CTA (the reduction aliases its smem)
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(NUM_THREADS);
@@ -722,7 +800,7 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = CG * p.ksplit;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -736,16 +814,8 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
       last_gm[dev & 63] = gm;
     }
   }
-  TFB_CUDA(cudaLaunchKernelEx(&cfg, kern, mOwn, mInbox, mB, mC, mP, p));
+  TFB_CUDA(cudaLaunchKernelEx(&cfg, kern, mOwn, mInbox, mB, mC, p));
   ++w->launches;
-  if (p.ksplit > 1) {
-    const size_t vecs = sh.m * sh.n / 8;
-    const unsigned blocks = unsigned(std::min<size_t>((vecs + 255) / 256, size_t(w->sm_count) * 16));
-    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(partial, static_cast<__nv_bfloat16*>(c), int(sh.m), int(sh.n),
-                                                 p.Mp, p.ksplit);
-    TFB_CUDA(cudaGetLastError());
-    ++w->launches;
-  }
   return TF_OK;
 }
 
@@ -897,10 +967,10 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
 
 void ag_sm100_preload() {  // see ag_exact_preload
   cudaFuncAttributes a;
-  cudaFuncGetAttributes(&a, ag_gemm_sm100_kernel<1>);
-  cudaFuncGetAttributes(&a, ag_gemm_sm100_kernel<2>);
+  cudaFuncGetAttributes(&a, ag_gemm_sm100_kernel<1, 1>);
+  cudaFuncGetAttributes(&a, ag_gemm_sm100_kernel<2, 2>);
+  cudaFuncGetAttributes(&a, ag_gemm_sm100_kernel<2, 1>);
   cudaFuncGetAttributes(&a, ag_push_kernel);
-  cudaFuncGetAttributes(&a, splitk_reduce_kernel);
 }
 
 }  // namespace tfb
