@@ -82,9 +82,12 @@ struct FdParams {
   DevErr* err;
   int board;
   float* ws;                  // [nlocal][G][S][gs][d+4] split partials [m l - - o[d]]
-  unsigned long long* ticket; // [nlocal][G] epoch-valued tickets
+  uint64_t* done;             // [nlocal][G] epoch-valued count of finished splits
+  uint64_t* gtick;            // [nlocal][G] epoch-valued count of split-folded heads (push)
   unsigned long long* claim;  // [nlocal][G] epoch-valued cross-rank fold claims
   unsigned int* ctr;          // [0] compute, [1] fold, [2] done
+  unsigned int* sfc;          // [nlocal] split-fold sub-item counters
+  int hc;                     // heads per split-fold sub-item
   uint64_t local_dst;         // bit dst: dst's inbox/flags live on this launch's device
   int push;                   // push rank partials to every inbox (+ signal)
   int fold_inline;            // fused: fold after compute
@@ -267,8 +270,6 @@ __device__ __forceinline__ uint32_t w4(const uint4& v, int i) {
 // 8 warps per CTA, 2 CTAs per SM at <= 128 registers: 16 streaming warps per
 // SM keep ~128 KB of KV loads in flight (what HBM3e needs at ~2 us latency).
 constexpr int kFastWarps = 8;
-constexpr int kFoldW = 1024;  // split weights cached in smem for the group fold
-constexpr int kChunk = 8;     // splits per level-1 fold (two-level split fold)
 constexpr int kFastThreads = kFastWarps * 32;
 
 // d index held by O^T accumulator row r of PV tile (i, j) (see header).
@@ -564,177 +565,203 @@ __device__ __forceinline__ float4 ldcg4(const float* p) {
   return __ldcg(reinterpret_cast<const float4*>(p));
 }
 
-// ---- split fold: max-first fold of n split-partial rows of a group -------
-// Rows first, first + step, ... (n of them) of the group's workspace; the
-// result goes in place into ws row `first` (level 1 of the two-level fold)
-// or out as the rank's wire rows (to_wire: every inbox when pushing, else
-// the published partial).  Max-first and fully parallel (every row loaded
-// independently, ld.cg through L2): M = max m_i, w_i = exp(m_i - M),
-// l = sum l_i w_i, o = sum o_i w_i -- the same monoid as combine_partials
-// (tilemath.hpp:186-220) evaluated in one pass instead of n dependent steps.
-// Identical code in every schedule, so schedules stay bitwise equal.
-// Non-inlined: its own register allocation keeps the attention loop's.
-__device__ __noinline__ void fold_ws(const FdParams& P, int lr, int g, float* grp, int first, int step,
-                                     int n, int to_wire, float* s_M, float* s_L, float* s_w, float* s_l) {
-  // W = 1, fused: the rank's wire row is also the whole fold (one source),
-  // so finalize out here -- o / l on the same floats fold_group would take
-  // from the inbox (combine with an empty accumulator copies them), bitwise
-  // the same result one dependent round trip earlier.
-  const int direct = to_wire && P.direct;
-  void* const out = P.r[lr].out;
-  const int out_bf16 = P.out_bf16;
-  // Scalars and the peer inbox table into registers / smem once: P lives in
-  // the kernel's parameter space, reached through a generic pointer here,
-  // and the row stores below would otherwise force a reload per use.
-  const int d = P.d, row_len = d + 2, wrl = ws_row(d);
-  const int gs = P.gs, W = P.W, Hq = P.Hq, Hkv = P.Hkv, push = P.push;
+// ---- split fold: the S split partials of a group -> the rank's wire rows --
+// One sub-item = hc heads of one group (host-chosen so that a warp folds at
+// most ~8 rows).  wph = 8 / hc warps share a head (hc <= 8), warp j of a
+// head taking rows j, j + wph, ...; for hc > 8 every warp owns whole heads.
+// Max-first and deterministic: per warp M = max m_i (over l_i != 0),
+// w_i = exp(m_i - M), L = sum l_i w_i, O = sum o_i w_i (rows ascending),
+// then the warps of a head combine the same way in ascending warp order --
+// the monoid of combine_partials (tilemath.hpp:186-220) in two flat levels.  Every
+// schedule runs this code, so schedules stay bitwise equal.  The first rows'
+// o values are loaded before the m/l round trip: a sub-item costs about one
+// L2 round trip.  Writes the wire rows [M | L | O] (every inbox when
+// pushing, else the published partial) and, W = 1 fused (`direct`), the
+// finalized output o / l (tilemath.hpp:225-239) -- bitwise what fold_group
+// would compute from the single source.
+template <int EL, int RB>
+__device__ __forceinline__ void fold_heads(const FdParams& P, int lr, int g, int h0, int hc, float* s_wm,
+                                        float* s_L, float* s_O) {
+  const int d = P.d, wrl = ws_row(d), gs = P.gs, S = P.S, W = P.W, Hq = P.Hq, Hkv = P.Hkv, row_len = d + 2;
+  const int G = P.B * Hkv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = P.r[lr].rank;
+  const int direct = P.direct, push = P.push, out_bf16 = P.out_bf16;
+  void* const out = P.r[lr].out;
   float* const pub = P.r[lr].pub;
-  __shared__ float* s_inbox[64];
-  if (to_wire && push) {
-    for (int i = threadIdx.x; i < W; i += blockDim.x) s_inbox[i] = P.inbox_all[i];
-    __syncthreads();
-  }
   const int b = g / Hkv, kvh = g % Hkv;
+  const float* grp = P.ws + ((size_t(lr) * G + g) * S) * gs * wrl;
   const size_t base_src = size_t(rank) * P.B * Hq * row_len;
-  auto row = [&](int i) { return grp + size_t(first + i * step) * gs * wrl; };  // split row block
-  auto row_off = [&](int h) { return (size_t(b) * Hq + kvh * gs + h) * row_len; };
-  // Result element e of head h; e in wire numbering (0 = m, 1 = l, 2.. = o).
-  auto put = [&](int h, int e, float val) {
-    if (!to_wire) {
-      row(0)[size_t(h) * wrl + (e < 2 ? e : kWsO + e - 2)] = val;
-    } else if (push) {
-      for (int dst = 0; dst < W; ++dst) s_inbox[dst][base_src + row_off(h) + e] = val;
-    } else {
-      pub[row_off(h) + e] = val;
-    }
-  };
-  auto put2 = [&](int h, int e, float x, float y) {  // e even: 8-byte aligned
-    const float2 v2 = make_float2(x, y);
-    if (!to_wire) {
-      *reinterpret_cast<float2*>(row(0) + size_t(h) * wrl + (e < 2 ? e : kWsO + e - 2)) = v2;
-    } else if (push) {
-      for (int dst = 0; dst < W; ++dst)
-        *reinterpret_cast<float2*>(s_inbox[dst] + base_src + row_off(h) + e) = v2;
-    } else {
-      *reinterpret_cast<float2*>(pub + row_off(h) + e) = v2;
-    }
-  };
-  const int NG = n * gs;
-  if (NG <= kFoldW && (d % 4) == 0) {
-    // Each thread owns one (head, 4 d) quad and keeps UF 16-byte loads in
-    // flight; the first UF rows are issued before the m/l round trip, so a
-    // level of the fold (n <= kChunk = UF) costs about one L2 round trip.
-    constexpr int UF = 8;
-    const int qpr = d / 4, quads = gs * qpr;
-    float4 v[UF];
-    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    auto load_rows = [&](int h, int e, int i0) {
+  const int wph = hc >= 8 ? 1 : 8 / hc;
+  // Fold rows r0, r0 + step, ... of head h into (L, O[EL]) with max M.
+  auto fold_rows = [&](int h, int r0, int step, float M, float& L, float (&O)[EL]) {
+    L = 0.0f;
 #pragma unroll
-      for (int u = 0; u < UF; ++u)
-        v[u] = i0 + u < n ? ldcg4(row(i0 + u) + size_t(h) * wrl + kWsO + e) : z4;
-    };
-    if (int(threadIdx.x) < quads) load_rows(threadIdx.x / qpr, 4 * (threadIdx.x % qpr), 0);
-    // (1) every (row, head) m/l pair, one 8-byte load each
-    for (int i = threadIdx.x; i < NG; i += blockDim.x) {
-      const float2 ml = __ldcg(reinterpret_cast<const float2*>(row(i / gs) + size_t(i % gs) * wrl));
-      s_w[i] = ml.y != 0.0f ? ml.x : -INFINITY;
-      s_l[i] = ml.y;
-    }
-    __syncthreads();
-    trace_at(P, to_wire ? 11 : 10);
-    // (2) per-head max
-    for (int h = threadIdx.x; h < gs; h += blockDim.x) {
-      float M = -INFINITY;
-      for (int i = 0; i < n; ++i) M = fmaxf(M, s_w[i * gs + h]);
-      s_M[h] = M;
-    }
-    __syncthreads();
-    // (3) weights, (4) normalisers
-    for (int i = threadIdx.x; i < NG; i += blockDim.x)
-      s_w[i] = s_l[i] != 0.0f ? expf(s_w[i] - s_M[i % gs]) : 0.0f;
-    __syncthreads();
-    for (int h = threadIdx.x; h < gs; h += blockDim.x) {
-      float L = 0.0f;
-      for (int i = 0; i < n; ++i) L = __fadd_rn(L, __fmul_rn(s_l[i * gs + h], s_w[i * gs + h]));
-      s_L[h] = L;
-      if (direct && L == 0.0f)
-        raise_err(P.err, TF_ERR_EMPTY_ATTENTION, kEmpty, rank, -1, 0, 0, 0, 0, uint64_t(kvh * gs + h));
-    }
-    if (direct) __syncthreads();
-    // (5) the weighted o sums
-    bool first_quad = true;
-    for (int pi = threadIdx.x; pi < quads; pi += blockDim.x) {
-      const int h = pi / qpr, e = 4 * (pi % qpr);
-      float4 acc[2] = {z4, z4};
-      for (int i0 = 0; i0 < n; i0 += UF) {
-        if (!first_quad) load_rows(h, e, i0);
-        first_quad = false;
+    for (int x = 0; x < EL; ++x) O[x] = 0.0f;
+    for (int i0 = r0; i0 < S; i0 += RB * step) {
+      float v[RB][EL];
+      float2 ml[RB];
 #pragma unroll
-        for (int u = 0; u < UF; ++u) {
-          if (i0 + u >= n) break;
-          const float w = s_w[(i0 + u) * gs + h];
-          float4& a = acc[u & 1];
-          a.x = __fadd_rn(a.x, __fmul_rn(v[u].x, w));
-          a.y = __fadd_rn(a.y, __fmul_rn(v[u].y, w));
-          a.z = __fadd_rn(a.z, __fmul_rn(v[u].z, w));
-          a.w = __fadd_rn(a.w, __fmul_rn(v[u].w, w));
+      for (int u = 0; u < RB; ++u) {
+        const int i = i0 + u * step;
+        const float* row = grp + (size_t(i) * gs + h) * wrl;
+        ml[u] = i < S ? make_float2(__ldcg(row), __ldcg(row + 1)) : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int x = 0; x < EL; ++x) {
+          const int e = lane + 32 * x;
+          v[u][x] = (i < S && e < d) ? __ldcg(row + kWsO + e) : 0.0f;
         }
       }
-      const float o0 = __fadd_rn(acc[0].x, acc[1].x), o1 = __fadd_rn(acc[0].y, acc[1].y);
-      const float o2 = __fadd_rn(acc[0].z, acc[1].z), o3 = __fadd_rn(acc[0].w, acc[1].w);
-      put2(h, 2 + e, o0, o1);
-      put2(h, 4 + e, o2, o3);
-      if (direct && s_L[h] != 0.0f) {
-        const size_t ooff = (size_t(b) * Hq + kvh * gs + h) * d + e;
-        const float L = s_L[h];
-        store_out(out, ooff, o0 / L, out_bf16);
-        store_out(out, ooff + 1, o1 / L, out_bf16);
-        store_out(out, ooff + 2, o2 / L, out_bf16);
-        store_out(out, ooff + 3, o3 / L, out_bf16);
+#pragma unroll
+      for (int u = 0; u < RB; ++u) {
+        if (i0 + u * step >= S) break;
+        const float w = ml[u].y != 0.0f ? expf(ml[u].x - M) : 0.0f;
+        L = __fadd_rn(L, __fmul_rn(ml[u].y, w));
+#pragma unroll
+        for (int x = 0; x < EL; ++x) O[x] = __fadd_rn(O[x], __fmul_rn(v[u][x], w));
       }
     }
-    __syncthreads();
-    for (int h = threadIdx.x; h < gs; h += blockDim.x) put2(h, 0, s_M[h], s_L[h]);
-  } else {
-    // Large n x gs or d % 4 != 0: per-head scalar fold (weights recomputed).
-    for (int h = threadIdx.x; h < gs; h += blockDim.x) {
-      float M = -INFINITY;
-      for (int i = 0; i < n; ++i) {
-        const float* r = row(i) + size_t(h) * wrl;
-        if (__ldcg(r + 1) != 0.0f) M = fmaxf(M, __ldcg(r));
-      }
-      float L = 0.0f;
-      for (int i = 0; i < n; ++i) {
-        const float* r = row(i) + size_t(h) * wrl;
-        const float l = __ldcg(r + 1);
-        L = __fadd_rn(L, __fmul_rn(l, l != 0.0f ? expf(__ldcg(r) - M) : 0.0f));
-      }
-      s_M[h] = M;
-      s_L[h] = L;
-      if (direct && L == 0.0f)
-        raise_err(P.err, TF_ERR_EMPTY_ATTENTION, kEmpty, rank, -1, 0, 0, 0, 0, uint64_t(kvh * gs + h));
+  };
+  auto row_max = [&](int h, int r0, int step) {
+    float M = -INFINITY;
+    for (int i = r0; i < S; i += step) {
+      const float* row = grp + (size_t(i) * gs + h) * wrl;
+      const float2 ml = make_float2(__ldcg(row), __ldcg(row + 1));
+      if (ml.y != 0.0f) M = fmaxf(M, ml.x);
     }
-    __syncthreads();
-    // In place: every thread reads all n rows of its elements before any
-    // result element is written, and each element has one owner thread.
-    for (int idx = threadIdx.x; idx < gs * d; idx += blockDim.x) {
-      const int h = idx / d, e = idx % d;
-      float o = 0.0f;
-      for (int i = 0; i < n; ++i) {
-        const float* r = row(i) + size_t(h) * wrl;
-        const float w = __ldcg(r + 1) != 0.0f ? expf(__ldcg(r) - s_M[h]) : 0.0f;
-        if (w != 0.0f) o = __fadd_rn(o, __fmul_rn(__ldcg(r + kWsO + e), w));
+    return M;
+  };
+  auto emit = [&](int h, float M, float L, const float (&O)[EL]) {
+    const size_t off = (size_t(b) * Hq + kvh * gs + h) * row_len;
+    const int hq = kvh * gs + h;
+    if (push) {
+      for (int dst = 0; dst < W; ++dst) {
+        float* r = P.inbox_all[dst] + base_src + off;
+        if (lane == 0) {
+          r[0] = M;
+          r[1] = L;
+        }
+#pragma unroll
+        for (int x = 0; x < EL; ++x)
+          if (lane + 32 * x < d) r[2 + lane + 32 * x] = O[x];
       }
-      put(h, 2 + e, o);
-      if (direct && s_L[h] != 0.0f) store_out(out, (size_t(b) * Hq + kvh * gs + h) * d + e, o / s_L[h], out_bf16);
+    } else {
+      float* r = pub + off;
+      if (lane == 0) {
+        r[0] = M;
+        r[1] = L;
+      }
+#pragma unroll
+      for (int x = 0; x < EL; ++x)
+        if (lane + 32 * x < d) r[2 + lane + 32 * x] = O[x];
     }
-    __syncthreads();
-    for (int h = threadIdx.x; h < gs; h += blockDim.x) {
-      put(h, 0, s_M[h]);
-      put(h, 1, s_L[h]);
+    if (direct) {
+      if (L == 0.0f) {
+        if (lane == 0) raise_err(P.err, TF_ERR_EMPTY_ATTENTION, kEmpty, rank, -1, 0, 0, 0, 0, uint64_t(hq));
+        return;
+      }
+      const size_t ooff = (size_t(b) * Hq + hq) * d;
+#pragma unroll
+      for (int x = 0; x < EL; ++x)
+        if (lane + 32 * x < d) store_out(out, ooff + lane + 32 * x, O[x] / L, out_bf16);
     }
+  };
+  // One load batch (every row of this warp's share in flight at once, m/l
+  // and o together): the common case, one L2 round trip per sub-item.
+  auto one_batch = [&](int h, int r0, int step, float (&v)[RB][EL], float2 (&ml)[RB]) {
+#pragma unroll
+    for (int u = 0; u < RB; ++u) {
+      const int i = r0 + u * step;
+      const float* row = grp + (size_t(i) * gs + h) * wrl;
+      ml[u] = i < S ? make_float2(__ldcg(row), __ldcg(row + 1)) : make_float2(0.f, 0.f);
+#pragma unroll
+      for (int x = 0; x < EL; ++x) {
+        const int e = lane + 32 * x;
+        v[u][x] = (i < S && e < d) ? __ldcg(row + kWsO + e) : 0.0f;
+      }
+    }
+  };
+  auto sum_batch = [&](const float (&v)[RB][EL], const float2 (&ml)[RB], float M, float& L, float (&O)[EL]) {
+    L = 0.0f;
+#pragma unroll
+    for (int x = 0; x < EL; ++x) O[x] = 0.0f;
+#pragma unroll
+    for (int u = 0; u < RB; ++u) {
+      const float w = ml[u].y != 0.0f ? expf(ml[u].x - M) : 0.0f;  // rows past S carry l = 0
+      L = __fadd_rn(L, __fmul_rn(ml[u].y, w));
+#pragma unroll
+      for (int x = 0; x < EL; ++x) O[x] = __fadd_rn(O[x], __fmul_rn(v[u][x], w));
+    }
+  };
+  auto batch_max = [&](const float2 (&ml)[RB]) {
+    float M = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < RB; ++u)
+      if (ml[u].y != 0.0f) M = fmaxf(M, ml[u].x);
+    return M;
+  };
+  if (wph == 1) {
+    // Whole heads per warp.
+    for (int hh = warp; hh < hc; hh += 8) {
+      const int h = h0 + hh;
+      float L, O[EL], M;
+      if (S <= RB) {
+        float v[RB][EL];
+        float2 ml[RB];
+        one_batch(h, 0, 1, v, ml);
+        M = batch_max(ml);
+        sum_batch(v, ml, M, L, O);
+      } else {
+        M = row_max(h, 0, 1);
+        fold_rows(h, 0, 1, M, L, O);
+      }
+      emit(h, M, L, O);
+    }
+    return;
   }
+  // wph warps per head: each warp folds its rows against its own max m_w
+  // (nothing held across the barrier), then the head combines the wph warp
+  // partials in ascending warp order: M = max m_w, L = sum L_w e^(m_w - M),
+  // O = sum O_w e^(m_w - M).
+  const int hh = warp / wph, j = warp % wph, h = h0 + hh;
+  float L, O[EL], Mw;
+  if ((S + wph - 1) / wph <= RB) {
+    float v[RB][EL];
+    float2 ml[RB];
+    one_batch(h, j, wph, v, ml);
+    Mw = batch_max(ml);
+    sum_batch(v, ml, Mw, L, O);
+  } else {
+    Mw = row_max(h, j, wph);
+    fold_rows(h, j, wph, Mw, L, O);
+  }
+  if (lane == 0) {
+    s_wm[warp] = Mw;
+    s_L[warp] = L;
+  }
+#pragma unroll
+  for (int x = 0; x < EL; ++x)
+    if (lane + 32 * x < d) s_O[warp * d + lane + 32 * x] = O[x];
+  __syncthreads();
+  if (j == 0) {
+    float M = -INFINITY;
+    for (int y = 0; y < wph; ++y)
+      if (s_L[warp + y] != 0.0f) M = fmaxf(M, s_wm[warp + y]);
+    float LL = 0.0f, OO[EL];
+#pragma unroll
+    for (int x = 0; x < EL; ++x) OO[x] = 0.0f;
+    for (int y = 0; y < wph; ++y) {
+      const float ly = s_L[warp + y];
+      if (ly == 0.0f) continue;
+      const float a = expf(s_wm[warp + y] - M);
+      LL = __fadd_rn(LL, __fmul_rn(ly, a));
+#pragma unroll
+      for (int x = 0; x < EL; ++x)
+        if (lane + 32 * x < d) OO[x] = __fadd_rn(OO[x], __fmul_rn(s_O[(warp + y) * d + lane + 32 * x], a));
+    }
+    emit(h, M, LL, OO);
+  }
+  __syncthreads();
 }
 
 // ---- the persistent kernel ------------------------------------------------
@@ -744,7 +771,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
   __shared__ unsigned int s_item;
   __shared__ int s_last, s_src;
   __shared__ FastSmem fsm;
-  __shared__ float s_M[32], s_L[32], s_w[kFoldW], s_l[kFoldW];
+  __shared__ float s_wm[8], s_fL[8], s_fO[8 * 256];
   const int G = P.B * P.Hkv;
   const unsigned total = unsigned(P.nlocal) * G * P.S;
   const int d = P.d, row_len = d + 2, wrl = ws_row(d);
@@ -753,6 +780,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
     if (tr && threadIdx.x == 0) tr[i] = globaltimer_ns();
   };
   stamp(0);
+  unsigned ranks_mask = 0;  // local ranks this CTA computed for
   __shared__ unsigned long long s_t0;  // CTA entry time (straggler model)
   if (threadIdx.x == 0) s_t0 = globaltimer_ns();
   if (tr && threadIdx.x == 0)
@@ -767,6 +795,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
     const int sp = item % P.S;
     const int g = (item / P.S) % G;
     const int lr = item / (unsigned(P.S) * G);
+    ranks_mask |= 1u << lr;
     if (P.r[lr].skew_ns) {  // straggler model: this rank's compute starts late
       if (threadIdx.x == 0)
         while (globaltimer_ns() - s_t0 < P.r[lr].skew_ns) __nanosleep(1000);
@@ -778,60 +807,106 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
     else if (MODE == 1) fast_split<false>(P, lr, g, sp, wsrow, fsm);
     else generic_split(P, lr, g, sp, wsrow);
     stamp(1);
-    // Two-level ticketed fold.  Level 1: the last split of each chunk of
-    // kChunk consecutive splits folds the chunk in place into its first
-    // row.  Level 2: the last chunk to finish folds the chunk rows into the
-    // rank's wire rows.  Each level is ~one L2 round trip (kChunk rows, all
-    // loads in flight), where one CTA folding all S rows paid S/UF of them.
-    const int nch = (P.S + kChunk - 1) / kChunk;
-    const int c = sp / kChunk, c0 = c * kChunk, cn = min(kChunk, P.S - c0);
-    unsigned long long* tks = P.ticket + (size_t(lr) * G + g) * (nch + 1);
-    auto ticket = [&](int slot, int count) {
-      __syncthreads();
-      if (threadIdx.x == 0) s_last = atom_add_acq_rel_gpu(&tks[slot], 1ull) == P.epoch * count - 1;
-      __syncthreads();
-      return s_last != 0;
-    };
-    if (!ticket(c, cn)) continue;
-    stamp(2);
-    if (nch > 1) {
-      if (cn > 1) fold_ws(P, lr, g, grp, c0, 1, cn, /*to_wire=*/0, s_M, s_L, s_w, s_l);
-      stamp(8);
-      if (!ticket(nch, nch)) continue;
-      stamp(9);
-      fold_ws(P, lr, g, grp, 0, kChunk, nch, /*to_wire=*/1, s_M, s_L, s_w, s_l);
-    } else {
-      fold_ws(P, lr, g, grp, 0, 1, P.S, /*to_wire=*/1, s_M, s_L, s_w, s_l);
+    if (tr && threadIdx.x == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      tr[14] = smid;
+      tr[15] = item;
     }
-    const FdRank& R = P.r[lr];
-    if (P.push) {
-      // bar.sync makes every thread's row stores visible to the releasing
-      // threads; the release (gpu scope for same-device inboxes, sys scope
-      // across NVLink) is cumulative over them -- no separate fence.
+    // Publish the split: bar.sync orders every thread's ws stores before
+    // thread 0's release (cumulative), which the split-fold acquires.
+    __syncthreads();
+    if (threadIdx.x == 0) red_release_gpu(P.done + size_t(lr) * G + g, 1);
+  }
+  stamp(2);
+  // Split-fold phase: sub-items (group, hc heads) of every local rank this
+  // CTA computed for, each waiting for its group's S splits.  Every compute
+  // item has been claimed by a CTA that never blocks before publishing it,
+  // so these waits always complete (no co-residency assumption), and every
+  // rank's sub-items are claimed by CTAs that computed for it.  CTAs that ran
+  // out of compute early fold finished groups while the others still
+  // stream; in a loopback world a rank's CTAs never sit on another rank's
+  // (straggling) groups -- they go on to the cross-rank fold, whose waits
+  // are the ones the tax meter attributes (flash_decode_test.cpp:250-286).
+  {
+    const int nhc = P.gs / P.hc;
+    const unsigned nsub = unsigned(G) * nhc;
+    int lr = 0;
+    for (;;) {
+      while (lr < P.nlocal && !((ranks_mask >> lr) & 1u)) ++lr;
+      if (lr >= P.nlocal) break;
       __syncthreads();
+      if (threadIdx.x == 0) s_item = atomicAdd(&P.sfc[lr], 1u);
+      __syncthreads();
+      const unsigned item = s_item;
+      __syncthreads();
+      if (item >= nsub) {
+        ++lr;
+        continue;
+      }
+      const int hb = item % nhc, g = item / nhc;
+      if (threadIdx.x == 0) {
+        // Intra-rank completion counter: a local spin, not a fabric signal
+        // (not counted as a signal wait in the tax meter).
+        const uint64_t* c = P.done + size_t(lr) * G + g;
+        const uint64_t want = P.epoch * uint64_t(P.S);
+        const uint64_t t0 = globaltimer_ns();
+        int ok = 1;
+        for (unsigned polls = 0; ld_acquire_gpu(c) < want; ++polls) {
+          if ((polls & 255u) == 255u) {
+            if (err_raised(P.err) || globaltimer_ns() - t0 > P.watchdog_ns) {
+              ok = 0;
+              break;
+            }
+          }
+        }
+        s_last = ok;
+      }
+      __syncthreads();
+      if (!s_last) break;  // an error elsewhere (e.g. NumericError) ends the launch
+      stamp(9);
+      if (P.d <= 128) fold_heads<4, 8>(P, lr, g, hb * P.hc, P.hc, s_wm, s_fL, s_fO);
+      else fold_heads<8, 4>(P, lr, g, hb * P.hc, P.hc, s_wm, s_fL, s_fO);
+      stamp(8);
+      // The last sub-item of a group releases its flags to every rank
+      // (push).  Every schedule counts, so the epoch-valued count stays in
+      // step with the ticket epoch.
+      const FdRank& R = P.r[lr];
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        // This sub-item's rows before the count (system scope only when a
+        // destination inbox is on another device).
+        if (P.push) {
+          if (P.local_dst == (P.W >= 64 ? ~0ull : ((1ull << P.W) - 1))) __threadfence();
+          else __threadfence_system();
+        }
+        s_last = atom_add_acq_rel_gpu(reinterpret_cast<unsigned long long*>(P.gtick + size_t(lr) * G + g), 1ull) ==
+                 P.epoch * uint64_t(nhc) - 1;
+      }
+      __syncthreads();
+      if (!P.push || !s_last) continue;
       stamp(7);
       if (threadIdx.x < P.W) {
         uint64_t* f = P.flags_all[threadIdx.x] + size_t(R.rank) * G + g;
         if ((P.local_dst >> threadIdx.x) & 1ull) red_release_gpu(f, 1);
         else red_release_sys(f, 1);
       }
-    }
-    stamp(3);
-    if (P.fold_inline && !P.direct) {
-      // Early fold: when every source of this group has already landed
-      // (always at W = 1; the last rank to push otherwise) fold it here
-      // instead of handing it to the fold phase.  Non-blocking check, so
-      // the compute phase still never waits.
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        bool all = true;
-        for (int i = 0; i < P.W && all; ++i) all = ld_acquire_sys(R.flags + size_t(i) * G + g) >= P.flag_epoch;
-        s_src = all && atomicMax(&P.claim[size_t(lr) * G + g], (unsigned long long)P.epoch) < P.epoch;
+      stamp(3);
+      if (P.fold_inline && !P.direct) {
+        // Early fold: when every source of this group has already landed
+        // (the last rank to push) fold it here instead of handing it to the
+        // fold phase.  Non-blocking check.
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          bool all = true;
+          for (int i = 0; i < P.W && all; ++i) all = ld_acquire_sys(R.flags + size_t(i) * G + g) >= P.flag_epoch;
+          s_src = all && atomicMax(&P.claim[size_t(lr) * G + g], (unsigned long long)P.epoch) < P.epoch;
+        }
+        __syncthreads();
+        const int mine = s_src;
+        __syncthreads();
+        if (mine) fold_group(P, lr, g, s_src);
       }
-      __syncthreads();
-      const int mine = s_src;
-      __syncthreads();
-      if (mine) fold_group(P, lr, g, s_src);
     }
   }
   stamp(4);
@@ -864,6 +939,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
       P.ctr[0] = 0;
       P.ctr[1] = 0;
       P.ctr[2] = 0;
+      for (int i = 0; i < P.nlocal; ++i) P.sfc[i] = 0;
       __threadfence();
     }
   }
@@ -1035,8 +1111,12 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   const int nlocal_max = std::min(w->n_local, kMaxLocal);
   const size_t ws_floats = size_t(nlocal_max) * G * S_eff * gs * ws_row(d);
   TFB_CHECK(heap_get(w, "fd.ws[" + std::to_string(ws_floats) + "]", sizeof(float) * ws_floats, &ws_off));
+  // Split-fold granularity: hc heads per sub-item, a power of two dividing
+  // gs, as many as keep a warp's share at <= 8 rows (one load batch).
+  int hc = 1;
+  while (hc * 2 <= 32 && gs % (hc * 2) == 0 && S_eff * hc * 2 <= 64) hc *= 2;
   TFB_CHECK(heap_get(w, "fd.tickets[" + std::to_string(G) + "x" + std::to_string(S_eff) + "]",
-                     sizeof(unsigned long long) * nlocal_max * G * (S_eff / kChunk + 3), &tick_off));  // tickets | claims
+                     sizeof(unsigned long long) * (nlocal_max * G * 3 + kMaxLocal), &tick_off));  // done | gtick | claims | sfc
   TFB_CHECK(heap_get(w, "fd.ctr", 64, &ctr_off));
   // Tickets are epoch-valued per (group, split-count) geometry.
   const uint64_t tepoch = ++w->epochs["fd.tickets@" + std::to_string(tick_off)];
@@ -1102,8 +1182,11 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
           TFB_CHECK(heap_get(w, "fd.trace", sizeof(unsigned long long) * 16 * 4096, &toff));
           Q.trace = reinterpret_cast<unsigned long long*>(w->ptr(lead, toff));
         }
-        Q.ticket = reinterpret_cast<unsigned long long*>(w->ptr(lead, tick_off));
-        Q.claim = Q.ticket + size_t(nlocal_max) * G * ((S_eff + kChunk - 1) / kChunk + 1);
+        Q.done = reinterpret_cast<uint64_t*>(w->ptr(lead, tick_off));
+        Q.gtick = Q.done + size_t(nlocal_max) * G;
+        Q.claim = reinterpret_cast<unsigned long long*>(Q.gtick + size_t(nlocal_max) * G);
+        Q.sfc = reinterpret_cast<unsigned int*>(Q.claim + size_t(nlocal_max) * G);
+        Q.hc = hc;
         Q.local_dst = 0;
         for (int r = 0; r < W; ++r)
           if (w->ranks[r].local && w->ranks[r].device == kv.first) Q.local_dst |= 1ull << r;

@@ -22,10 +22,34 @@ with tf.World(1, [0], 512 << 20) as w:
     t = w.get(ptr, (4096, 16), np.uint64).astype(np.int64)
     t = t[t[:, 0] > 0]
     t0 = t[:, 0].min()
-    names = ["entry", "computed", "ticketed", "group-fold+push", "fold-phase", "fold-item", "exit", "group-folded",
-             "L1-folded", "L2-ticketed", "L1:ml-in", "L2:ml-in", "q-in-smem", "warps-done"]
+    names = ["entry", "computed", "split-published", "flags+early-fold", "fold-phase", "fold-item", "exit",
+             "flags-released", "split-folded", "split-fold-start", "-", "-", "q-in-smem",
+             "warps-done"]
     for i, n in enumerate(names):
         col = t[:, i]
         col = col[col > 0] - t0
         if len(col):
             print(f"{n:16s} n={len(col):4d}  min {col.min()/1e3:7.2f}  p50 {np.median(col)/1e3:7.2f}  max {col.max()/1e3:7.2f} us")
+    # Per-CTA streaming time (q in smem -> warps done) vs SM and group.
+    dur = (t[:, 13] - t[:, 12]) / 1e3
+    sm = t[:, 14]
+    item = t[:, 15]
+    S = int(os.environ.get("TFB_FD_SPLITS", "37"))
+    grp = item // S
+    print("stream us: min %.1f p50 %.1f max %.1f" % (dur.min(), np.median(dur), dur.max()))
+    for gi in range(8):
+        sel = grp == gi
+        if sel.any():
+            print("  group %d: n=%3d mean %.1f min %.1f max %.1f" % (gi, sel.sum(), dur[sel].mean(), dur[sel].min(),
+                                                                 dur[sel].max()))
+    order = np.argsort(sm)
+    per_sm = {}
+    for s_, d_ in zip(sm, dur):
+        per_sm.setdefault(int(s_), []).append(d_)
+    sms = sorted(per_sm)
+    row = ["%d:%.0f" % (s_, max(per_sm[s_])) for s_ in sms]
+    print("per-SM max stream us:", " ".join(row))
+    split = t[:, 15] % S
+    for lo, hi in ((0, 12), (12, 25), (25, 37)):
+        sel = (split >= lo) & (split < hi)
+        print("  splits %d-%d: mean %.1f" % (lo, hi - 1, dur[sel].mean()))
