@@ -91,6 +91,9 @@ struct AgTcParams {
   int board;
   int dbg;  // TFB_DEBUG knobs: 1 skip C stores, 2 skip MMAs, 8 force CG=1, 16 skip the split-K reduce (profiling aids)
   int ksplit;  // > 1: skinny-M split-K across a cluster of ksplit CTAs (pairs), reduced through DSMEM
+  int full_items;   // items [0, full_items) are whole tiles (x k-splits)
+  int q_tail;       // > 1: the tiles after them run as q_tail column slices each (last-wave balance)
+  int total_items;
   int ldc;     // row pitch of C (elements)
   const __nv_bfloat16* peer_shard[64];
 };
@@ -232,12 +235,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // Work items: (tile, k-split).  Split ks covers k-block slots
   // [ks*kb/S, (ks+1)*kb/S) of the rank's rotated k order (never empty:
   // the host keeps kb_total >= 4 * ksplit).
-  const int num_tiles = num_mt * p.num_n * p.ksplit;
+  const int num_tiles = p.total_items;
   auto item_coords = [&](int t, int& mt, int& nb, int& i0, int& i1) {
     const int ks = t % p.ksplit;
     tile_coords(num_mt, p.num_n, t / p.ksplit, mt, nb);
     i0 = ks * p.kb_total / p.ksplit;
     i1 = (ks + 1) * p.kb_total / p.ksplit;
+  };
+  // Item geometry: rows (tile row mt), columns [col0, col0 + w), k-blocks
+  // [i0, i1).  The tiles of a partial last wave are cut into q_tail column
+  // slices (w = BN_TILE / q_tail: 256 or 128) so every pair has work at the
+  // end instead of a quarter of them running whole tiles.
+  auto item_geom = [&](int t, int& mt, int& col0, int& w, int& i0, int& i1) {
+    int nb;
+    if (t < p.full_items) {
+      item_coords(t, mt, nb, i0, i1);
+      col0 = nb * K_::BN_TILE;
+      w = K_::BN_TILE;
+    } else {
+      const int j = t - p.full_items;
+      tile_coords(num_mt, p.num_n, p.full_items + j / p.q_tail, mt, nb);
+      w = K_::BN_TILE / p.q_tail;
+      col0 = nb * K_::BN_TILE + (j % p.q_tail) * w;
+      i0 = 0;
+      i1 = p.kb_total;
+    }
   };
 
   if (warp == 0 && lane == 0) {
@@ -268,10 +290,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cid; t < num_tiles; t += ncl) {
-        int mt, nb, i0, i1;
-        item_coords(t, mt, nb, i0, i1);
+        int mt, n0, wcol, i0, i1;
+        item_geom(t, mt, n0, wcol, i0, i1);
         const int mb = mt * CG + int(prank);  // this CTA's 128-row block
-        const int m0 = mb * BM, n0 = nb * K_::BN_TILE;
+        const int m0 = mb * BM;
+        // B chunks (64 columns) this CTA stages per k-block: its share of
+        // every 256-column MMA (CG = 2: 128 columns), or of one 128-wide one.
+        const int nhalf = wcol >= 256 ? wcol / 256 : 1;
+        const int cpc = wcol >= 256 ? CPH : 2 / CG;  // chunks per MMA per CTA
+        const uint32_t tx = uint32_t(CG) * uint32_t(A_BYTES + nhalf * cpc * BK * 128);
         uint64_t ready_mask = 0;
         for (int i = i0; i < i1; ++i) {
           const int kb = p.own >= 0 ? (i + p.own * p.kbw) % p.kb_total : i;
@@ -285,18 +312,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ready_mask |= 1ull << src;
           }
           const uint32_t bar = CG == 2 ? mapa(&full[stage], lead) : smem_u32(&full[stage]);
-          if (leader) mbar_arrive_expect_tx(&full[stage], CG * K_::STAGE_BYTES);
+          if (leader) mbar_arrive_expect_tx(&full[stage], tx);
           else mbar_arrive_cluster(bar);
           uint8_t* a_dst = smA + stage * A_BYTES;
           if (from_own) tma_load<CG>(a_dst, &tmA_own, bar, kb * BK - p.own * p.kw, m0);
           else tma_load<CG>(a_dst, &tmA_inbox, bar, kb * BK, m0);
           uint8_t* b_dst = smB + stage * K_::B_BYTES;
-#pragma unroll
-          for (int h = 0; h < NH; ++h)
-#pragma unroll
-            for (int c = 0; c < CPH; ++c)
+          for (int h = 0; h < nhalf; ++h)
+            for (int c = 0; c < cpc; ++c)
               tma_load<CG>(b_dst + (h * CPH + c) * (BK * 128), &tmB, bar,
-                           n0 + h * 256 + int(prank) * (256 / CG) + c * 64, kb * BK);
+                           n0 + h * 256 + int(prank) * (cpc * 64) + c * 64, kb * BK);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -312,8 +337,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int acc = 0;
       uint32_t aphase = 0;
       for (int t = cid; t < num_tiles; t += ncl) {
-        int mt_, nb_, i0, i1;
-        item_coords(t, mt_, nb_, i0, i1);
+        int mt_, c0_, wcol, i0, i1;
+        item_geom(t, mt_, c0_, wcol, i0, i1);
+        const int nhalf = wcol >= 256 ? wcol / 256 : 1;
+        const uint32_t idesc = wcol >= 256 ? K_::IDESC : idesc_bf16(BM * CG, wcol, 0, 1);
         mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
         for (int i = i0; i < i1; ++i) {
@@ -326,13 +353,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int k = 0; k < BK / 16; ++k) {
               // A: K-major SW128, 8-row groups 1024 B apart; +32 B per K=16.
               const uint64_t ad = smem_desc_sw128(a_addr + k * 32, 16, 1024);
-#pragma unroll
-              for (int h = 0; h < NH; ++h) {
+              for (int h = 0; h < nhalf; ++h) {
                 // B: MN-major SW128, 64-column chunks 8 KB apart (LBO),
                 // 8-row K groups 1 KB apart (SBO); +16 rows (2 KB) per K=16.
                 const uint64_t bd = smem_desc_sw128(b_addr + h * CPH * (BK * 128) + k * 2048, BK * 128, 1024);
-                mma_issue<CG>(tmem_base + uint32_t((acc * NH + h) * 256), ad, bd, K_::IDESC,
-                              ((i - i0) | k) != 0);
+                mma_issue<CG>(tmem_base + uint32_t((acc * NH + h) * 256), ad, bd, idesc, ((i - i0) | k) != 0);
               }
             }
           }
@@ -357,9 +382,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tempty_leader0 = CG == 2 ? mapa(&tempty[0], lead) : smem_u32(&tempty[0]);
     // Split-K: one item per CTA, reduced after the role loops (below).
     for (int t = p.ksplit > 1 ? num_tiles : cid; t < num_tiles; t += ncl) {
-      int mt, nb;
+      int mt, col0, wcol;
       int i0_, i1_;
-      item_coords(t, mt, nb, i0_, i1_);
+      item_geom(t, mt, col0, wcol, i0_, i1_);
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       // 64-column slabs: two tcgen05.ld (32 columns each) -> bf16 -> a
@@ -369,7 +394,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int row0 = (mt * CG + int(prank)) * BM + 32 * q;
       uint8_t* stg = smStage + q * (2 * 4096);
 #pragma unroll 1
-      for (int cc = 0; cc < NH * 4; ++cc) {
+      for (int cc = 0; cc < wcol / 64; ++cc) {
         uint32_t r0[32], r1[32];
         const uint32_t tcol = uint32_t(acc * NH * 256 + 64 * cc);
         tmem_ld_32x32b_x32(tmem_base + (uint32_t(32 * q) << 16) + tcol, r0);
@@ -391,7 +416,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         fence_proxy_async_shared();
         __syncwarp();
         if (lane == 0 && !(p.dbg & 1) && row0 < p.M) {
-          tma_store_2d(&tmC, buf, nb * K_::BN_TILE + 64 * cc, row0);
+          tma_store_2d(&tmC, buf, col0 + 64 * cc, row0);
           bulk_commit();
         }
       }
@@ -777,6 +802,9 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   p.num_n = num_n;
   p.num_tiles = tiles;
   p.ksplit = ks;
+  p.full_items = tiles * ks;
+  p.q_tail = 1;
+  p.total_items = tiles * ks;
   if (std::getenv("TFB_KSPLIT_VERBOSE"))
     std::fprintf(stderr, "[ag] m=%zu n=%zu k=%zu CG=%d NH=%d tiles=%d ksplit=%d\n", sh.m, sh.n, sh.k, CG,
                  shp->NH, tiles, ks);
@@ -793,6 +821,22 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   unsigned grid = std::min(pair_tiles * CG, grid_cap / CG * CG);
   grid = std::max(grid, unsigned(CG));
   if (p.ksplit > 1) grid = pair_tiles * CG;  // exactly one item per CTA (the reduction aliases its smem)
+  // Last-wave balance (CTA pairs, whole-K tiles): when the tiles leave a
+  // partial last round, cut its tiles into 2 or 4 column slices so that
+  // round runs on (nearly) every pair for a half or quarter of a tile time.
+  if (CG == 2 && p.ksplit == 1 && !std::getenv("TFB_NO_TAIL_SPLIT")) {
+    const int ncl = int(grid) / CG, T = p.num_tiles;
+    const int fr = T / ncl, rem = T % ncl;
+    if (fr >= 1 && rem > 0) {
+      int q = shp->NH == 2 ? 4 : 2;
+      while (q > 1 && rem * q > ncl) q /= 2;
+      if (q > 1) {
+        p.full_items = fr * ncl;
+        p.q_tail = q;
+        p.total_items = p.full_items + rem * q;
+      }
+    }
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(NUM_THREADS);

@@ -86,3 +86,18 @@ def test_repeated_runs_reuse_flags(oracle):
                                         _abi.ptr_array([c.data_ptr() for c in Cs]), None, None))
             for c in Cs:
                 assert norm_err(c.float().cpu().numpy(), ref) <= TOL, it
+
+
+def test_last_wave_column_slices_bitwise(oracle, monkeypatch):
+    """80 CTA-pair tiles on 74 pairs: the 6 tiles of the partial last round
+    run as 4 column slices each (N=128 / 256 MMAs).  Same k order per
+    element, so C is bitwise the whole-tile result."""
+    import torch
+    m, n, k = 1024, 10240, 256
+    p = bf16_problem(31, m, n, k, oracle)
+    sliced = tf.ag.run_pull(p, tf.WorldConfig(world_size=1), dtype=1).c[0]
+    monkeypatch.setenv("TFB_NO_TAIL_SPLIT", "1")
+    whole = tf.ag.run_pull(p, tf.WorldConfig(world_size=1), dtype=1).c[0]
+    assert np.array_equal(sliced, whole)
+    ref = (torch.from_numpy(p.a).double() @ torch.from_numpy(p.b).double()).float().numpy()
+    assert norm_err(sliced, ref) <= TOL

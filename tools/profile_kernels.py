@@ -14,8 +14,9 @@ from paper_2511_02168_b200 import _abi  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "ag"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-if which == "ag":
-    M, N, K = 8192, 28672, 8192
+if which.startswith("ag"):
+    # ag: config 2; agM<m>: config 5's M x 8192 x 8192 (e.g. agM128: split-K cluster path)
+    M, N, K = (8192, 28672, 8192) if which == "ag" else (int(which[3:]), 8192, 8192)
     with tf.World(1, [0], M * K * 2 + (64 << 20)) as w:
         sh = w.alloc("ag.a", M * K * 2)
         A = (torch.rand(M, K, device="cuda") * 2 - 1).bfloat16()
