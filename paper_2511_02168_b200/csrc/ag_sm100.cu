@@ -385,7 +385,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int mt, col0, wcol;
       int i0_, i1_;
       item_geom(t, mt, col0, wcol, i0_, i1_);
-      mbar_wait(&tfull[acc], aphase);
+      if (!(p.dbg & 32)) mbar_wait_sleep(&tfull[acc], aphase);
+      else mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       // 64-column slabs: two tcgen05.ld (32 columns each) -> bf16 -> a
       // SWIZZLE_128B smem box [32 rows][64 cols] (conflict-free: 16-byte
@@ -787,7 +788,10 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   const Shape* shp = &shapes[(p.num_m >= 2 && !(p.dbg & 8)) ? 1 : 0];
   int tiles = 0, num_n = 0, ks = 1;
   TFB_CHECK(plan(*shp, tiles, num_n, ks));
-  if (shp->CG == 2 && !std::getenv("TFB_NO_NARROW")) {
+  if (shp->CG == 2 && std::getenv("TFB_FORCE_NARROW")) {
+    shp = &shapes[2];
+    TFB_CHECK(plan(*shp, tiles, num_n, ks));
+  } else if (shp->CG == 2 && !std::getenv("TFB_NO_NARROW")) {
     int t2, n2, k2;
     TFB_CHECK(plan(shapes[2], t2, n2, k2));
     // Narrow pair tiles only when the wide ones leave a quarter of the SMs idle.

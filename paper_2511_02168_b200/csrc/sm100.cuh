@@ -32,6 +32,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Long waits (the epilogue waiting out a whole mainloop): try_wait with a
+// suspend-time hint parks the warp until the phase completes instead of
+// re-polling -- the plain loop above re-issued ~25M try_waits per config-2
+// GEMM, a third of all instructions (profiles/r1_ncu.md).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITS_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
 // Wait for a phase completed by ANOTHER CTA of the cluster (multicast commit,
 // remote arrive): poll with test_wait (acquire at cluster scope) instead of
 // try_wait, whose hardware suspend is only woken early by local arrivals.
