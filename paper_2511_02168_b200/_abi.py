@@ -12,7 +12,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtilefabric_b200.so")
+LIB_PATH = os.environ.get("TFB_LIB") or os.path.join(HERE, "libtilefabric_b200.so")
 
 # tf_status -> the reference's exception classes (common.hpp:39-94).
 

@@ -89,7 +89,8 @@ struct AgTcParams {
   uint64_t watchdog_ns;
   DevErr* err;
   int board;
-  int dbg;  // TFB_DEBUG knobs: 1 skip C stores, 2 skip MMAs, 8 force CG=1, 16 skip the split-K reduce (profiling aids)
+  int dbg;  // TFB_DEBUG knobs: 1 skip C stores, 2 skip MMAs, 8 force CG=1, 16 skip the split-K reduce,
+           // 32 poll-wait the epilogue, 64 skip the epilogue (profiling aids)
   int ksplit;  // > 1: skinny-M split-K across a cluster of ksplit CTAs (pairs), reduced through DSMEM
   int full_items;   // items [0, full_items) are whole tiles (x k-splits)
   int q_tail;       // > 1: the tiles after them run as q_tail column slices each (last-wave balance)
@@ -318,10 +319,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (from_own) tma_load<CG>(a_dst, &tmA_own, bar, kb * BK - p.own * p.kw, m0);
           else tma_load<CG>(a_dst, &tmA_inbox, bar, kb * BK, m0);
           uint8_t* b_dst = smB + stage * K_::B_BYTES;
-          for (int h = 0; h < nhalf; ++h)
-            for (int c = 0; c < cpc; ++c)
-              tma_load<CG>(b_dst + (h * CPH + c) * (BK * 128), &tmB, bar,
-                           n0 + h * 256 + int(prank) * (cpc * 64) + c * 64, kb * BK);
+          if (wcol == K_::BN_TILE) {
+#pragma unroll
+            for (int h = 0; h < NH; ++h)
+#pragma unroll
+              for (int c = 0; c < CPH; ++c)
+                tma_load<CG>(b_dst + (h * CPH + c) * (BK * 128), &tmB, bar,
+                             n0 + h * 256 + int(prank) * (CPH * 64) + c * 64, kb * BK);
+          } else {
+            for (int h = 0; h < nhalf; ++h)
+              for (int c = 0; c < cpc; ++c)
+                tma_load<CG>(b_dst + (h * CPH + c) * (BK * 128), &tmB, bar,
+                             n0 + h * 256 + int(prank) * (cpc * 64) + c * 64, kb * BK);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -339,6 +349,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int t = cid; t < num_tiles; t += ncl) {
         int mt_, c0_, wcol, i0, i1;
         item_geom(t, mt_, c0_, wcol, i0, i1);
+        const bool whole = wcol == K_::BN_TILE;
         const int nhalf = wcol >= 256 ? wcol / 256 : 1;
         const uint32_t idesc = wcol >= 256 ? K_::IDESC : idesc_bf16(BM * CG, wcol, 0, 1);
         mbar_wait(&tempty[acc], aphase ^ 1);
@@ -353,11 +364,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int k = 0; k < BK / 16; ++k) {
               // A: K-major SW128, 8-row groups 1024 B apart; +32 B per K=16.
               const uint64_t ad = smem_desc_sw128(a_addr + k * 32, 16, 1024);
-              for (int h = 0; h < nhalf; ++h) {
-                // B: MN-major SW128, 64-column chunks 8 KB apart (LBO),
-                // 8-row K groups 1 KB apart (SBO); +16 rows (2 KB) per K=16.
-                const uint64_t bd = smem_desc_sw128(b_addr + h * CPH * (BK * 128) + k * 2048, BK * 128, 1024);
-                mma_issue<CG>(tmem_base + uint32_t((acc * NH + h) * 256), ad, bd, idesc, ((i - i0) | k) != 0);
+              // B: MN-major SW128, 64-column chunks 8 KB apart (LBO),
+              // 8-row K groups 1 KB apart (SBO); +16 rows (2 KB) per K=16.
+              // Whole tiles take the unrolled constant-descriptor path: the
+              // single issuing thread must stay well ahead of the tensor pipe
+              // (a runtime-bounded loop here cost 16 % of the config-2 cycles).
+              if (whole) {
+#pragma unroll
+                for (int h = 0; h < NH; ++h) {
+                  const uint64_t bd = smem_desc_sw128(b_addr + h * CPH * (BK * 128) + k * 2048, BK * 128, 1024);
+                  mma_issue<CG>(tmem_base + uint32_t((acc * NH + h) * 256), ad, bd, K_::IDESC,
+                                ((i - i0) | k) != 0);
+                }
+              } else {
+                for (int h = 0; h < nhalf; ++h) {
+                  const uint64_t bd = smem_desc_sw128(b_addr + h * CPH * (BK * 128) + k * 2048, BK * 128, 1024);
+                  mma_issue<CG>(tmem_base + uint32_t((acc * NH + h) * 256), ad, bd, idesc, ((i - i0) | k) != 0);
+                }
               }
             }
           }
@@ -395,7 +418,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int row0 = (mt * CG + int(prank)) * BM + 32 * q;
       uint8_t* stg = smStage + q * (2 * 4096);
 #pragma unroll 1
-      for (int cc = 0; cc < wcol / 64; ++cc) {
+      for (int cc = 0; cc < ((p.dbg & 64) ? 0 : wcol / 64); ++cc) {
         uint32_t r0[32], r1[32];
         const uint32_t tcol = uint32_t(acc * NH * 256 + 64 * cc);
         tmem_ld_32x32b_x32(tmem_base + (uint32_t(32 * q) << 16) + tcol, r0);
