@@ -191,7 +191,7 @@ def time_steps(ctx, stream, fn, steps, warmup):
 # ---------------------------------------------------------------------------------
 # AG+GEMM (headline)
 
-def bench_ag(ctx, steps, warmup, variant_name="pull"):
+def bench_ag(ctx, steps, warmup, variant_name="pull", cooldown=lambda: None):
     from paper_2511_02168_b200 import _abi
     torch = ctx.torch
     W = ctx.W
@@ -226,7 +226,9 @@ def bench_ag(ctx, steps, warmup, variant_name="pull"):
             rows = torch.arange(0, M, M // 64, device=ctx.dev)
             ref = A_local[rows].float() @ B.float()
             err = float(((Cm[rows].float() - ref).abs().max() / ref.abs().max()).item())
-        # BSP baseline: NCCL all-gather (W > 1) + relayout + cuBLAS.
+        # BSP baseline: NCCL all-gather (W > 1) + relayout + cuBLAS, from
+        # the same idle-GPU start as the fused run.
+        cooldown()
         bsp_ms = bench_bsp_ag(ctx, A_local, B, steps, warmup)
         # End to end through the C ABI with host buffers: H2D of the shard and
         # B from pinned memory, the fused step, D2H of C -- every step.
@@ -359,7 +361,9 @@ def bench_fd(ctx, cfg, steps, warmup):
                     _abi.ptr_array(ptrs_for(ctx, k.data_ptr())), _abi.ptr_array(ptrs_for(ctx, v.data_ptr())),
                     _abi.ptr_array(ptrs_for(ctx, out.data_ptr())), None, None)
             step = lambda: _abi.check(w.lib.tf_flash_decode_async(*args))  # noqa: E731
-            res[name] = time_steps(ctx, w.stream(ctx.rank), step, steps, warmup)
+            with ClockSampler(ctx.local) as clk:
+                res[name] = time_steps(ctx, w.stream(ctx.rank), step, steps, warmup)
+            res[name + "_clocks"] = clk.summary()
         _abi.check(w.lib.tf_world_sync(w.handle))
         # numerics spot check (W=1): torch fp32 attention on the same bf16 data
         err = None
@@ -371,7 +375,8 @@ def bench_fd(ctx, cfg, steps, warmup):
             ref = torch.einsum("hgl,hld->hgd", torch.softmax(s, -1), v[bb].float()).reshape(Hq, d)
             err = float(((out[bb].float() - ref).abs().amax(-1) / ref.abs().amax(-1)).max().item())
         kv_bytes = 2 * B * Hkv * ln * d * 2
-        return dict(fused_ms=res["fused"], bsp_ms=res["bsp"], kv_bytes=kv_bytes, err=err)
+        return dict(fused_ms=res["fused"], bsp_ms=res["bsp"], kv_bytes=kv_bytes, err=err,
+                    clocks=res["fused_clocks"])
     finally:
         w.close()
 
@@ -460,6 +465,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-fd", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the config-5 M sweep")
+    ap.add_argument("--cooldown", type=float, default=2.0, help="idle seconds before each timed section")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
@@ -467,13 +473,26 @@ def main():
     args.warmup = max(args.warmup, 3)
     ctx = Ctx(args.gpus)
     pk = peaks()
-    ag_res = bench_ag(ctx, args.steps, args.warmup)
+
+    def cooldown():
+        # Each workload is timed from an idle GPU: the power-capped clock
+        # state a long GEMM leaves behind (sw_power_cap) would otherwise
+        # carry into the next, memory-bound, section.
+        ctx.torch.cuda.synchronize()
+        ctx.barrier()
+        time.sleep(args.cooldown)
+        ctx.barrier()
+
     fd3 = fd4 = sweep = None
-    if not args.no_sweep:
-        sweep = bench_msweep(ctx, max(5, args.steps // 4), args.warmup)
     if not args.no_fd:
+        cooldown()
         fd3 = bench_fd(ctx, FD3, args.steps, args.warmup)
         fd4 = bench_fd(ctx, FD4, max(5, args.steps // 2), args.warmup)
+    cooldown()
+    ag_res = bench_ag(ctx, args.steps, args.warmup, cooldown=cooldown)
+    if not args.no_sweep:
+        cooldown()
+        sweep = bench_msweep(ctx, max(5, args.steps // 4), args.warmup)
     if ctx.rank != 0:
         return
     W = ctx.W
@@ -515,7 +534,7 @@ def main():
                          "fused_speedup_vs_bsp": r["bsp_ms"] / r["fused_ms"],
                          "roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm"], "unit": "GB/s",
                                       "frac": gbs / pk["hbm"], "algorithmic_bytes_per_launch": r["kv_bytes"]},
-                         "head_rel_err_vs_torch_fp32": r["err"], "config": cfg}
+                         "head_rel_err_vs_torch_fp32": r["err"], "config": cfg, "clocks": r["clocks"]}
         line["secondary"] = sec
     if sweep:
         line.setdefault("secondary", {})["ag_msweep_K8192_N8192"] = {
