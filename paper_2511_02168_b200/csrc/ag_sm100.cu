@@ -341,54 +341,91 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ===== MMA issuer (leader CTA, one thread) =====
+    // 256 x 512 tiles (NH = 2) keep ONE accumulator (the whole TMEM), so the
+    // epilogue of tile t drains it while tile t+1 waits.  The drain is split
+    // per 256-column half (tempty[0] / tempty[1]): tile t+1 issues its
+    // half-0 MMAs for the first STAGES k-blocks as soon as half 0 is free,
+    // and catches up half 1 once the epilogue has drained it.
     if (lane == 0 && leader) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t aphase = 0;
+      auto mma_kblock = [&](int stg, int h0, int h1, bool first_kb, bool whole, int nhalf, uint32_t idesc) {
+        const uint32_t a_addr = smem_u32(smA + stg * A_BYTES);
+        const uint32_t b_addr = smem_u32(smB + stg * K_::B_BYTES);
+        if (p.dbg & 2) return;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          // A: K-major SW128, 8-row groups 1024 B apart; +32 B per K=16.
+          const uint64_t ad = smem_desc_sw128(a_addr + k * 32, 16, 1024);
+          // B: MN-major SW128, 64-column chunks 8 KB apart (LBO), 8-row K
+          // groups 1 KB apart (SBO); +16 rows (2 KB) per K=16.  Whole tiles
+          // take the unrolled constant-descriptor path: the single issuing
+          // thread must stay well ahead of the tensor pipe (a runtime-bounded
+          // loop here cost 16 % of the config-2 cycles).
+          if (whole) {
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+              if (h < h0 || h >= h1) continue;
+              const uint64_t bd = smem_desc_sw128(b_addr + h * CPH * (BK * 128) + k * 2048, BK * 128, 1024);
+              mma_issue<CG>(tmem_base + uint32_t((acc * NH + h) * 256), ad, bd, K_::IDESC, !first_kb || k != 0);
+            }
+          } else {
+            for (int h = 0; h < nhalf; ++h) {
+              const uint64_t bd = smem_desc_sw128(b_addr + h * CPH * (BK * 128) + k * 2048, BK * 128, 1024);
+              mma_issue<CG>(tmem_base + uint32_t((acc * NH + h) * 256), ad, bd, idesc, !first_kb || k != 0);
+            }
+          }
+        }
+      };
+      auto advance = [&](int& stg, uint32_t& ph) {
+        if (++stg == STAGES) {
+          stg = 0;
+          ph ^= 1;
+        }
+      };
       for (int t = cid; t < num_tiles; t += ncl) {
         int mt_, c0_, wcol, i0, i1;
         item_geom(t, mt_, c0_, wcol, i0, i1);
         const bool whole = wcol == K_::BN_TILE;
         const int nhalf = wcol >= 256 ? wcol / 256 : 1;
         const uint32_t idesc = wcol >= 256 ? K_::IDESC : idesc_bf16(BM * CG, wcol, 0, 1);
-        mbar_wait(&tempty[acc], aphase ^ 1);
-        tc_fence_after();
-        for (int i = i0; i < i1; ++i) {
+        int i = i0;
+        if (NH == 2 && whole) {
+          mbar_wait(&tempty[0], aphase ^ 1);
+          tc_fence_after();
+          const int pre = min(STAGES, i1 - i0);
+          int s2 = stage;
+          uint32_t p2 = phase;
+          for (int j = 0; j < pre; ++j) {
+            mbar_wait(&full[s2], p2);
+            tc_fence_after();
+            mma_kblock(s2, 0, 1, j == 0, true, 2, idesc);
+            advance(s2, p2);
+          }
+          mbar_wait(&tempty[1], aphase ^ 1);
+          tc_fence_after();
+          for (int j = 0; j < pre; ++j) {
+            mma_kblock(stage, 1, 2, j == 0, true, 2, idesc);
+            mma_commit_all<CG>(&empty[stage], pair_mask);
+            advance(stage, phase);
+          }
+          i = i0 + pre;
+        } else if (NH == 2) {
+          mbar_wait(&tempty[0], aphase ^ 1);
+          mbar_wait(&tempty[1], aphase ^ 1);
+          tc_fence_after();
+        } else {
+          mbar_wait(&tempty[acc], aphase ^ 1);
+          tc_fence_after();
+        }
+        for (; i < i1; ++i) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(smA + stage * A_BYTES);
-          const uint32_t b_addr = smem_u32(smB + stage * K_::B_BYTES);
-          if (!(p.dbg & 2)) {
-#pragma unroll
-            for (int k = 0; k < BK / 16; ++k) {
-              // A: K-major SW128, 8-row groups 1024 B apart; +32 B per K=16.
-              const uint64_t ad = smem_desc_sw128(a_addr + k * 32, 16, 1024);
-              // B: MN-major SW128, 64-column chunks 8 KB apart (LBO),
-              // 8-row K groups 1 KB apart (SBO); +16 rows (2 KB) per K=16.
-              // Whole tiles take the unrolled constant-descriptor path: the
-              // single issuing thread must stay well ahead of the tensor pipe
-              // (a runtime-bounded loop here cost 16 % of the config-2 cycles).
-              if (whole) {
-#pragma unroll
-                for (int h = 0; h < NH; ++h) {
-                  const uint64_t bd = smem_desc_sw128(b_addr + h * CPH * (BK * 128) + k * 2048, BK * 128, 1024);
-                  mma_issue<CG>(tmem_base + uint32_t((acc * NH + h) * 256), ad, bd, K_::IDESC,
-                                ((i - i0) | k) != 0);
-                }
-              } else {
-                for (int h = 0; h < nhalf; ++h) {
-                  const uint64_t bd = smem_desc_sw128(b_addr + h * CPH * (BK * 128) + k * 2048, BK * 128, 1024);
-                  mma_issue<CG>(tmem_base + uint32_t((acc * NH + h) * 256), ad, bd, idesc, ((i - i0) | k) != 0);
-                }
-              }
-            }
-          }
+          mma_kblock(stage, 0, NH, i == i0, whole, nhalf, idesc);
           mma_commit_all<CG>(&empty[stage], pair_mask);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+          advance(stage, phase);
         }
         mma_commit_all<CG>(&tfull[acc], pair_mask);
         if (++acc == K_::ACC_BUFS) {
@@ -397,12 +434,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else if (warp < 6) {
+  } else if (warp < 6 || (NH == 2 && !p.gather && warp < 10)) {
     // ===== epilogue (both CTAs): TMEM -> registers -> bf16 -> global =====
+    // Warps 2-5; with NH = 2 and no gather work (W = 1, push, baseline) also
+    // warps 6-9, the two sets draining the two 256-column halves at once.
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const bool epi8 = NH == 2 && !p.gather;
+    const int e = warp - 2, set = epi8 && warp >= 6 ? 1 : 0;
     int acc = 0;
     uint32_t aphase = 0;
     const uint32_t tempty_leader0 = CG == 2 ? mapa(&tempty[0], lead) : smem_u32(&tempty[0]);
+    auto arrive = [&](int idx) {
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(tempty_leader0 + uint32_t(idx) * 8);
+        else mbar_arrive(&tempty[idx]);
+      }
+    };
+    int nst = 0;  // TMA stores issued by this warp (staging-buffer reuse)
     // Split-K: one item per CTA, reduced after the role loops (below).
     for (int t = p.ksplit > 1 ? num_tiles : cid; t < num_tiles; t += ncl) {
       int mt, col0, wcol;
@@ -414,18 +462,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // 64-column slabs: two tcgen05.ld (32 columns each) -> bf16 -> a
       // SWIZZLE_128B smem box [32 rows][64 cols] (conflict-free: 16-byte
       // chunk j of row r sits at j ^ (r & 7)) -> one TMA store per warp per
-      // slab, double-buffered so the next slab's TMEM reads overlap the store.
+      // slab; the next slab's TMEM reads overlap the store (two staging
+      // buffers per warp with four epilogue warps, one with eight).
       const int row0 = (mt * CG + int(prank)) * BM + 32 * q;
-      uint8_t* stg = smStage + q * (2 * 4096);
+      const int slabs = (p.dbg & 64) ? 0 : wcol / 64;
+      const int half0 = min(slabs, 4);  // slabs in TMEM columns [0, 256)
+      const int c_begin = !epi8 ? 0 : set == 0 ? 0 : half0;
+      const int c_end = !epi8 ? slabs : set == 0 ? half0 : slabs;
 #pragma unroll 1
-      for (int cc = 0; cc < ((p.dbg & 64) ? 0 : wcol / 64); ++cc) {
+      for (int cc = c_begin; cc < c_end; ++cc) {
         uint32_t r0[32], r1[32];
         const uint32_t tcol = uint32_t(acc * NH * 256 + 64 * cc);
         tmem_ld_32x32b_x32(tmem_base + (uint32_t(32 * q) << 16) + tcol, r0);
         tmem_ld_32x32b_x32(tmem_base + (uint32_t(32 * q) << 16) + tcol + 32, r1);
         tmem_ld_wait();
-        uint8_t* buf = stg + (cc & 1) * 4096;
-        if (cc >= 2 && lane == 0) bulk_wait_read<1>();
+        uint8_t* buf = epi8 ? smStage + e * 4096 : smStage + (e * 2 + (nst & 1)) * 4096;
+        if (lane == 0) {
+          if (epi8) bulk_wait_read<0>();
+          else if (nst >= 2) bulk_wait_read<1>();
+        }
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -443,12 +498,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tma_store_2d(&tmC, buf, col0 + 64 * cc, row0);
           bulk_commit();
         }
+        ++nst;
+        if (NH == 2 && !epi8 && cc + 1 == half0) {
+          tc_fence_before();
+          __syncwarp();
+          arrive(0);  // half 0 drained: the next tile's half-0 MMAs may start
+        }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        if (CG == 2) mbar_arrive_cluster(tempty_leader0 + uint32_t(acc) * 8);
-        else mbar_arrive(&tempty[acc]);
+      if (NH == 2) {
+        if (epi8) arrive(set);
+        else {
+          if (half0 == 0) arrive(0);
+          arrive(1);
+        }
+      } else {
+        arrive(acc);
       }
       if (++acc == K_::ACC_BUFS) {
         acc = 0;
