@@ -82,8 +82,8 @@ struct FdParams {
   DevErr* err;
   int board;
   float* ws;                  // [nlocal][G][S][gs][d+4] split partials [m l - - o[d]]
-  uint64_t* done;             // [nlocal][G] epoch-valued count of finished splits
-  uint64_t* gtick;            // [nlocal][G] epoch-valued count of split-folded heads (push)
+  uint64_t* done;             // [nlocal][G] finished splits this launch (reset by the last CTA)
+  uint64_t* gtick;            // [nlocal][G] split-folded sub-items this launch (reset by the last CTA)
   unsigned long long* claim;  // [nlocal][G] epoch-valued cross-rank fold claims
   unsigned int* ctr;          // [0] compute, [1] fold, [2] done
   unsigned int* sfc;          // [nlocal] split-fold sub-item counters
@@ -849,12 +849,17 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
         // Intra-rank completion counter: a local spin, not a fabric signal
         // (not counted as a signal wait in the tax meter).
         const uint64_t* c = P.done + size_t(lr) * G + g;
-        const uint64_t want = P.epoch * uint64_t(P.S);
+        const uint64_t want = uint64_t(P.S);
         const uint64_t t0 = globaltimer_ns();
         int ok = 1;
         for (unsigned polls = 0; ld_acquire_gpu(c) < want; ++polls) {
           if ((polls & 255u) == 255u) {
-            if (err_raised(P.err) || globaltimer_ns() - t0 > P.watchdog_ns) {
+            if (err_raised(P.err)) {
+              ok = 0;
+              break;
+            }
+            if (globaltimer_ns() - t0 > P.watchdog_ns) {  // never silent: a DeadlockError
+              raise_err(P.err, TF_ERR_DEADLOCK, kWaitSignal, P.r[lr].rank, -1, g, 0, want, ld_acquire_gpu(c), 0);
               ok = 0;
               break;
             }
@@ -881,7 +886,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
           else __threadfence_system();
         }
         s_last = atom_add_acq_rel_gpu(reinterpret_cast<unsigned long long*>(P.gtick + size_t(lr) * G + g), 1ull) ==
-                 P.epoch * uint64_t(nhc) - 1;
+                 uint64_t(nhc) - 1;
       }
       __syncthreads();
       if (!P.push || !s_last) continue;
@@ -931,17 +936,30 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
     }
   }
   stamp(6);
-  // Last CTA out resets the work counters for the next launch.
+  // Last CTA out resets the work counters and the per-launch completion
+  // counts (done / gtick) for the next launch.  Plain per-launch counts,
+  // not epoch-valued: the fused schedule keeps every local rank's counts in
+  // one launch's buffer while the other schedules launch per rank, so an
+  // epoch-valued count would fall behind when schedules are mixed.
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(&P.ctr[2], 1u) == gridDim.x - 1) {
+    s_last = atomicAdd(&P.ctr[2], 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    const int n = P.nlocal * G;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      P.done[i] = 0;
+      P.gtick[i] = 0;
+    }
+    if (threadIdx.x == 0) {
       P.ctr[0] = 0;
       P.ctr[1] = 0;
       P.ctr[2] = 0;
       for (int i = 0; i < P.nlocal; ++i) P.sfc[i] = 0;
-      __threadfence();
     }
+    __threadfence();
   }
 }
 
