@@ -123,14 +123,32 @@ class Ctx:
         if self.ws != n_gpus and self.ws > 1:
             raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={self.ws}")
         self.W = max(self.ws, 1)
+        # TFB_BENCH_SHARED_GPU=1: every rank on GPU 0 with gloo plumbing -- a
+        # test mode that exercises the multi-process (IPC) paths on a one-GPU
+        # box; its numbers are not scaling numbers.
+        self.shared = os.environ.get("TFB_BENCH_SHARED_GPU") == "1" and self.ws > 1
+        if self.shared:
+            self.local = 0
         torch.cuda.set_device(self.local)
         self.dev = torch.device("cuda", self.local)
         self.pg = None
         if self.ws > 1:
             import torch.distributed as dist
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group("nccl", device_id=self.dev)
+            if self.shared:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=self.dev)
             self.dist = dist
+
+    def all_gather(self, out, inp):
+        """all_gather_into_tensor (NCCL); through host memory in shared-GPU test mode."""
+        if not self.shared:
+            self.dist.all_gather_into_tensor(out, inp)
+            return
+        parts = [self.torch.empty_like(inp, device="cpu") for _ in range(self.ws)]
+        self.dist.all_gather(parts, inp.cpu())
+        out.copy_(self.torch.stack(parts).view_as(out))
 
     def barrier(self):
         if self.ws > 1:
@@ -140,7 +158,7 @@ class Ctx:
         if self.ws == 1:
             return x
         from paper_2511_02168_b200.dist import max_over_ranks
-        return max_over_ranks(self.dist, x, self.dev)
+        return max_over_ranks(self.dist, x, None if self.shared else self.dev)
 
     def world(self, heap_bytes):
         import paper_2511_02168_b200 as tf
@@ -248,7 +266,7 @@ def bench_bsp_ag(ctx, A_local, B, steps, warmup):
 
     def step():
         if W > 1:
-            ctx.dist.all_gather_into_tensor(gathered, A_local)
+            ctx.all_gather(gathered, A_local)
             A = gathered.permute(1, 0, 2).reshape(M, W * kw)  # relayout [W][M][kw] -> M x K
         else:
             A = A_local
@@ -302,7 +320,7 @@ def bench_msweep(ctx, steps, warmup, Ms=(128, 256, 512, 1024, 2048, 4096, 8192, 
         w.memcpy(shard_ptrs[ctx.rank], A.data_ptr(), A.numel() * 2)
         B = (torch.rand(K, N, device=ctx.dev, generator=g) * 2 - 1).bfloat16()
         Cm = torch.empty(Mmax, N, device=ctx.dev, dtype=torch.bfloat16)
-        gathered = torch.empty(W, Mmax, kw, device=ctx.dev, dtype=torch.bfloat16)
+        gathered_flat = torch.empty(W * Mmax * kw, device=ctx.dev, dtype=torch.bfloat16)
         torch.cuda.synchronize()
         for M in Ms:
             shape = _abi.AgShape(M, N, K, 0, 0, 0, _abi.TF_BF16)
@@ -319,8 +337,9 @@ def bench_msweep(ctx, steps, warmup, Ms=(128, 256, 512, 1024, 2048, 4096, 8192, 
 
             def bsp():
                 if W > 1:
-                    ctx.dist.all_gather_into_tensor(gathered[:, :M], Am)
-                    a = gathered[:, :M].permute(1, 0, 2).reshape(M, K)
+                    gathered = gathered_flat[: W * M * kw].view(W, M, kw)  # contiguous for NCCL
+                    ctx.all_gather(gathered, Am)
+                    a = gathered.permute(1, 0, 2).reshape(M, K)
                 else:
                     a = Am
                 torch.matmul(a, B, out=Cm[:M])

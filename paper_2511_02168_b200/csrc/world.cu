@@ -66,16 +66,12 @@ tf_status heap_get(World* w, const std::string& name, size_t bytes, size_t* offs
     return set_error(TF_ERR_CONFIG, "alloc_symmetric(\"" + name + "\"): symmetric heap exhausted (" +
                                         std::to_string(off + bytes) + " > " +
                                         std::to_string(w->heap_bytes) + " bytes per rank)");
-  // Zero-fill every local region (fabric.hpp:142-144); remote ranks zero
-  // their own copy in their own process.
-  for (int r = 0; r < w->W; ++r) {
-    if (!w->ranks[r].local) continue;
-    TFB_CUDA(cudaSetDevice(w->ranks[r].device));
-    TFB_CUDA(cudaMemset(w->ranks[r].heap + off, 0, bytes));
-    // The world's streams are non-blocking: they do not order against the
-    // legacy-stream memset, so finish it before any kernel can read the zeros.
-    TFB_CUDA(cudaDeviceSynchronize());
-  }
+  // Zero-filled by construction (fabric.hpp:142-144): the heap is zeroed
+  // (and synchronized) when the world is created or reset, and bump
+  // allocations never reuse memory.  No memset here: in a multi-process
+  // world a peer that allocated its copy first may already be storing into
+  // this rank's new region (pushes, flags), and a late zero-fill would wipe
+  // those stores (a lost flag = a deadlock; found with two processes).
   w->heap_used = off + bytes;
   w->heap[name] = HeapEntry{off, bytes};
   *offset = off;
@@ -418,6 +414,7 @@ tf_status tf_world_create(int world_size, const int* devices, size_t heap_bytes_
     cudaError_t e = cudaSetDevice(rr.device);
     if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&rr.heap), w->heap_bytes);
     if (e == cudaSuccess) e = cudaMemset(rr.heap, 0, w->heap_bytes);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();  // zeros land before any peer can map the heap
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&rr.stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&rr.side, cudaStreamNonBlocking);
     if (e != cudaSuccess) return fail(cuda_status(e, "rank heap/stream setup"));
@@ -458,6 +455,7 @@ tf_status tf_world_create_ipc(int rank, int world_size, int device, size_t heap_
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&rr.heap), w->heap_bytes);
   if (e == cudaSuccess) e = cudaMemset(rr.heap, 0, w->heap_bytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();  // zeros land before the handle is exported
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&rr.stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&rr.side, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
