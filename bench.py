@@ -524,13 +524,16 @@ def main():
         "metric": METRIC, "value": us, "unit": "us", "n_gpus": W, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ag_res["ms"], "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": ag_config(W),
+        "config": dict(ag_config(W), **({"test_mode": "TFB_BENCH_SHARED_GPU: all ranks time-slice one GPU"}
+                                         if ctx.shared else {})),
         "roofline": {"bound": "tensor", "achieved": tflops, "peak": pk["bf16"], "unit": "TFLOP/s",
                      "frac": tflops / pk["bf16"], "peak_source": pk["src"] + " burst (MEASURED_PEAKS.json)",
                      "frac_vs_sustained": tflops / pk["bf16_sus"],
                      "algorithmic_flop_per_launch": flops,
                      "traffic": ncu_traffic("ag_gemm_sm100_kernel")},
-        "bsp": {"what": "cuBLAS matmul" + (" after NCCL all_gather_into_tensor + relayout" if W > 1 else
+        "bsp": {"what": "cuBLAS matmul" + ((" after gloo all_gather through host memory + relayout (shared-GPU "
+                                            "test mode: not a baseline)" if ctx.shared else
+                                            " after NCCL all_gather_into_tensor + relayout") if W > 1 else
                                            " (W=1: nothing to gather)"),
                 "value": ag_res["bsp_ms"] * 1e3, "unit": "us",
                 "fused_speedup": ag_res["bsp_ms"] / ag_res["ms"]},
