@@ -423,6 +423,7 @@ struct FastSmem {
   float o[kFastWarps][8 * 128];
   uint4 q[8 * 16];  // the group's 8 q heads x 128 d (bf16), fragment-ordered reads
   int bad;
+  unsigned long long wend[kFastWarps];  // TFB_TRACE: per-warp finish times
 };
 
 template <bool HILO>
@@ -444,8 +445,18 @@ __device__ void fast_split(const FdParams& P, int lr, int g, int sp, float* wsro
   trace_at(P, 12);
   fast_warp_range<HILO>(P, K, V, reinterpret_cast<const __nv_bfloat16*>(sm.q), wb, we, sm.m[warp], sm.l[warp],
                   sm.o[warp], &sm.bad);
+  if (P.trace && (threadIdx.x & 31) == 0) sm.wend[warp] = globaltimer_ns();
   __syncthreads();
   trace_at(P, 13);
+  if (P.trace && threadIdx.x == 0) {  // first / last warp of the CTA to finish streaming
+    unsigned long long lo = ~0ull, hi = 0;
+    for (int w = 0; w < kFastWarps; ++w) {
+      lo = min(lo, sm.wend[w]);
+      hi = max(hi, sm.wend[w]);
+    }
+    P.trace[size_t(blockIdx.x) * 16 + 10] = lo;
+    P.trace[size_t(blockIdx.x) * 16 + 11] = hi;
+  }
   if (sm.bad) {
     if (threadIdx.x == 0)
       raise_err(P.err, TF_ERR_NUMERIC, kNumeric, R.rank, -1, 0, 0, 0, 0,

@@ -23,7 +23,7 @@ with tf.World(1, [0], 512 << 20) as w:
     t = t[t[:, 0] > 0]
     t0 = t[:, 0].min()
     names = ["entry", "computed", "split-published", "flags+early-fold", "fold-phase", "fold-item", "exit",
-             "flags-released", "split-folded", "split-fold-start", "-", "-", "q-in-smem",
+             "flags-released", "split-folded", "split-fold-start", "first-warp-done", "last-warp-done", "q-in-smem",
              "warps-done"]
     for i, n in enumerate(names):
         col = t[:, i]
@@ -53,3 +53,5 @@ with tf.World(1, [0], 512 << 20) as w:
     for lo, hi in ((0, 12), (12, 25), (25, 37)):
         sel = (split >= lo) & (split < hi)
         print("  splits %d-%d: mean %.1f" % (lo, hi - 1, dur[sel].mean()))
+    spread = (t[:, 11] - t[:, 10]) / 1e3
+    print("intra-CTA warp finish spread us: min %.1f p50 %.1f max %.1f" % (spread.min(), np.median(spread), spread.max()))
