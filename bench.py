@@ -375,7 +375,10 @@ def bench_fd(ctx, cfg, steps, warmup):
         ctx.barrier()
         shape = _abi.FdShape(B, Hq, Hkv, d, L, float(d ** -0.5), _abi.TF_BF16, _abi.TF_BF16)
         res = {}
-        for name, var in (("fused", _abi.TF_FD_FUSED), ("bsp", _abi.TF_FD_BSP)):
+        variants = [("fused", _abi.TF_FD_FUSED), ("bsp", _abi.TF_FD_BSP)]
+        if W > 1:  # owner-combine: 1/(W-1) of the all-gather's fabric bytes
+            variants.append(("owner", _abi.TF_FD_FUSED_OWNER))
+        for name, var in variants:
             args = (w.handle, var, C.byref(shape), _abi.ptr_array(ptrs_for(ctx, q.data_ptr())),
                     _abi.ptr_array(ptrs_for(ctx, k.data_ptr())), _abi.ptr_array(ptrs_for(ctx, v.data_ptr())),
                     _abi.ptr_array(ptrs_for(ctx, out.data_ptr())), None, None)
@@ -394,8 +397,8 @@ def bench_fd(ctx, cfg, steps, warmup):
             ref = torch.einsum("hgl,hld->hgd", torch.softmax(s, -1), v[bb].float()).reshape(Hq, d)
             err = float(((out[bb].float() - ref).abs().amax(-1) / ref.abs().amax(-1)).max().item())
         kv_bytes = 2 * B * Hkv * ln * d * 2
-        return dict(fused_ms=res["fused"], bsp_ms=res["bsp"], kv_bytes=kv_bytes, err=err,
-                    clocks=res["fused_clocks"])
+        return dict(fused_ms=res["fused"], bsp_ms=res["bsp"], owner_ms=res.get("owner"), kv_bytes=kv_bytes,
+                    err=err, clocks=res["fused_clocks"])
     finally:
         w.close()
 
@@ -557,6 +560,8 @@ def main():
                          "roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm"], "unit": "GB/s",
                                       "frac": gbs / pk["hbm"], "algorithmic_bytes_per_launch": r["kv_bytes"]},
                          "head_rel_err_vs_torch_fp32": r["err"], "config": cfg, "clocks": r["clocks"]}
+            if r.get("owner_ms"):
+                sec[name]["owner_combine_us"] = r["owner_ms"] * 1e3
         line["secondary"] = sec
     if sweep:
         line.setdefault("secondary", {})["ag_msweep_K8192_N8192"] = {

@@ -58,7 +58,15 @@ typedef enum {
   TF_FD_FUSED = 3,
   /* run_fused with FdOptions::fold_by_arrival (flash_decode.hpp:108-114,
    * 377-408): fold whichever source landed first; not bitwise reproducible. */
-  TF_FD_FUSED_BY_ARRIVAL = 4
+  TF_FD_FUSED_BY_ARRIVAL = 4,
+  /* Extension (not in the reference): fused, owner-combine.
+   * Group g = (b, kv_head) is folded by rank g % W only: every rank pushes
+   * its partial rows of g to that owner, the owner folds them in ascending
+   * source order (bitwise the other schedules' result), finalizes, and
+   * pushes the finished rows to every other rank -- (W-1)/W x (rows of
+   * partials + rows of outputs) on the fabric instead of (W-1) x partial
+   * rows.  One launch, no barriers; W = 1 is TF_FD_FUSED. */
+  TF_FD_FUSED_OWNER = 5
 } tf_fd_variant;
 
 typedef enum { TF_F32 = 0, TF_BF16 = 1 } tf_dtype;

@@ -345,6 +345,7 @@ inline DecodeProblem make_problem(std::uint64_t seed, int heads, int head_dim, s
 
 struct FdOptions {  // :108-114
   bool fold_by_arrival = false;  // fused only: fold in arrival order (not bitwise reproducible)
+  bool owner_combine = false;    // extension: fused with per-group owners (TF_FD_FUSED_OWNER)
 };
 
 struct FdRun {  // :116-123
@@ -357,6 +358,11 @@ struct FdRun {  // :116-123
 
 inline FdRun run_fd(const DecodeProblem& p, Variant variant, const WorldConfig& cfg,
                     const FdOptions& opts = {}) {
+  if (opts.owner_combine) {
+    if (variant != Variant::kFused || opts.fold_by_arrival)
+      throw ConfigError("owner_combine applies to the fused schedule (ascending fold) only");
+    variant = static_cast<Variant>(TF_FD_FUSED_OWNER);
+  }
   if (opts.fold_by_arrival) {
     if (variant != Variant::kFused) throw ConfigError("fold_by_arrival applies to the fused schedule only");
     variant = static_cast<Variant>(TF_FD_FUSED_BY_ARRIVAL);

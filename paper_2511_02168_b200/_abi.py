@@ -58,6 +58,7 @@ _STATUS = {1: ConfigError, 2: BoundsError, 3: ShapeError, 4: DeadlockError, 5: W
 
 TF_AG_BASELINE, TF_AG_PULL, TF_AG_PUSH = 0, 1, 2
 TF_FD_BSP, TF_FD_INDEPENDENT_AG, TF_FD_FINE_WAITS, TF_FD_FUSED, TF_FD_FUSED_BY_ARRIVAL = 0, 1, 2, 3, 4
+TF_FD_FUSED_OWNER = 5
 TF_F32, TF_BF16 = 0, 1
 TF_OK, TF_ERR_CONFIG, TF_ERR_BOUNDS, TF_ERR_SHAPE, TF_ERR_DEADLOCK, TF_ERR_WORLD = 0, 1, 2, 3, 4, 5
 TF_ERR_EMPTY_ATTENTION, TF_ERR_NUMERIC, TF_ERR_CUDA = 6, 7, 8

@@ -93,6 +93,10 @@ struct FdParams {
   int fold_inline;            // fused: fold after compute
   int direct;                 // fused, W = 1: the final split fold also finalizes out
   int by_arrival;             // fused: FdOptions::fold_by_arrival
+  int owner;                  // fused, owner-combine: group g is folded by rank g % W only
+  uint64_t oflag_epoch;       // owner-combine: epoch of the final-row flag board
+  float* outbox_all[64];      // owner-combine: every rank's [B][Hq][d] fp32 final rows (this parity)
+  uint64_t* oflags_all[64];   // owner-combine: every rank's [G] final-row flags
   unsigned long long* trace;  // TFB_TRACE: [grid][16] %globaltimer stamps per CTA (else null)
   float* inbox_all[64];       // every rank's inbox (this parity), this process' view
   uint64_t* flags_all[64];    // every rank's flag board
@@ -566,9 +570,47 @@ __device__ __noinline__ bool fold_group(const FdParams& P, int lr, int g, int& s
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int e = lane + 32 * i;
-      if (e < d) store_out(R.out, ooff + e, ao[j][i] / al[j], P.out_bf16);
+      if (e < d) {
+        const float y = ao[j][i] / al[j];
+        store_out(R.out, ooff + e, y, P.out_bf16);
+        if (P.owner)  // owner-combine: the finalized row to every other rank
+          for (int dst = 0; dst < P.W; ++dst)
+            if (dst != R.rank) P.outbox_all[dst][ooff + e] = y;
+      }
     }
   }
+  if (P.owner) {
+    __syncthreads();
+    if (threadIdx.x < P.W && int(threadIdx.x) != R.rank) {
+      uint64_t* f = P.oflags_all[threadIdx.x] + g;
+      if ((P.local_dst >> threadIdx.x) & 1ull) {
+        __threadfence();
+        red_release_gpu(f, 1);
+      } else {
+        fence_sys();
+        red_release_sys(f, 1);
+      }
+    }
+  }
+  return true;
+}
+
+// Owner-combine, the receiving side: wait for group g's final rows from its
+// owner, then copy them from the outbox into out (dtype of out).
+__device__ __noinline__ bool take_group(const FdParams& P, int lr, int g) {
+  const FdRank& R = P.r[lr];
+  const int b = g / P.Hkv, kvh = g % P.Hkv, d = P.d, owner = g % P.W;
+  __shared__ int s_ok;
+  if (threadIdx.x == 0)
+    s_ok = wait_geq(P.oflags_all[R.rank] + g, P.oflag_epoch, P.watchdog_ns, P.err, kWaitSignal, R.rank,
+                    P.board, owner, g, 0);
+  __syncthreads();
+  const int ok = s_ok;
+  __syncthreads();
+  if (!ok) return false;
+  const size_t base = (size_t(b) * P.Hq + kvh * P.gs) * d;
+  const float* src = P.outbox_all[R.rank] + base;
+  for (int e = threadIdx.x; e < P.gs * d; e += blockDim.x) store_out(R.out, base + e, __ldcg(src + e), P.out_bf16);
   return true;
 }
 
@@ -647,6 +689,7 @@ __device__ __forceinline__ void fold_heads(const FdParams& P, int lr, int g, int
     const int hq = kvh * gs + h;
     if (push) {
       for (int dst = 0; dst < W; ++dst) {
+        if (P.owner && dst != g % W) continue;  // owner-combine: the group's owner only
         float* r = P.inbox_all[dst] + base_src + off;
         if (lane == 0) {
           r[0] = M;
@@ -902,7 +945,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
       __syncthreads();
       if (!P.push || !s_last) continue;
       stamp(7);
-      if (threadIdx.x < P.W) {
+      if (threadIdx.x < P.W && (!P.owner || int(threadIdx.x) == g % P.W)) {
         uint64_t* f = P.flags_all[threadIdx.x] + size_t(R.rank) * G + g;
         if ((P.local_dst >> threadIdx.x) & 1ull) red_release_gpu(f, 1);
         else red_release_sys(f, 1);
@@ -911,9 +954,10 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
       if (P.fold_inline && !P.direct) {
         // Early fold: when every source of this group has already landed
         // (the last rank to push) fold it here instead of handing it to the
-        // fold phase.  Non-blocking check.
+        // fold phase.  Non-blocking check.  Owner-combine: owners only.
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == 0) s_src = 0;
+        if (threadIdx.x == 0 && (!P.owner || g % P.W == R.rank)) {
           bool all = true;
           for (int i = 0; i < P.W && all; ++i) all = ld_acquire_sys(R.flags + size_t(i) * G + g) >= P.flag_epoch;
           s_src = all && atomicMax(&P.claim[size_t(lr) * G + g], (unsigned long long)P.epoch) < P.epoch;
@@ -942,8 +986,25 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
       __syncthreads();
       if (item >= nfold) break;
       if (!mine) continue;  // folded early by its group's last CTA
+      if (P.owner && int(item % G) % P.W != P.r[item / G].rank) continue;  // another rank's group
       stamp(5);
       if (!fold_group(P, item / G, item % G, s_src)) break;
+    }
+    if (P.owner) {
+      // Owner-combine, last phase: collect the groups other ranks own.  Every
+      // fold item was claimed before any CTA gets here, by CTAs whose waits
+      // depend only on pushes that never wait -- these waits complete.
+      for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_item = atomicAdd(&P.ctr[3], 1u);
+        __syncthreads();
+        const unsigned item = s_item;
+        __syncthreads();
+        if (item >= nfold) break;
+        const int lr = item / G, g = item % G;
+        if (g % P.W == P.r[lr].rank) continue;
+        if (!take_group(P, lr, g)) break;
+      }
     }
   }
   stamp(6);
@@ -968,6 +1029,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
       P.ctr[0] = 0;
       P.ctr[1] = 0;
       P.ctr[2] = 0;
+      P.ctr[3] = 0;
       for (int i = 0; i < P.nlocal; ++i) P.sfc[i] = 0;
     }
     __threadfence();
@@ -1107,7 +1169,7 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   if (!tw) return set_error(TF_ERR_CONFIG, "tf_flash_decode: NULL world");
   World* w = &tw->impl;
   TFB_CHECK(fd_validate(w, shape, q, k_shard, v_shard, out));
-  if (variant < TF_FD_BSP || variant > TF_FD_FUSED_BY_ARRIVAL)
+  if (variant < TF_FD_BSP || variant > TF_FD_FUSED_OWNER)
     return set_error(TF_ERR_CONFIG, "run_fd: unknown variant");
   const tf_fd_shape& sh = *shape;
   auto st = resolve_streams(w, streams);
@@ -1121,23 +1183,38 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
 
   // Boards: per (src, group) for fused, per src otherwise (fd.flags is
   // W x 1 in the reference, flash_decode.hpp:357).
-  const bool fused = variant == TF_FD_FUSED || variant == TF_FD_FUSED_BY_ARRIVAL;
+  const bool fused = variant == TF_FD_FUSED || variant == TF_FD_FUSED_BY_ARRIVAL || variant == TF_FD_FUSED_OWNER;
+  const bool owner = variant == TF_FD_FUSED_OWNER && W > 1;
   BoardEntry fb;
   // Only schedules that signal advance the board's epoch: every rank (every
   // process, in an IPC world) must agree on "run e waits for >= e".
   if (variant == TF_FD_BSP) {
     TFB_CHECK(board_get(w, "fd.flags[" + std::to_string(W) + "x1]", W, 1, &fb));
     fb.epoch = w->boards["fd.flags[" + std::to_string(W) + "x1]"].epoch;
+  } else if (owner) {
+    // Owner-combine keeps its own boards and inbox: only the owner's cells
+    // advance, so sharing them with the all-gather schedules would leave
+    // their epochs behind.
+    TFB_CHECK(board_next_epoch(w, "fd.flags.owner", W, G, &fb));
   } else {
     TFB_CHECK(board_next_epoch(w, "fd.flags", W, fused ? G : 1, &fb));
     w->fd_flags = FlagSnapshot{w->board_names[fb.id], size_t(W) * (fused ? G : 1), fb.epoch};
+  }
+  BoardEntry ob{};
+  size_t outbox_off = 0;
+  const size_t out_floats = size_t(sh.batch) * sh.q_heads * d;
+  if (owner) {
+    TFB_CHECK(board_next_epoch(w, "fd.oflags", 1, G, &ob));
+    TFB_CHECK(heap_get(w, "fd.outbox[" + std::to_string(out_floats) + "]", sizeof(float) * out_floats * 2,
+                       &outbox_off));
   }
   // Inbox / pubs / stage in the symmetric heap.  The internal inbox is
   // double-buffered by epoch parity: a fast peer's next push can never land
   // in the buffer a slow rank is still folding.
   size_t inbox_off = 0, pub_off = 0, ws_off = 0, tick_off = 0, ctr_off = 0;
   const std::string geo = "[" + std::to_string(row_floats) + "]";
-  TFB_CHECK(heap_get(w, "fd.inbox" + geo, sizeof(float) * W * row_floats * 2, &inbox_off));
+  TFB_CHECK(heap_get(w, (owner ? "fd.inbox.owner" : "fd.inbox") + geo, sizeof(float) * W * row_floats * 2,
+                     &inbox_off));
   TFB_CHECK(heap_get(w, "fd.partials" + geo, sizeof(float) * row_floats, &pub_off));
   const int nlocal_max = std::min(w->n_local, kMaxLocal);
   const size_t ws_floats = size_t(nlocal_max) * G * S_eff * gs * ws_row(d);
@@ -1186,6 +1263,13 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
 
   P.epoch = tepoch;
   P.flag_epoch = fb.epoch;
+  if (owner) {
+    P.oflag_epoch = ob.epoch;
+    for (int r = 0; r < W; ++r) {
+      P.outbox_all[r] = reinterpret_cast<float*>(w->ptr(r, outbox_off)) + size_t(ob.epoch & 1) * out_floats;
+      P.oflags_all[r] = reinterpret_cast<uint64_t*>(w->ptr(r, ob.offset));
+    }
+  }
   // One attention launch per device (a loopback device runs all its ranks
   // in one persistent grid, so the fused waits can never starve a producer).
   // The fused schedule shares one launch per device (its waits need every
@@ -1226,6 +1310,7 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
         Q.fold_inline = fold_inline;
         Q.direct = fold_inline && W == 1;
         Q.by_arrival = variant == TF_FD_FUSED_BY_ARRIVAL;
+        Q.owner = owner;
         cudaSetDevice(kv.first);
         const unsigned items = unsigned(Q.nlocal) * G * S_eff;
         // Tensor-core split with bf16 P for bf16 output, hi/lo P when the

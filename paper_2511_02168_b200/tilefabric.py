@@ -342,6 +342,7 @@ class fd:  # namespace tilefabric::fd
     class FdOptions:
         """flash_decode.hpp:108-114"""
         fold_by_arrival: bool = False
+        owner_combine: bool = False  # extension (SURVEY f4): TF_FD_FUSED_OWNER
 
     @dataclass
     class FdRun:
@@ -367,6 +368,10 @@ class fd:  # namespace tilefabric::fd
     def run_fd(p: "fd.DecodeProblem", variant, cfg: WorldConfig, opts: Optional["fd.FdOptions"] = None,
                dtype: int = _abi.TF_F32, out_dtype: Optional[int] = None):
         """flash_decode.hpp:425-438"""
+        if opts is not None and opts.owner_combine:
+            if int(variant) != _abi.TF_FD_FUSED or opts.fold_by_arrival:
+                raise ConfigError("owner_combine applies to the fused schedule (ascending fold) only")
+            variant = _abi.TF_FD_FUSED_OWNER
         if opts is not None and opts.fold_by_arrival:
             # flash_decode.hpp:377-408: fused only; arrival order, not bitwise reproducible.
             if int(variant) != _abi.TF_FD_FUSED:

@@ -216,3 +216,39 @@ def test_fold_by_arrival_option(oracle):
             assert counts == [1] * w
     with pytest.raises(tf.ConfigError):
         tf.fd.run_bsp(p, tf.WorldConfig(world_size=2), opts=tf.fd.FdOptions(fold_by_arrival=True))
+
+
+@pytest.mark.parametrize("w", [2, 3, 4])
+def test_owner_combine_matches_all_gather_bitwise(oracle, w):
+    """TF_FD_FUSED_OWNER: group g folded by rank g % W, final
+    rows pushed to every rank.  Same fold, same bits as the all-gather
+    schedules; groups a rank does not own arrive from their owner; ranks
+    that own nothing (W > groups) still end with the full output.
+    Interleaved with the other schedules in one world, so the boards'
+    epochs must stay consistent."""
+    p = tf.fd.make_problem(9, 2, 8, 96)  # 2 groups (MHA): at W = 3, 4 some ranks own none
+    want = oracle.attention(p.q[0], p.k[0], p.v[0], p.scale)
+    cfg = tf.WorldConfig(world_size=w)
+    fused = tf.fd.run_fd(p, V.kFused, cfg)
+    owner = tf.fd.run_fd(p, 5, cfg)
+    bsp = tf.fd.run_fd(p, V.kBsp, cfg)
+    for out in owner.out + bsp.out:
+        assert np.array_equal(out.view(np.uint32), fused.out[0].view(np.uint32))
+    assert oracle.head_rel_err(owner.out[0], want) <= 1e-5
+    assert owner.launches == 1
+
+
+def test_owner_combine_gqa_bf16_eight_ranks(oracle):
+    import torch  # noqa: F401
+    p = tf.fd.make_problem(21, 64, 128, 2048)
+    p.kv_heads = 8
+    p.batch = 1
+    p.q, _ = oracle.round_bf16(p.q)
+    p.k, _ = oracle.round_bf16(p.k[:, :8])
+    p.v, _ = oracle.round_bf16(p.v[:, :8])
+    cfg = tf.WorldConfig(world_size=8)
+    a = tf.fd.run_fd(p, V.kFused, cfg, dtype=1, out_dtype=0)
+    b = tf.fd.run_fd(p, 5, cfg, dtype=1, out_dtype=0)
+    c = tf.fd.run_fd(p, 5, cfg, dtype=1, out_dtype=0)  # back to back: epochs / parity
+    for out in b.out + c.out:
+        assert np.array_equal(out.view(np.uint32), a.out[0].view(np.uint32))

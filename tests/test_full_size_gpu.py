@@ -138,9 +138,12 @@ def test_fd_config3(W):
             assert _head_err(outs[0], ref) <= tol, out_dtype
             for o in outs[1:]:
                 assert torch.equal(o, outs[0])
-            # the BSP schedule folds the same partial bits
+            # the BSP and owner-combine schedules fold the same partial bits
             bsp = _run_fd(w, W, _abi.TF_FD_BSP, q, ks, vs, scale, out_dtype)
             assert torch.equal(bsp[0], outs[0])
+            own = _run_fd(w, W, _abi.TF_FD_FUSED_OWNER, q, ks, vs, scale, out_dtype)
+            for o in own:
+                assert torch.equal(o, outs[0])
         if W > 1:
             cnt = C.c_size_t()
             _abi.check(w.lib.tf_fd_flag_counts(w.handle, 0, None, 0, C.byref(cnt)))

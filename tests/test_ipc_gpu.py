@@ -114,7 +114,7 @@ def _worker(rank, world, port, q):
         fshape = _abi.FdShape(1, 2, 2, 8, 96, float(scale), _abi.TF_F32, _abi.TF_F32)
         tbl = lambda p: _abi.ptr_array(rank_pointer_table(world, rank, p))  # noqa: E731
         for variant in (_abi.TF_FD_FUSED, _abi.TF_FD_BSP, _abi.TF_FD_FINE_WAITS, _abi.TF_FD_INDEPENDENT_AG,
-                        _abi.TF_FD_FUSED):
+                        _abi.TF_FD_FUSED, _abi.TF_FD_FUSED_OWNER, _abi.TF_FD_FUSED_OWNER, _abi.TF_FD_FUSED):
             od.zero_()
             torch.cuda.synchronize()
             dist.barrier()
