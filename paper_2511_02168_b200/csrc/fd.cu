@@ -497,6 +497,96 @@ __device__ void fast_split(const FdParams& P, int lr, int g, int sp, float* wsro
   }
 }
 
+// Ascending-order fold, batched (W <= 8, not fold_by_arrival): wait for the
+// W sources in ascending order, then load every source's row of a head at
+// once and combine them in ascending order in registers -- the same
+// arithmetic as fold_group's wait-then-fold loop (bitwise), one L2 round
+// trip per head instead of W dependent ones.  EL: d / 32 rounded up.
+template <int EL>
+__device__ __noinline__ bool fold_group_batched(const FdParams& P, int lr, int g, int& s_src) {
+  const int G = P.B * P.Hkv, d = P.d, row_len = d + 2;
+  const FdRank& R = P.r[lr];
+  const int b = g / P.Hkv, kvh = g % P.Hkv;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // Ascending order, batched: wait for the W sources in ascending order,
+    // then load every source's row of a head at once and combine them in
+    // ascending order in registers -- the same arithmetic as the
+    // wait-then-fold loop below (bitwise), one L2 round trip per head
+    // instead of W dependent ones.
+    if (threadIdx.x == 0) {
+      int ok = 1;
+      for (int i = 0; i < P.W && ok; ++i)
+        ok = wait_geq(R.flags + size_t(i) * G + g, P.flag_epoch, P.watchdog_ns, P.err, kWaitSignal, R.rank,
+                      P.board, i, g, 0);
+      s_src = ok;
+    }
+    __syncthreads();
+    const int ok = s_src;
+    __syncthreads();
+    if (!ok) return false;
+    const size_t src_stride = size_t(P.B) * P.Hq * row_len;
+    for (int h = warp; h < P.gs; h += nw) {
+      const int hq = kvh * P.gs + h;
+      const float* row0 = R.inbox + (size_t(b) * P.Hq + hq) * row_len;
+      float bm[8], bl[8], bo[8][EL];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (i < P.W) {
+          const float* row = row0 + size_t(i) * src_stride;
+          bm[i] = __ldcg(row);
+          bl[i] = __ldcg(row + 1);
+#pragma unroll
+          for (int x = 0; x < EL; ++x) bo[i][x] = lane + 32 * x < d ? __ldcg(row + 2 + lane + 32 * x) : 0.0f;
+        }
+      }
+      float m = -INFINITY, l = 0.0f, o[EL];
+#pragma unroll
+      for (int x = 0; x < EL; ++x) o[x] = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (i < P.W) {
+          float nm, nl, ax = 0.f, ay = 0.f;
+          int mode;
+          combine_scalars(m, l, bm[i], bl[i], &nm, &nl, &ax, &ay, &mode);
+#pragma unroll
+          for (int x = 0; x < EL; ++x) o[x] = combine_elem(mode, o[x], bo[i][x], ax, ay);
+          m = nm;
+          l = nl;
+        }
+      }
+      if (l == 0.0f) {
+        if (lane == 0) raise_err(P.err, TF_ERR_EMPTY_ATTENTION, kEmpty, R.rank, -1, 0, 0, 0, 0, uint64_t(hq));
+        continue;
+      }
+      const size_t ooff = (size_t(b) * P.Hq + hq) * d;
+#pragma unroll
+      for (int x = 0; x < EL; ++x) {
+        const int e = lane + 32 * x;
+        if (e < d) {
+          const float y = o[x] / l;
+          store_out(R.out, ooff + e, y, P.out_bf16);
+          if (P.owner)
+            for (int dst = 0; dst < P.W; ++dst)
+              if (dst != R.rank) P.outbox_all[dst][ooff + e] = y;
+        }
+      }
+    }
+    if (P.owner) {
+      __syncthreads();
+      if (threadIdx.x < P.W && int(threadIdx.x) != R.rank) {
+        uint64_t* f = P.oflags_all[threadIdx.x] + g;
+        if ((P.local_dst >> threadIdx.x) & 1ull) {
+          __threadfence();
+          red_release_gpu(f, 1);
+        } else {
+          fence_sys();
+          red_release_sys(f, 1);
+        }
+      }
+    }
+    return true;
+  }
+
 // ---- cross-rank fold of one (local rank, group) ---------------------------
 // W inbox rows per q-head, folded in ascending source order with a
 // per-source wait right before each fold (flash_decode.hpp:409-418) or --
@@ -517,6 +607,8 @@ __device__ __noinline__ bool fold_group(const FdParams& P, int lr, int g, int& s
     for (int i = 0; i < 8; ++i) ao[j][i] = 0.0f;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (!P.by_arrival && P.W <= 8)
+    return d <= 128 ? fold_group_batched<4>(P, lr, g, s_src) : fold_group_batched<8>(P, lr, g, s_src);
   uint64_t folded = 0;
   for (int i = 0; i < P.W; ++i) {
     if (threadIdx.x == 0) {
