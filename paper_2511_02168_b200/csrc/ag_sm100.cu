@@ -44,6 +44,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <string>
 
 #include "ag_internal.hpp"
@@ -956,6 +957,14 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   return TF_OK;
 }
 
+// GEMM grid cap per rank for the push schedule: n ranks on one device share
+// its SMs with their n producers (an even number of CTAs: pairs).
+static unsigned push_cap(unsigned sms, unsigned push_ctas, unsigned n) {
+  if (n == 0) n = 1;
+  const unsigned left = sms > push_ctas * n ? sms - push_ctas * n : 2;
+  return std::max(2u, left / n / 2 * 2);
+}
+
 tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, void* const* a_shard,
                       const void* const* b, void* const* c, void* const* gathered,
                       const std::vector<cudaStream_t>& streams, const AgLayout& lay) {
@@ -1060,8 +1069,15 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
   }
 
   // PUSH: producers first on the side streams (they never wait), then the
-  // gated GEMMs with a few SMs left for the producers.
-  const unsigned push_ctas = 16;
+  // gated GEMMs with a few SMs left for the producers.  Ranks sharing a
+  // device (loopback) split its SMs: every rank's GEMM and producer CTAs
+  // must fit at once, or GEMM CTAs spinning on flags could hold every SM
+  // while a peer's producer waits for one.
+  std::map<int, unsigned> per_dev;
+  for (int r = 0; r < W; ++r)
+    if (w->ranks[r].local) ++per_dev[w->ranks[r].device];
+  // 16 producer CTAs per device, split among the ranks sharing it.
+  auto push_ctas_of = [&](int r) { return std::max(2u, 16u / per_dev[w->ranks[r].device]); };
   for (int r = 0; r < W; ++r) {
     if (!w->ranks[r].local) continue;
     cudaSetDevice(w->ranks[r].device);
@@ -1083,7 +1099,7 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
     pp.self = r;
     pp.num_m = num_m;
     pp.ctr = ctr_of(r, 1);
-    ag_push_kernel<<<push_ctas, 512, 0, w->ranks[r].side>>>(pp);
+    ag_push_kernel<<<push_ctas_of(r), 512, 0, w->ranks[r].side>>>(pp);
     TFB_CUDA(cudaGetLastError());
     ++w->launches;
   }
@@ -1092,7 +1108,7 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
     AgTcParams proto{};
     TFB_CHECK(launch_skew(w, r, streams[r]));
     TFB_CHECK(launch_gemm(w, r, sh, a_shard[r], inbox_of(r), b[r], c[r], ready_of(r), rb.epoch, r, 0,
-                          proto, streams[r], rb.id, sms > push_ctas ? sms - push_ctas : 1, lay));
+                          proto, streams[r], rb.id, push_cap(sms, push_ctas_of(r), per_dev[w->ranks[r].device]), lay));
     cudaEvent_t ev;
     TFB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     TFB_CUDA(cudaEventRecord(ev, w->ranks[r].side));
