@@ -101,3 +101,20 @@ def test_last_wave_column_slices_bitwise(oracle, monkeypatch):
     assert np.array_equal(sliced, whole)
     ref = (torch.from_numpy(p.a).double() @ torch.from_numpy(p.b).double()).float().numpy()
     assert norm_err(sliced, ref) <= TOL
+
+
+def test_push_loopback_ranks_share_the_sms(oracle):
+    """Four ranks' push schedules on one GPU with more GEMM CTAs than SMs:
+    the ranks must split the SMs (GEMM CTAs spinning on ready flags could
+    otherwise hold every SM while a peer's producer waits for one -- this
+    shape deadlocked before).  Repeated, so epochs and inbox parity turn."""
+    import torch
+    m, n, k, w = 2048, 2048, 1024, 4
+    p = bf16_problem(77, m, n, k, oracle)
+    ref = (torch.from_numpy(p.a).double() @ torch.from_numpy(p.b).double()).float().numpy()
+    for _ in range(2):
+        run = tf.ag.run_push(p, tf.WorldConfig(world_size=w), dtype=1)
+        for c in run.c:
+            assert norm_err(c, ref) <= TOL
+        for counts in run.flag_counts:
+            assert counts == [1] * len(counts)
