@@ -197,6 +197,18 @@ tf_status tf_ag_gemm_host_async(tf_world* w, tf_ag_variant variant,
                                 const void* const* b_host, void* const* c_host,
                                 void* const* streams);
 
+/* Event log (the reference's protocol-safety and overlap checks,
+ * ag_gemm_test.cpp:175-244, made on the device): while enabled, every
+ * pull/push run records per (m-block, source) chunk the %globaltimer of the
+ * chunk's store into the consumer's inbox (gather warp or push producer,
+ * just before the release) and of the consumer's first acquire of it (the
+ * TMA producer, just before the first load).  tf_ag_events copies rank's
+ * record of the last such run: num_m x W pairs {store_ns, first_load_ns}
+ * (~0 where nothing was recorded: the rank's own shard).  Debug aid --
+ * enabling it adds a device sync per run. */
+tf_status tf_world_set_events(tf_world* w, int enable);
+tf_status tf_ag_events(tf_world* w, int rank, uint64_t* out, size_t cap, size_t* count);
+
 /* Flag snapshot after the last push run (ag_gemm.hpp:296-302): per rank,
  * `count` counters normalised so that one completed run reads 1.
  * *count receives the number of cells per rank. */

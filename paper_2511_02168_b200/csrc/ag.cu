@@ -1,6 +1,7 @@
 // ag.cu -- tf_ag_gemm: validation (AgGemmProblem::validate,
 // ag_gemm.hpp:55-66; TileSpec::validate, tilemath.hpp:83-87) and dispatch to
 // the fp32 exact-order path or the bf16 tensor-core path.
+#include <algorithm>
 #include <string>
 
 #include "ag_internal.hpp"
@@ -73,5 +74,23 @@ extern "C" tf_status tf_ag_flag_counts(tf_world* tw, int rank, uint64_t* out, si
   TFB_CUDA(cudaMemcpy(v.data(), w->ptr(rank, it->second.offset), sizeof(uint64_t) * f.cells,
                       cudaMemcpyDefault));
   for (size_t i = 0; i < f.cells && i < cap; ++i) out[i] = v[i] - (f.epoch - 1);
+  return TF_OK;
+}
+
+extern "C" tf_status tf_world_set_events(tf_world* tw, int enable) {
+  if (!tw) return set_error(TF_ERR_CONFIG, "NULL world");
+  tw->impl.events = enable != 0;
+  return TF_OK;
+}
+
+extern "C" tf_status tf_ag_events(tf_world* tw, int rank, uint64_t* out, size_t cap, size_t* count) {
+  if (!tw) return set_error(TF_ERR_CONFIG, "NULL world");
+  World* w = &tw->impl;
+  if (rank < 0 || rank >= w->W) return set_error(TF_ERR_BOUNDS, "ag_events: bad rank");
+  if (count) *count = w->ag_events_n;
+  if (!out || w->ag_events_n == 0) return TF_OK;
+  const size_t n = std::min(cap, w->ag_events_n);
+  TFB_CUDA(cudaDeviceSynchronize());
+  TFB_CUDA(cudaMemcpy(out, w->ptr(rank, w->ag_events_off), n * sizeof(uint64_t), cudaMemcpyDefault));
   return TF_OK;
 }

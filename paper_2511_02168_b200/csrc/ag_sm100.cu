@@ -86,6 +86,7 @@ struct AgTcParams {
   int gather;             // gather warps active (PULL)
   __nv_bfloat16* inbox;   // local inbox, m x k
   uint64_t* ready_w;      // writable view of `ready` (gather)
+  unsigned long long* events;  // event log (tf_world_set_events): [num_m][W] x {store, first load} %globaltimer
   unsigned int* ctr;      // [0] gather chunk counter, [1] done counter
   uint64_t watchdog_ns;
   DevErr* err;
@@ -312,6 +313,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                      p.own, p.board, src, mb, 0);
             fence_proxy_async_global();
             ready_mask |= 1ull << src;
+            if (p.events)  // first consumer load of this (m-block, source) chunk
+              atomicMin(p.events + (size_t(mb) * p.W + src) * 2 + 1, (unsigned long long)globaltimer_ns());
           }
           const uint32_t bar = CG == 2 ? mapa(&full[stage], lead) : smem_u32(&full[stage]);
           if (leader) mbar_arrive_expect_tx(&full[stage], tx);
@@ -561,6 +564,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       named_bar(1, GATHER_T);
       if (gt == 0) {
         __threadfence();
+        if (p.events) p.events[(size_t(mb) * p.W + src) * 2] = globaltimer_ns();  // chunk landed
         red_release_sys(p.ready_w + size_t(mb) * p.W + src, 1);
       }
     }
@@ -671,6 +675,7 @@ struct PushParams {
   const __nv_bfloat16* shard;
   __nv_bfloat16* inbox[64];
   uint64_t* ready[64];
+  unsigned long long* events[64];  // every rank's event log (or null)
   int M, K, kw, W, self, num_m;
   unsigned int* ctr;  // [0] chunk counter, [1] done
 };
@@ -713,6 +718,7 @@ __global__ void __launch_bounds__(512) ag_push_kernel(const PushParams p) {
     __syncthreads();
     if (threadIdx.x == 0) {
       fence_sys();
+      if (p.events[dst]) p.events[dst][(size_t(mb) * p.W + p.self) * 2] = globaltimer_ns();  // chunk stored
       red_release_sys(p.ready[dst] + size_t(mb) * p.W + p.self, 1);
     }
   }
@@ -1014,6 +1020,28 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
   };
   auto ready_of = [&](int r) { return reinterpret_cast<uint64_t*>(w->ptr(r, rb.offset)); };
   auto ctr_of = [&](int r, int slot) { return reinterpret_cast<unsigned int*>(w->ptr(r, ctr_off)) + slot * 4; };
+  // Event log (tf_world_set_events; debug, untimed): per (m-block, source)
+  // the %globaltimer of the chunk's store and of its first consumer load.
+  // Filled with ~0 synchronously before anything launches: a peer's
+  // producer may record into this rank's log as soon as it runs.
+  size_t ev_off = 0;
+  const bool events = w->events && variant != TF_AG_BASELINE && !lay.inbox_complete;
+  if (events) {
+    const size_t bytes = size_t(num_m) * W * 2 * sizeof(unsigned long long);
+    TFB_CHECK(heap_get(w, "ag.events[" + std::to_string(num_m) + "x" + std::to_string(W) + "]", bytes, &ev_off));
+    for (int r = 0; r < W; ++r) {
+      if (!w->ranks[r].local) continue;
+      cudaSetDevice(w->ranks[r].device);
+      TFB_CUDA(cudaDeviceSynchronize());
+      TFB_CUDA(cudaMemset(w->ptr(r, ev_off), 0xFF, bytes));
+      TFB_CUDA(cudaDeviceSynchronize());
+    }
+    w->ag_events_off = ev_off;
+    w->ag_events_n = size_t(num_m) * W * 2;
+  }
+  auto events_of = [&](int r) -> unsigned long long* {
+    return events ? reinterpret_cast<unsigned long long*>(w->ptr(r, ev_off)) : nullptr;
+  };
   // Every schedule lands the gathered operand in HBM once per rank (PULL via
   // the gather warps; the reference's pull re-fetches tiles instead).
   if (lay.inbox_complete) {
@@ -1061,6 +1089,7 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
       proto.inbox = inbox_of(r);
       proto.ready_w = ready_of(r);
       proto.ctr = ctr_of(r, 0);
+      proto.events = events_of(r);
       TFB_CHECK(launch_skew(w, r, streams[r]));
       TFB_CHECK(launch_gemm(w, r, sh, a_shard[r], inbox_of(r), b[r], c[r], ready_of(r), rb.epoch, r,
                             1, proto, streams[r], rb.id, sms, lay));
@@ -1099,6 +1128,7 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
     pp.self = r;
     pp.num_m = num_m;
     pp.ctr = ctr_of(r, 1);
+    for (int d = 0; d < W; ++d) pp.events[d] = events_of(d);
     ag_push_kernel<<<push_ctas_of(r), 512, 0, w->ranks[r].side>>>(pp);
     TFB_CUDA(cudaGetLastError());
     ++w->launches;
@@ -1106,6 +1136,7 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
   for (int r = 0; r < W; ++r) {
     if (!w->ranks[r].local) continue;
     AgTcParams proto{};
+    proto.events = events_of(r);
     TFB_CHECK(launch_skew(w, r, streams[r]));
     TFB_CHECK(launch_gemm(w, r, sh, a_shard[r], inbox_of(r), b[r], c[r], ready_of(r), rb.epoch, r, 0,
                           proto, streams[r], rb.id, push_cap(sms, push_ctas_of(r), per_dev[w->ranks[r].device]), lay));

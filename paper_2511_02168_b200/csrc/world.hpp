@@ -84,6 +84,10 @@ struct World {
   uint64_t ag_epoch = 0;
   uint64_t fd_epoch = 0;
   FlagSnapshot ag_flags, fd_flags;
+  // Event log (tf_world_set_events): the last pull/push run's per-chunk
+  // store / first-load timestamps, [num_m][W][2] u64 in every rank's heap.
+  bool events = false;
+  size_t ag_events_off = 0, ag_events_n = 0;
   // Named monotonic epochs for counters that live in the heap (tickets,
   // soak boards); cleared with the heap.
   std::map<std::string, uint64_t> epochs;

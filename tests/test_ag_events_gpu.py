@@ -1,0 +1,62 @@
+"""GPU: the reference's protocol-safety and overlap witnesses
+(ag_gemm_test.cpp:175-244) from the device event log (tf_world_set_events /
+tf_ag_events): for every remote (m-block, source) chunk of every rank, the
+consumer's first load is stamped after the chunk's store (no inbox block is
+read before its owner's store), and in some rank a consumer loads a chunk
+before the last chunk is stored (the exchange overlaps the GEMM instead of
+completing first, as a bulk-synchronous schedule would)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_2511_02168_b200 as tf
+from paper_2511_02168_b200 import _abi
+
+pytestmark = pytest.mark.gpu
+NONE = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+@pytest.mark.parametrize("variant", [_abi.TF_AG_PULL, _abi.TF_AG_PUSH])
+def test_safety_and_overlap_witnesses(variant):
+    import torch
+    W, m, n, k = 4, 2048, 2048, 1024
+    kw = k // W
+    num_m = m // 128
+    g = torch.Generator(device="cuda").manual_seed(11)
+    A = (torch.rand(m, k, device="cuda", generator=g) * 2 - 1).bfloat16()
+    B = (torch.rand(k, n, device="cuda", generator=g) * 2 - 1).bfloat16()
+    Cs = [torch.empty(m, n, device="cuda", dtype=torch.bfloat16) for _ in range(W)]
+    with tf.World(W, [0] * W, m * kw * 2 + 2 * 2 * m * k * 2 + (64 << 20)) as w:
+        sh = w.alloc("ag.a", m * kw * 2)
+        for r in range(W):
+            s = A[:, r * kw:(r + 1) * kw].contiguous()
+            w.memcpy(sh[r], s.data_ptr(), s.numel() * 2)
+        _abi.check(w.lib.tf_world_set_events(w.handle, 1))
+        shape = _abi.AgShape(m, n, k, 0, 0, 0, _abi.TF_BF16)
+        _abi.check(w.lib.tf_ag_gemm(w.handle, variant, C.byref(shape), _abi.ptr_array(sh),
+                                    _abi.ptr_array([B.data_ptr()] * W), _abi.ptr_array([c.data_ptr() for c in Cs]),
+                                    None, None))
+        ref = A.float() @ B.float()
+        for c in Cs:
+            assert float((c.float() - ref).abs().max() / ref.abs().max()) <= 4e-3
+        stores, loads = [], []
+        for r in range(W):
+            cnt = C.c_size_t()
+            _abi.check(w.lib.tf_ag_events(w.handle, r, None, 0, C.byref(cnt)))
+            assert cnt.value == num_m * W * 2
+            buf = (C.c_uint64 * cnt.value)()
+            _abi.check(w.lib.tf_ag_events(w.handle, r, buf, cnt.value, C.byref(cnt)))
+            ev = np.frombuffer(buf, dtype=np.uint64).reshape(num_m, W, 2)
+            for mb in range(num_m):
+                for src in range(W):
+                    if src == r:
+                        continue  # the rank's own shard: no exchange
+                    st, ld = ev[mb, src]
+                    assert st != NONE and ld != NONE, (r, mb, src)
+                    assert ld >= st, (r, mb, src, int(st), int(ld))  # safety: read after the owner's store
+                    stores.append(int(st))
+                    loads.append(int(ld))
+        # overlap witness: the first consumer load precedes the last store
+        assert min(loads) < max(stores)
+        _abi.check(w.lib.tf_world_set_events(w.handle, 0))
