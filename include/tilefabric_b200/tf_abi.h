@@ -208,6 +208,10 @@ tf_status tf_ag_gemm_host_async(tf_world* w, tf_ag_variant variant,
  * enabling it adds a device sync per run. */
 tf_status tf_world_set_events(tf_world* w, int enable);
 tf_status tf_ag_events(tf_world* w, int rank, uint64_t* out, size_t cap, size_t* count);
+/* Flash Decode, fused (W > 1): per (source, group) the %globaltimer of the
+ * source's release of its rows into this rank's inbox and of this rank's
+ * fold reading them (flash_decode_test.cpp:200-247): W x G pairs. */
+tf_status tf_fd_events(tf_world* w, int rank, uint64_t* out, size_t cap, size_t* count);
 
 /* Flag snapshot after the last push run (ag_gemm.hpp:296-302): per rank,
  * `count` counters normalised so that one completed run reads 1.

@@ -96,6 +96,7 @@ struct FdParams {
   int owner;                  // fused, owner-combine: group g is folded by rank g % W only
   uint64_t oflag_epoch;       // owner-combine: epoch of the final-row flag board
   float* outbox_all[64];      // owner-combine: every rank's [B][Hq][d] fp32 final rows (this parity)
+  unsigned long long* events_all[64];  // event log (tf_world_set_events): [W src][G] x {store, first load}
   uint64_t* oflags_all[64];   // owner-combine: every rank's [G] final-row flags
   unsigned long long* trace;  // TFB_TRACE: [grid][16] %globaltimer stamps per CTA (else null)
   float* inbox_all[64];       // every rank's inbox (this parity), this process' view
@@ -515,9 +516,12 @@ __device__ __noinline__ bool fold_group_batched(const FdParams& P, int lr, int g
     // instead of W dependent ones.
     if (threadIdx.x == 0) {
       int ok = 1;
-      for (int i = 0; i < P.W && ok; ++i)
+      for (int i = 0; i < P.W && ok; ++i) {
         ok = wait_geq(R.flags + size_t(i) * G + g, P.flag_epoch, P.watchdog_ns, P.err, kWaitSignal, R.rank,
                       P.board, i, g, 0);
+        if (ok && P.events_all[R.rank])  // first (only) read of source i's rows of g
+          P.events_all[R.rank][(size_t(i) * G + g) * 2 + 1] = globaltimer_ns();
+      }
       s_src = ok;
     }
     __syncthreads();
@@ -634,6 +638,7 @@ __device__ __noinline__ bool fold_group(const FdParams& P, int lr, int g, int& s
           }
         }
       }
+      if (src >= 0 && P.events_all[R.rank]) P.events_all[R.rank][(size_t(src) * G + g) * 2 + 1] = globaltimer_ns();
       s_src = src;
     }
     __syncthreads();
@@ -1039,6 +1044,8 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
       stamp(7);
       if (threadIdx.x < P.W && (!P.owner || int(threadIdx.x) == g % P.W)) {
         uint64_t* f = P.flags_all[threadIdx.x] + size_t(R.rank) * G + g;
+        if (P.events_all[threadIdx.x])  // this source's rows of g are in dst's inbox
+          P.events_all[threadIdx.x][(size_t(R.rank) * G + g) * 2] = globaltimer_ns();
         if ((P.local_dst >> threadIdx.x) & 1ull) red_release_gpu(f, 1);
         else red_release_sys(f, 1);
       }
@@ -1355,6 +1362,22 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
 
   P.epoch = tepoch;
   P.flag_epoch = fb.epoch;
+  if (w->events && fused && !owner && W > 1) {
+    // Event log (debug, untimed): ~0-filled synchronously before any launch.
+    size_t ev_off = 0;
+    const size_t bytes = size_t(W) * G * 2 * sizeof(unsigned long long);
+    TFB_CHECK(heap_get(w, "fd.events[" + std::to_string(W) + "x" + std::to_string(G) + "]", bytes, &ev_off));
+    for (int r = 0; r < W; ++r) {
+      if (!w->ranks[r].local) continue;
+      cudaSetDevice(w->ranks[r].device);
+      TFB_CUDA(cudaDeviceSynchronize());
+      TFB_CUDA(cudaMemset(w->ptr(r, ev_off), 0xFF, bytes));
+      TFB_CUDA(cudaDeviceSynchronize());
+    }
+    for (int r = 0; r < W; ++r) P.events_all[r] = reinterpret_cast<unsigned long long*>(w->ptr(r, ev_off));
+    w->fd_events_off = ev_off;
+    w->fd_events_n = size_t(W) * G * 2;
+  }
   if (owner) {
     P.oflag_epoch = ob.epoch;
     for (int r = 0; r < W; ++r) {
@@ -1531,5 +1554,17 @@ extern "C" tf_status tf_fd_flag_counts(tf_world* tw, int rank, uint64_t* out, si
     for (size_t g = 0; g < per; ++g) mn = std::min(mn, v[size_t(s) * per + g]);
     out[s] = mn - (f.epoch - 1);
   }
+  return TF_OK;
+}
+
+extern "C" tf_status tf_fd_events(tf_world* tw, int rank, uint64_t* out, size_t cap, size_t* count) {
+  if (!tw) return set_error(TF_ERR_CONFIG, "NULL world");
+  World* w = &tw->impl;
+  if (rank < 0 || rank >= w->W) return set_error(TF_ERR_BOUNDS, "fd_events: bad rank");
+  if (count) *count = w->fd_events_n;
+  if (!out || w->fd_events_n == 0) return TF_OK;
+  const size_t n = cap < w->fd_events_n ? cap : w->fd_events_n;
+  TFB_CUDA(cudaDeviceSynchronize());
+  TFB_CUDA(cudaMemcpy(out, w->ptr(rank, w->fd_events_off), n * sizeof(uint64_t), cudaMemcpyDefault));
   return TF_OK;
 }

@@ -88,6 +88,7 @@ struct World {
   // store / first-load timestamps, [num_m][W][2] u64 in every rank's heap.
   bool events = false;
   size_t ag_events_off = 0, ag_events_n = 0;
+  size_t fd_events_off = 0, fd_events_n = 0;  // fused FD: [W src][G][2]
   // Named monotonic epochs for counters that live in the heap (tickets,
   // soak boards); cleared with the heap.
   std::map<std::string, uint64_t> epochs;

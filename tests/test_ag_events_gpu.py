@@ -60,3 +60,45 @@ def test_safety_and_overlap_witnesses(variant):
         # overlap witness: the first consumer load precedes the last store
         assert min(loads) < max(stores)
         _abi.check(w.lib.tf_world_set_events(w.handle, 0))
+
+
+def test_fd_fused_safety_and_overlap_witnesses():
+    """flash_decode_test.cpp:200-247 on the device: every (source, group) row
+    set is folded only after its source released it, and some fold starts
+    before the last push -- the exchange overlaps the attention compute."""
+    import torch
+    W, B, Hq, Hkv, d, L = 4, 16, 64, 8, 128, 8192
+    G = B * Hkv
+    g = torch.Generator(device="cuda").manual_seed(12)
+    q = (torch.rand(B, Hq, d, device="cuda", generator=g) * 2 - 1).bfloat16()
+    k = (torch.rand(B, Hkv, L, d, device="cuda", generator=g) * 2 - 1).bfloat16()
+    v = (torch.rand(B, Hkv, L, d, device="cuda", generator=g) * 2 - 1).bfloat16()
+    ln = L // W
+    ks = [k[:, :, r * ln:(r + 1) * ln].contiguous() for r in range(W)]
+    vs = [v[:, :, r * ln:(r + 1) * ln].contiguous() for r in range(W)]
+    outs = [torch.empty(B, Hq, d, device="cuda", dtype=torch.bfloat16) for _ in range(W)]
+    with tf.World(W, [0] * W, 256 << 20) as w:
+        _abi.check(w.lib.tf_world_set_events(w.handle, 1))
+        shape = _abi.FdShape(B, Hq, Hkv, d, L, d ** -0.5, _abi.TF_BF16, _abi.TF_BF16)
+        _abi.check(w.lib.tf_flash_decode(w.handle, _abi.TF_FD_FUSED, C.byref(shape), _abi.ptr_array([q.data_ptr()] * W),
+                                         _abi.ptr_array([x.data_ptr() for x in ks]),
+                                         _abi.ptr_array([x.data_ptr() for x in vs]),
+                                         _abi.ptr_array([o.data_ptr() for o in outs]), None, None))
+        for o in outs[1:]:
+            assert torch.equal(o, outs[0])
+        stores, loads = [], []
+        for r in range(W):
+            cnt = C.c_size_t()
+            _abi.check(w.lib.tf_fd_events(w.handle, r, None, 0, C.byref(cnt)))
+            assert cnt.value == W * G * 2
+            buf = (C.c_uint64 * cnt.value)()
+            _abi.check(w.lib.tf_fd_events(w.handle, r, buf, cnt.value, C.byref(cnt)))
+            ev = np.frombuffer(buf, dtype=np.uint64).reshape(W, G, 2)
+            for src in range(W):
+                for grp in range(G):
+                    st, ld = ev[src, grp]
+                    assert st != NONE and ld != NONE, (r, src, grp)
+                    assert ld >= st, (r, src, grp)
+                    stores.append(int(st))
+                    loads.append(int(ld))
+        assert min(loads) < max(stores)
