@@ -159,7 +159,9 @@ tf_status tf_signal_soak(tf_world* w, uint64_t seed, int rounds,
  * gathered_opt[r] (m x k, dtype of A) receives the gathered operand, bit for
  * bit the logical A (the reference's inbox/stage, ag_gemm.hpp:139,234); pass
  * NULL to let the world use an internal heap buffer.  streams: per-rank
- * cudaStream_t or NULL (world streams).  Arrays are indexed by global rank;
+ * cudaStream_t or NULL (world streams, ordered after the work already
+ * issued on the legacy default stream -- where callers usually produce the
+ * inputs; with explicit streams the caller owns the ordering).  Arrays are indexed by global rank;
  * entries for ranks not local to this process are ignored except a_shard,
  * whose peer entries must be the heap mappings tf_heap_alloc returned. */
 typedef struct {

@@ -967,7 +967,10 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
     // Publish the split: bar.sync orders every thread's ws stores before
     // thread 0's release (cumulative), which the split-fold acquires.
     __syncthreads();
-    if (threadIdx.x == 0) red_release_gpu(P.done + size_t(lr) * G + g, 1);
+    if (threadIdx.x == 0) {
+      __threadfence();  // every thread's ws rows (ordered by the barrier) before the count
+      red_release_gpu(P.done + size_t(lr) * G + g, 1);
+    }
   }
   stamp(2);
   // Split-fold phase: sub-items (group, hc heads) of every local rank this
@@ -1272,6 +1275,7 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
     return set_error(TF_ERR_CONFIG, "run_fd: unknown variant");
   const tf_fd_shape& sh = *shape;
   auto st = resolve_streams(w, streams);
+  TFB_CHECK(order_after_legacy(w, streams));
   const int W = w->W, d = sh.head_dim, G = sh.batch * sh.kv_heads, gs = sh.q_heads / sh.kv_heads;
   const size_t len = sh.kv_len / W;
   const size_t row_floats = size_t(sh.batch) * sh.q_heads * (d + 2);

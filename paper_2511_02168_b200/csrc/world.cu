@@ -117,6 +117,18 @@ std::vector<cudaStream_t> resolve_streams(World* w, void* const* streams) {
   return s;
 }
 
+tf_status order_after_legacy(World* w, void* const* streams) {
+  for (int r = 0; r < w->W; ++r) {
+    if (!w->ranks[r].local || (streams && streams[r])) continue;
+    RankRes& rr = w->ranks[r];
+    cudaSetDevice(rr.device);
+    if (!rr.legacy_ev) TFB_CUDA(cudaEventCreateWithFlags(&rr.legacy_ev, cudaEventDisableTiming));
+    TFB_CUDA(cudaEventRecord(rr.legacy_ev, 0));
+    TFB_CUDA(cudaStreamWaitEvent(rr.stream, rr.legacy_ev, 0));
+  }
+  return TF_OK;
+}
+
 tf_status check_record(World* w) {
   DevErr rec{};
   DevErr* dev_rec = nullptr;
@@ -516,6 +528,7 @@ tf_status tf_world_destroy(tf_world* tw) {
     if (rr.stream) cudaStreamSynchronize(rr.stream), cudaStreamDestroy(rr.stream);
     if (rr.side) cudaStreamSynchronize(rr.side), cudaStreamDestroy(rr.side);
     if (rr.h2d) cudaStreamSynchronize(rr.h2d), cudaStreamDestroy(rr.h2d);
+    if (rr.legacy_ev) cudaEventDestroy(rr.legacy_ev);
     if (rr.d2h) cudaStreamSynchronize(rr.d2h), cudaStreamDestroy(rr.d2h);
     for (void* p : rr.scratch)
       if (p) cudaFree(p);

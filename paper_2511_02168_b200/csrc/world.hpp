@@ -27,6 +27,7 @@ struct RankRes {
   // Host-buffer runs (ag_host.cu): copy-engine streams and device operand
   // buffers, created on first use, grow-only.
   cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t legacy_ev = nullptr;  // order_after_legacy
   void* scratch[2] = {nullptr, nullptr};
   size_t scratch_bytes[2] = {0, 0};
 };
@@ -145,6 +146,10 @@ tf_status board_next_epoch(World* w, const std::string& base, int rows, int slot
 tf_status world_barrier(World* w, const std::vector<cudaStream_t>& streams, int only_rank = -1);
 // Resolve caller streams (NULL -> world streams).
 std::vector<cudaStream_t> resolve_streams(World* w, void* const* streams);
+// For ranks driven on the world's own (non-blocking) streams: order them
+// after everything already issued on the legacy default stream, where a
+// caller typically produced the inputs (torch, cudaMemcpy, ...).
+tf_status order_after_legacy(World* w, void* const* streams);
 // Wait for local streams and turn the device error record into a status.
 tf_status sync_and_check(World* w, const std::vector<cudaStream_t>& streams);
 tf_status check_record(World* w);

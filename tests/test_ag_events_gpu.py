@@ -27,6 +27,7 @@ def test_safety_and_overlap_witnesses(variant):
     A = (torch.rand(m, k, device="cuda", generator=g) * 2 - 1).bfloat16()
     B = (torch.rand(k, n, device="cuda", generator=g) * 2 - 1).bfloat16()
     Cs = [torch.empty(m, n, device="cuda", dtype=torch.bfloat16) for _ in range(W)]
+    torch.cuda.synchronize()
     with tf.World(W, [0] * W, m * kw * 2 + 2 * 2 * m * k * 2 + (64 << 20)) as w:
         sh = w.alloc("ag.a", m * kw * 2)
         for r in range(W):
@@ -77,6 +78,7 @@ def test_fd_fused_safety_and_overlap_witnesses():
     ks = [k[:, :, r * ln:(r + 1) * ln].contiguous() for r in range(W)]
     vs = [v[:, :, r * ln:(r + 1) * ln].contiguous() for r in range(W)]
     outs = [torch.empty(B, Hq, d, device="cuda", dtype=torch.bfloat16) for _ in range(W)]
+    torch.cuda.synchronize()
     with tf.World(W, [0] * W, 256 << 20) as w:
         _abi.check(w.lib.tf_world_set_events(w.handle, 1))
         shape = _abi.FdShape(B, Hq, Hkv, d, L, d ** -0.5, _abi.TF_BF16, _abi.TF_BF16)

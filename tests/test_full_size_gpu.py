@@ -38,6 +38,7 @@ def test_ag_config2_single_gpu():
     A = (torch.rand(M, K, device="cuda", generator=g) * 2 - 1).bfloat16()
     B = (torch.rand(K, N_TOTAL, device="cuda", generator=g) * 2 - 1).bfloat16()
     Cout = torch.empty(M, N_TOTAL, device="cuda", dtype=torch.bfloat16)
+    torch.cuda.synchronize()
     with tf.World(1, [0], M * K * 2 + (64 << 20)) as w:
         sh = w.alloc("ag.a", M * K * 2)
         w.memcpy(sh[0], A.data_ptr(), M * K * 2)
@@ -59,6 +60,7 @@ def test_ag_config2_eight_ranks_loopback():
     rows = torch.arange(0, M, M // 32, device="cuda")
     heap = M * kw * 2 + 2 * M * K * 2 + (64 << 20)
     outs = {}
+    torch.cuda.synchronize()
     with tf.World(W, [0] * W, heap) as w:
         sh = w.alloc("ag.a", M * kw * 2)
         for r in range(W):
@@ -132,6 +134,7 @@ def test_fd_config3(W):
     ln = L // W
     ks = [k[:, :, r * ln:(r + 1) * ln].contiguous() for r in range(W)]  # slice_shard
     vs = [v[:, :, r * ln:(r + 1) * ln].contiguous() for r in range(W)]
+    torch.cuda.synchronize()
     with tf.World(W, [0] * W, 64 << 20) as w:
         for out_dtype, tol in ((_abi.TF_BF16, 8e-3), (_abi.TF_F32, 1e-4)):
             outs = _run_fd(w, W, _abi.TF_FD_FUSED, q, ks, vs, scale, out_dtype)
@@ -161,6 +164,7 @@ def test_fd_config4_single_gpu():
     v = (torch.rand(B, Hkv, L, d, device="cuda", generator=g) * 2 - 1).bfloat16()
     scale = d ** -0.5
     ref = _attention_ref(q, k, v, scale)
+    torch.cuda.synchronize()
     with tf.World(1, [0], 64 << 20) as w:
         for out_dtype, tol in ((_abi.TF_BF16, 8e-3), (_abi.TF_F32, 1e-4)):
             out = _run_fd(w, 1, _abi.TF_FD_FUSED, q, [k], [v], scale, out_dtype)[0]

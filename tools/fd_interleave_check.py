@@ -11,6 +11,7 @@ for (B, L) in cases:
         q = (torch.rand(B, Hq, d, device="cuda", generator=g) * 2 - 1).bfloat16()
         k = (torch.rand(B, Hkv, L, d, device="cuda", generator=g) * 2 - 1).bfloat16()
         v = (torch.rand(B, Hkv, L, d, device="cuda", generator=g) * 2 - 1).bfloat16()
+        torch.cuda.synchronize()  # the world's streams do not order against torch's
         res = {}
         for mode in ("int", "contig"):
             if mode == "contig": os.environ["TFB_FD_CONTIGUOUS"] = "1"
