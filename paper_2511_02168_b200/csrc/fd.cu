@@ -88,6 +88,7 @@ struct FdParams {
   unsigned int* ctr;          // [0] compute, [1] fold, [2] done
   unsigned int* sfc;          // [nlocal] split-fold sub-item counters
   int hc;                     // heads per split-fold sub-item
+  int interleave;             // fast split: the CTA's warps interleave 16-key tiles
   uint64_t local_dst;         // bit dst: dst's inbox/flags live on this launch's device
   int push;                   // push rank partials to every inbox (+ signal)
   int fold_inline;            // fused: fold after compute
@@ -287,7 +288,7 @@ __device__ __forceinline__ int fast_d(int i, int j, int r) {
 template <bool HILO>
 __device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
                                 const __nv_bfloat16* V, const __nv_bfloat16* Q, size_t kb,
-                                size_t ke, float* sm_m, float* sm_l, float* sm_o, int* bad) {
+                                size_t ke, int stride, float* sm_m, float* sm_l, float* sm_o, int* bad) {
   const int lane = threadIdx.x & 31;
   const int gq = lane >> 2, t = lane & 3;
   const float sl2 = P.scale * kLog2e;
@@ -310,7 +311,8 @@ __device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
   // (A one-tile-ahead register pipeline was measured: it spills at the
   //  128-register budget 16 warps/SM need and lost 10 %; the loads are issued
   //  at the top of each tile instead and the 16 resident warps overlap them.)
-  for (int rem = int(ke - kb) - gq; rem > -gq; rem -= 16, kp += 16 * 128, vp += 16 * 128) {
+  // 16-key tiles kb, kb + stride, ... below ke.
+  for (int rem = int(ke - kb) - gq; rem > -gq; rem -= stride, kp += size_t(stride) * 128, vp += size_t(stride) * 128) {
     const bool va = rem > 0, vb = rem > 8;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -439,8 +441,23 @@ __device__ void fast_split(const FdParams& P, int lr, int g, int sp, float* wsro
   const int b = g / P.Hkv, kvh = g % P.Hkv;
   const size_t k0 = size_t(sp) * P.split_len;
   const size_t k1 = min(P.len, k0 + P.split_len);
-  const size_t per = ((k1 - k0 + kFastWarps - 1) / kFastWarps + 15) / 16 * 16;
-  const size_t wb = min(k1, k0 + warp * per), we = min(k1, wb + per);
+  // The CTA's warps interleave tile by tile over the split (warp w: tiles
+  // w, w + 8, ...): contiguous per-warp ranges finished up to 13 us apart
+  // inside a CTA (TFB_TRACE); interleaved, the warps share the same DRAM
+  // pages and finish closer together (config 4: -1.7 %).  P.interleave = 0
+  // (TFB_FD_CONTIGUOUS) restores contiguous ranges.
+  size_t wb, we;
+  int stride;
+  if (P.interleave) {
+    wb = min(k1, k0 + size_t(warp) * 16);
+    we = k1;
+    stride = 16 * kFastWarps;
+  } else {
+    const size_t per = ((k1 - k0 + kFastWarps - 1) / kFastWarps + 15) / 16 * 16;
+    wb = min(k1, k0 + warp * per);
+    we = min(k1, wb + per);
+    stride = 16;
+  }
   const __nv_bfloat16* K = static_cast<const __nv_bfloat16*>(R.k) + (size_t(b) * P.Hkv + kvh) * P.len * 128;
   const __nv_bfloat16* V = static_cast<const __nv_bfloat16*>(R.v) + (size_t(b) * P.Hkv + kvh) * P.len * 128;
   const __nv_bfloat16* Q = static_cast<const __nv_bfloat16*>(R.q) + (size_t(b) * P.Hq + kvh * 8) * 128;
@@ -448,7 +465,7 @@ __device__ void fast_split(const FdParams& P, int lr, int g, int sp, float* wsro
   for (int i = threadIdx.x; i < 8 * 16; i += blockDim.x) sm.q[i] = reinterpret_cast<const uint4*>(Q)[i];
   __syncthreads();
   trace_at(P, 12);
-  fast_warp_range<HILO>(P, K, V, reinterpret_cast<const __nv_bfloat16*>(sm.q), wb, we, sm.m[warp], sm.l[warp],
+  fast_warp_range<HILO>(P, K, V, reinterpret_cast<const __nv_bfloat16*>(sm.q), wb, we, stride, sm.m[warp], sm.l[warp],
                   sm.o[warp], &sm.bad);
   if (P.trace && (threadIdx.x & 31) == 0) sm.wend[warp] = globaltimer_ns();
   __syncthreads();
@@ -1421,6 +1438,7 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
         Q.claim = reinterpret_cast<unsigned long long*>(Q.gtick + size_t(nlocal_max) * G);
         Q.sfc = reinterpret_cast<unsigned int*>(Q.claim + size_t(nlocal_max) * G);
         Q.hc = hc;
+        Q.interleave = !std::getenv("TFB_FD_CONTIGUOUS");
         Q.local_dst = 0;
         for (int r = 0; r < W; ++r)
           if (w->ranks[r].local && w->ranks[r].device == kv.first) Q.local_dst |= 1ull << r;
