@@ -45,7 +45,7 @@ namespace tf = tilefabric;
 namespace {
 
 const std::vector<std::string> kAgPatterns = {"ag-baseline", "ag-pull", "ag-push"};
-const std::vector<std::string> kFdPatterns = {"fd-bsp", "fd-ag", "fd-wait", "fd-fused"};
+const std::vector<std::string> kFdPatterns = {"fd-bsp", "fd-ag", "fd-wait", "fd-fused", "fd-owner"};
 constexpr const char* kAgBaseline = "ag-baseline";
 constexpr const char* kFdBaseline = "fd-bsp";
 
@@ -57,6 +57,7 @@ tf_fd_variant fd_variant(const std::string& p, bool arrival) {
   if (p == "fd-bsp") return TF_FD_BSP;
   if (p == "fd-ag") return TF_FD_INDEPENDENT_AG;
   if (p == "fd-wait") return TF_FD_FINE_WAITS;
+  if (p == "fd-owner") return TF_FD_FUSED_OWNER;  // GPU extension: owner-combine
   return arrival ? TF_FD_FUSED_BY_ARRIVAL : TF_FD_FUSED;
 }
 
@@ -185,6 +186,7 @@ const char* kUsage =
     "Options:\n"
     "  -h,--help                 Print this help message and exit\n"
     "  --pattern TEXT            One pattern: ag-baseline|ag-pull|ag-push|fd-bsp|fd-ag|fd-wait|fd-fused\n"
+    "                            (GPU extension: fd-owner, fused with owner-combine)\n"
     "  --patterns TEXT,...       Comma-separated pattern list (sweep mode); excludes --pattern\n"
     "  --preset TEXT             Named configuration: paper-ag-gemm|desk-ag-gemm|paper-fd|desk-fd\n"
     "  --world-size INT          Ranks in the world\n"

@@ -1483,7 +1483,12 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   // Every schedule lands W wire rows per rank in an inbox / stage
   // (flash_decode_test.cpp:167-196: W*W*wire*4 bytes world-wide).
   for (int r = 0; r < W; ++r)
-    if (w->ranks[r].local) w->stage(r, sizeof(float) * W * row_floats);
+    if (w->ranks[r].local) {
+      // Owner-combine lands the partial rows of the groups this rank owns
+      // (W sources x 1/W of the rows) plus the finished rows of the others.
+      if (owner) w->stage(r, sizeof(float) * (row_floats + (W - 1) * out_floats / W));
+      else w->stage(r, sizeof(float) * W * row_floats);
+    }
   if (fused) return launch_attention(/*push=*/1, /*fold_inline=*/1);
   // Everything the later stages allocate exists before the first launch.
   TFB_CHECK(ensure_barrier(w));
