@@ -387,6 +387,23 @@ def bench_fd(ctx, cfg, steps, warmup):
                 res[name] = time_steps(ctx, w.stream(ctx.rank), step, steps, warmup)
             res[name + "_clocks"] = clk.summary()
         _abi.check(w.lib.tf_world_sync(w.handle))
+        # The BSP schedule again, captured once into a CUDA graph and replayed
+        # (report BSP eager and graphed -- graphs remove its host
+        # launch cost; the device-side barriers and launches remain).  W = 1:
+        # every stage of it runs on the one stream passed in.
+        if W == 1:
+            try:
+                cs = torch.cuda.Stream()
+                bargs = (w.handle, _abi.TF_FD_BSP, C.byref(shape), _abi.ptr_array(ptrs_for(ctx, q.data_ptr())),
+                         _abi.ptr_array(ptrs_for(ctx, k.data_ptr())), _abi.ptr_array(ptrs_for(ctx, v.data_ptr())),
+                         _abi.ptr_array(ptrs_for(ctx, out.data_ptr())), None, _abi.ptr_array([cs.cuda_stream]))
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr, stream=cs):
+                    _abi.check(w.lib.tf_flash_decode_async(*bargs))
+                # replay() launches on the current stream
+                res["bsp_graph"] = time_steps(ctx, torch.cuda.current_stream(), gr.replay, steps, warmup)
+            except Exception as e:  # noqa: BLE001 -- reported, not fatal
+                res["bsp_graph_error"] = repr(e)[:200]
         # numerics spot check (W=1): torch fp32 attention on the same bf16 data
         err = None
         if W == 1:
@@ -398,7 +415,8 @@ def bench_fd(ctx, cfg, steps, warmup):
             err = float(((out[bb].float() - ref).abs().amax(-1) / ref.abs().amax(-1)).max().item())
         kv_bytes = 2 * B * Hkv * ln * d * 2
         return dict(fused_ms=res["fused"], bsp_ms=res["bsp"], owner_ms=res.get("owner"), kv_bytes=kv_bytes,
-                    err=err, clocks=res["fused_clocks"])
+                    err=err, clocks=res["fused_clocks"], bsp_graph_ms=res.get("bsp_graph"),
+                    bsp_graph_error=res.get("bsp_graph_error"))
     finally:
         w.close()
 
@@ -562,6 +580,11 @@ def main():
                          "head_rel_err_vs_torch_fp32": r["err"], "config": cfg, "clocks": r["clocks"]}
             if r.get("owner_ms"):
                 sec[name]["owner_combine_us"] = r["owner_ms"] * 1e3
+            if r.get("bsp_graph_ms"):
+                sec[name]["bsp_cuda_graph_us"] = r["bsp_graph_ms"] * 1e3
+                sec[name]["fused_speedup_vs_bsp_graph"] = r["bsp_graph_ms"] / r["fused_ms"]
+            elif r.get("bsp_graph_error"):
+                sec[name]["bsp_cuda_graph_error"] = r["bsp_graph_error"]
         line["secondary"] = sec
     if sweep:
         line.setdefault("secondary", {})["ag_msweep_K8192_N8192"] = {
