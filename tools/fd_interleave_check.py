@@ -1,3 +1,4 @@
+"""FD fast path: interleaved vs contiguous warp key assignment (TFB_FD_CONTIGUOUS) against torch fp32 at several KV lengths."""
 import ctypes as C, os, sys, torch
 sys.path.insert(0, "/root/repo")
 import paper_2511_02168_b200 as tf
