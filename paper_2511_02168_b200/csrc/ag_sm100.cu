@@ -98,6 +98,7 @@ struct AgTcParams {
   int q_tail;       // > 1: the tiles after them run as q_tail column slices each (last-wave balance)
   int total_items;
   int ldc;     // row pitch of C (elements)
+  int b4;      // whole tiles load B with ONE 4-D box per stage (tmB4) instead of NH * CPH 2-D boxes
   const __nv_bfloat16* peer_shard[64];
 };
 
@@ -158,6 +159,28 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint
         : "memory");
 }
 
+// 4-D box: this CTA's whole B slice of a k-block (NH halves x CPH 64-column
+// chunks x BK rows, 32 KB) in one instruction.  A TMA box costs the issuing
+// CTA a roughly fixed time whatever its size (tools/micro_tma_req.cu: 8 KB
+// boxes stream at ~31 GB/s per CTA, 32 KB boxes at ~125), so fewer, larger
+// boxes is what raises the L2->SM rate.
+template <int CG>
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c1,
+                                            int c2, int c3) {
+  if (CG == 2)
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(0), "r"(c1), "r"(c2), "r"(c3), "r"(bar_cluster)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+        "{%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(0), "r"(c1), "r"(c2), "r"(c3), "r"(bar_cluster)
+        : "memory");
+}
+
 template <int CG>
 __device__ __forceinline__ void mma_issue(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
                                           uint32_t idesc, uint32_t accumulate) {
@@ -211,7 +234,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ag_gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA_own,
                          const __grid_constant__ CUtensorMap tmA_inbox,
                          const __grid_constant__ CUtensorMap tmB,
-                         const __grid_constant__ CUtensorMap tmC, const AgTcParams p) {
+                         const __grid_constant__ CUtensorMap tmC,
+                         const __grid_constant__ CUtensorMap tmB4, const AgTcParams p) {
   using K_ = Cfg<CG, NH_>;
   constexpr int STAGES = K_::STAGES, NH = K_::NH, CPH = K_::CPH;
   extern __shared__ uint8_t smem_raw[];
@@ -270,6 +294,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tma_prefetch(&tmA_inbox);
     tma_prefetch(&tmB);
     tma_prefetch(&tmC);
+    if (p.b4) tma_prefetch(&tmB4);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], CG);  // one arrive per CTA of the pair (the leader's copy is used)
       mbar_init(&empty[s], 1);
@@ -323,7 +348,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (from_own) tma_load<CG>(a_dst, &tmA_own, bar, kb * BK - p.own * p.kw, m0);
           else tma_load<CG>(a_dst, &tmA_inbox, bar, kb * BK, m0);
           uint8_t* b_dst = smB + stage * K_::B_BYTES;
-          if (wcol == K_::BN_TILE) {
+          if (wcol == K_::BN_TILE && p.b4) {
+            tma_load_4d<CG>(b_dst, &tmB4, bar, kb * BK, int(prank) * CPH, n0 / 256);
+          } else if (wcol == K_::BN_TILE) {
 #pragma unroll
             for (int h = 0; h < NH; ++h)
 #pragma unroll
@@ -826,7 +853,7 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   // fills the SMs better (skinny M); single CTAs (128 x 256) for M <= 128.
   struct Shape {
     int CG, NH;
-    void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, AgTcParams);
+    void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, AgTcParams);
     size_t smem;
     int id;
   };
@@ -958,7 +985,22 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
       last_gm[dev & 63] = gm;
     }
   }
-  TFB_CUDA(cudaLaunchKernelEx(&cfg, kern, mOwn, mInbox, mB, mC, p));
+  // B as 4-D (64 columns, K rows, 4 chunks of a 256-column group, N/256
+  // groups): one box (64, BK, CPH, NH) is a CTA's whole B stage.
+  CUtensorMap mB4{};
+  p.b4 = 0;
+  if (sh.n % 256 == 0 && !std::getenv("TFB_NO_B4")) {
+    EncodeFn enc = encode_fn();
+    cuuint64_t dims[4] = {64, sh.k, 4, sh.n / 256};
+    cuuint64_t strides[3] = {ldb * 2, 128, 512};
+    cuuint32_t box[4] = {64, uint32_t(BK), uint32_t(4 / CG), uint32_t(shp->NH)};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    if (enc && enc(&mB4, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(b), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      p.b4 = 1;
+  }
+  TFB_CUDA(cudaLaunchKernelEx(&cfg, kern, mOwn, mInbox, mB, mC, mB4, p));
   ++w->launches;
   return TF_OK;
 }
