@@ -18,17 +18,21 @@
 static bool layout_only_panel_skip(int rows, int pan) { return rows * pan > 512; }
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__global__ void __launch_bounds__(32) stream(const __grid_constant__ CUtensorMap map, int layout, int rows,
+__global__ void __launch_bounds__(128) stream(const __grid_constant__ CUtensorMap map, int layout, int rows,
                                              int ntiles_r, int ntiles_c, int iters, int stages, int pan) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[16];
+  extern __shared__ __align__(1024) uint8_t smem_all[];
+  __shared__ __align__(8) uint64_t full_all[4][16];
   const uint32_t box_bytes = 64 * 2 * rows * pan;
-  if (threadIdx.x != 0) return;
+  if (threadIdx.x % 32 != 0) return;
+  const int wi = threadIdx.x / 32, nw = blockDim.x / 32;
+  uint64_t* full = full_all[wi];
+  uint8_t* smem = smem_all + size_t(wi) * stages * box_bytes;
+  const int vblock = blockIdx.x * nw + wi, vgrid = gridDim.x * nw;
   for (int s = 0; s < stages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&full[s])));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   auto issue = [&](int i) {
     const int s = i % stages;
-    const int t = (blockIdx.x + i * gridDim.x) % (ntiles_r * ntiles_c);
+    const int t = (vblock + i * vgrid) % (ntiles_r * ntiles_c);
     const int tr = t % ntiles_r, tc = t / ntiles_r;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(box_bytes)
                  : "memory");
@@ -137,6 +141,42 @@ int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int C = 8192;
+  if (getenv("TMA_WARPS")) {  // issuing warps per CTA: 1 CTA/SM, each warp its own ring
+    const size_t bytes = size_t(32) << 20;
+    const int R = int(bytes / (C * 2));
+    void* buf;
+    cudaMalloc(&buf, bytes);
+    cudaMemset(buf, 1, bytes);
+    for (int rows : {64, 128}) {
+      CUtensorMap map;
+      cuuint64_t dims[2] = {cuuint64_t(C), cuuint64_t(R)}, str[1] = {cuuint64_t(C) * 2};
+      cuuint32_t box[2] = {64, cuuint32_t(rows)}, es[2] = {1, 1};
+      enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      for (int nw : {1, 2, 4}) {
+        const int stages = 8 / nw;
+        const size_t smem = size_t(nw) * stages * 128 * rows;
+        const int ntr = R / rows, ntc = C / 64;
+        const int iters = 400 / nw;
+        cudaFuncSetAttribute(stream, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        stream<<<sms, 32 * nw, smem>>>(map, 0, rows, ntr, ntc, iters, stages, 1);
+        cudaEventRecord(e0);
+        stream<<<sms, 32 * nw, smem>>>(map, 0, rows, ntr, ntc, iters, stages, 1);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double moved = double(iters) * nw * sms * 128 * rows;
+        printf("warps %d box %3d rows (%2d KB) stages/warp %d: %7.1f GB/s, %5.1f per SM (%s)\n", nw, rows,
+               rows * 128 / 1024, stages, moved / ms / 1e6, moved / ms / 1e6 / sms,
+               cudaGetErrorString(cudaGetLastError()));
+      }
+    }
+    return 0;
+  }
   {  // multicast sweep, L2-resident 32 MiB
     const size_t bytes = size_t(32) << 20;
     const int R = int(bytes / (C * 2));
