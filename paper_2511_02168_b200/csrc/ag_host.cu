@@ -29,23 +29,6 @@
 namespace tfb {
 namespace {
 
-tf_status ensure_scratch(World* w, int r, int slot, size_t bytes, void** out) {
-  RankRes& rr = w->ranks[r];
-  if (rr.scratch_bytes[slot] < bytes) {
-    cudaSetDevice(rr.device);
-    if (rr.scratch[slot]) {
-      TFB_CUDA(cudaDeviceSynchronize());
-      TFB_CUDA(cudaFree(rr.scratch[slot]));
-      rr.scratch[slot] = nullptr;
-      rr.scratch_bytes[slot] = 0;
-    }
-    TFB_CUDA(cudaMalloc(&rr.scratch[slot], bytes));
-    rr.scratch_bytes[slot] = bytes;
-  }
-  *out = rr.scratch[slot];
-  return TF_OK;
-}
-
 tf_status ensure_copy_streams(World* w, int r) {
   RankRes& rr = w->ranks[r];
   cudaSetDevice(rr.device);

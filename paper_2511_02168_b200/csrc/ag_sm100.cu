@@ -99,6 +99,7 @@ struct AgTcParams {
   int total_items;
   int ldc;     // row pitch of C (elements)
   int b4;      // whole tiles load B with ONE 4-D box per stage (tmB4) instead of NH * CPH 2-D boxes
+  uint8_t* ws;  // split-K exchange through L2: [grid CTAs][NH][128 rows x 1 KB]; nullptr: through DSMEM
   const __nv_bfloat16* peer_shard[64];
 };
 
@@ -247,7 +248,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rbar = tempty + 2;  // split-K (L2 exchange): siblings' slices landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Cluster = CG * ksplit CTAs: pairs (cta_group::2) at ranks (2j, 2j+1),
@@ -303,6 +305,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4 * CG);
     }
+    mbar_init(rbar, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc_cg<CG>(tmem_slot);
@@ -635,7 +638,50 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
-      cluster_sync();
+      if (p.ws) {
+        // L2 exchange: slice j of this partial (rows [j*rp, (j+1)*rp), whole
+        // 1 KB rows, contiguous in R) goes to workspace ws[cta][h] by one
+        // bulk copy each; after the cluster barrier each CTA bulk-loads its
+        // siblings' copies of the slice it owns into the vacated slice
+        // positions of its own R, then sums all S from local smem in
+        // ascending split order (the same bits as the DSMEM path).  DSMEM
+        // moves ~8-9 B/clk per SM when every SM reduces at once
+        // (tools/micro_dsmem.cu).
+        const uint32_t slice = uint32_t(rows_per) * 1024u;
+        uint8_t* wsme = p.ws + (size_t(blockIdx.x) * NH + h) * (size_t(BM) * 1024);
+        fence_proxy_async_shared();
+        named_bar(2, NUM_THREADS);
+        if (threadIdx.x == 0) {
+          for (int j = 0; j < S; ++j) {
+            if (j == ks) continue;
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(wsme + j * slice),
+                         "r"(smem_u32(R) + j * slice), "r"(slice)
+                         : "memory");
+          }
+          bulk_commit();
+          bulk_wait_all();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          mbar_arrive_expect_tx(rbar, slice * uint32_t(S - 1));
+        }
+        cluster_sync();
+        if (threadIdx.x == 0) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          const int cta0 = int(blockIdx.x) - int(crank);  // cluster's first CTA
+          for (int j = 0; j < S; ++j) {
+            if (j == ks) continue;
+            const uint8_t* from = p.ws + (size_t(cta0 + int(prank) + CG * j) * NH + h) * (size_t(BM) * 1024) +
+                                  size_t(ks) * slice;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(R) + j * slice),
+                "l"(from), "r"(slice), "r"(smem_u32(rbar))
+                : "memory");
+          }
+        }
+        mbar_wait(rbar, uint32_t(h & 1));
+      } else {
+        cluster_sync();
+      }
       uint32_t src[8];
 #pragma unroll
       for (int s2 = 0; s2 < 8; ++s2)
@@ -650,7 +696,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         float4 x[8], y[8];
 #pragma unroll
         for (int s2 = 0; s2 < 8; ++s2) {
-          if (s2 < S) {
+          if (s2 < S && p.ws) {  // sibling s2's copy sits in slice position s2 of R
+            const uint8_t* b = reinterpret_cast<const uint8_t*>(R) + (s2 - ks) * rows_per * 1024;
+            x[s2] = *reinterpret_cast<const float4*>(b + off0);
+            y[s2] = *reinterpret_cast<const float4*>(b + off1);
+          } else if (s2 < S) {
             asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
                          : "=f"(x[s2].x), "=f"(x[s2].y), "=f"(x[s2].z), "=f"(x[s2].w) : "r"(src[s2] + off0));
             asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -674,7 +724,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           *reinterpret_cast<uint4*>(p.C + size_t(grow) * p.ldc + gcol) = o;
         }
       }
-      cluster_sync();  // siblings done reading R before it is rewritten / released
+      if (p.ws) named_bar(2, NUM_THREADS);  // R fully read before the next half's dump
+      else cluster_sync();  // siblings done reading R before it is rewritten / released
     }
   }
 
@@ -948,6 +999,16 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   unsigned grid = std::min(pair_tiles * CG, grid_cap / CG * CG);
   grid = std::max(grid, unsigned(CG));
   if (p.ksplit > 1) grid = pair_tiles * CG;  // exactly one item per CTA (the reduction aliases its smem)
+  p.ws = nullptr;
+  // Split-K partials cross through L2 (bulk copies) for one-half tiles:
+  // measured 35.7 vs 37.7 us at M = 128 (tools/ab_gemm.py, TFB_SPLITK_DSMEM
+  // A/B); two-half tiles pay the copy-then-barrier latency chain twice and
+  // lose ~2 us at M = 512, so they keep the DSMEM path.
+  if (p.ksplit > 1 && shp->NH == 1 && !std::getenv("TFB_SPLITK_DSMEM")) {
+    void* ws = nullptr;
+    TFB_CHECK(ensure_scratch(w, r, 2, size_t(grid) * shp->NH * BM * 1024, &ws));
+    p.ws = static_cast<uint8_t*>(ws);
+  }
   // Last-wave balance (CTA pairs, whole-K tiles): when the tiles leave a
   // partial last round, cut its tiles into 2 or 4 column slices so that
   // round runs on (nearly) every pair for a half or quarter of a tile time.

@@ -117,6 +117,23 @@ std::vector<cudaStream_t> resolve_streams(World* w, void* const* streams) {
   return s;
 }
 
+tf_status ensure_scratch(World* w, int r, int slot, size_t bytes, void** out) {
+  RankRes& rr = w->ranks[r];
+  if (rr.scratch_bytes[slot] < bytes) {
+    cudaSetDevice(rr.device);
+    if (rr.scratch[slot]) {
+      TFB_CUDA(cudaDeviceSynchronize());
+      TFB_CUDA(cudaFree(rr.scratch[slot]));
+      rr.scratch[slot] = nullptr;
+      rr.scratch_bytes[slot] = 0;
+    }
+    TFB_CUDA(cudaMalloc(&rr.scratch[slot], bytes));
+    rr.scratch_bytes[slot] = bytes;
+  }
+  *out = rr.scratch[slot];
+  return TF_OK;
+}
+
 tf_status order_after_legacy(World* w, void* const* streams) {
   for (int r = 0; r < w->W; ++r) {
     if (!w->ranks[r].local || (streams && streams[r])) continue;

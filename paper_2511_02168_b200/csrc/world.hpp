@@ -28,8 +28,9 @@ struct RankRes {
   // buffers, created on first use, grow-only.
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t legacy_ev = nullptr;  // order_after_legacy
-  void* scratch[2] = {nullptr, nullptr};
-  size_t scratch_bytes[2] = {0, 0};
+  // [0] B / [1] C device operands of host-buffer runs, [2] split-K workspace
+  void* scratch[3] = {nullptr, nullptr, nullptr};
+  size_t scratch_bytes[3] = {0, 0, 0};
 };
 
 struct HeapEntry {
@@ -150,6 +151,8 @@ std::vector<cudaStream_t> resolve_streams(World* w, void* const* streams);
 // after everything already issued on the legacy default stream, where a
 // caller typically produced the inputs (torch, cudaMemcpy, ...).
 tf_status order_after_legacy(World* w, void* const* streams);
+// Grow-only device scratch of rank r (slot < 3); first use allocates.
+tf_status ensure_scratch(World* w, int r, int slot, size_t bytes, void** out);
 // Wait for local streams and turn the device error record into a status.
 tf_status sync_and_check(World* w, const std::vector<cudaStream_t>& streams);
 tf_status check_record(World* w);
