@@ -118,3 +118,25 @@ def test_push_loopback_ranks_share_the_sms(oracle):
             assert norm_err(c, ref) <= TOL
         for counts in run.flag_counts:
             assert counts == [1] * len(counts)
+
+
+@pytest.mark.parametrize("m,n,k", [(1024, 7168, 512),   # <2,2> pair tiles, N % 512 != 0 (last tile half OOB)
+                                   (128, 8192, 2048),   # <1,1> + split-K (L2 exchange)
+                                   (256, 2304, 1024)])  # <2,1> or <2,2> + split-K (DSMEM exchange)
+def test_b_box_and_splitk_exchange_bitwise(oracle, monkeypatch, m, n, k):
+    """The 4-D B box (a CTA's whole B stage in one TMA box) stages the same
+    bytes as the per-chunk 2-D boxes, and the L2 split-K exchange sums the
+    same partials in the same order as the DSMEM one: C is bitwise equal
+    across TFB_NO_B4 / TFB_SPLITK_DSMEM, and within the bf16 bar."""
+    import torch
+    p = bf16_problem(m + n + k, m, n, k, oracle)
+    base = tf.ag.run_pull(p, tf.WorldConfig(world_size=1), dtype=1).c[0]
+    monkeypatch.setenv("TFB_NO_B4", "1")
+    no_b4 = tf.ag.run_pull(p, tf.WorldConfig(world_size=1), dtype=1).c[0]
+    monkeypatch.delenv("TFB_NO_B4")
+    monkeypatch.setenv("TFB_SPLITK_DSMEM", "1")
+    dsmem = tf.ag.run_pull(p, tf.WorldConfig(world_size=1), dtype=1).c[0]
+    assert np.array_equal(base, no_b4)
+    assert np.array_equal(base, dsmem)
+    ref = (torch.from_numpy(p.a).double() @ torch.from_numpy(p.b).double()).float().numpy()
+    assert norm_err(base, ref) <= TOL
