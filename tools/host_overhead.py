@@ -27,3 +27,22 @@ with tf.World(1, [0], 512 << 20) as w:
     for _ in range(2000):
         f(w.handle)
     print(f"bare ctypes call {(time.perf_counter()-t0)/2000*1e6:.2f} us")
+# AG pull at the skinny end of config 5 (M = 128, K = N = 8192): host cost of
+# one call (tensor-map encodes, plan, launch) vs the kernel's ~36 us.
+M, K, N = 128, 8192, 8192
+with tf.World(1, [0], M * K * 2 + (64 << 20)) as w:
+    sh = w.alloc("ag.a", M * K * 2)
+    B = (torch.rand(K, N, device="cuda") * 2 - 1).bfloat16()
+    Cm = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    shape = _abi.AgShape(M, N, K, 0, 0, 0, _abi.TF_BF16)
+    args = (w.handle, _abi.TF_AG_PULL, C.byref(shape), _abi.ptr_array(sh), _abi.ptr_array([B.data_ptr()]),
+            _abi.ptr_array([Cm.data_ptr()]), None, None)
+    _abi.check(w.lib.tf_ag_gemm(*args))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(200):
+        w.lib.tf_ag_gemm_async(*args)
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    print(f"AG M=128 host per call {(t1-t0)/200*1e6:.1f} us, wall per call incl. GPU {(t2-t0)/200*1e6:.1f} us")
