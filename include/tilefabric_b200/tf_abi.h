@@ -161,7 +161,11 @@ tf_status tf_signal_soak(tf_world* w, uint64_t seed, int rounds,
  * NULL to let the world use an internal heap buffer.  streams: per-rank
  * cudaStream_t or NULL (world streams, ordered after the work already
  * issued on the legacy default stream -- where callers usually produce the
- * inputs; with explicit streams the caller owns the ordering).  Arrays are indexed by global rank;
+ * inputs; with explicit streams the caller owns the ordering).  CUDA-graph
+ * capture: a single-rank world's *_async calls may be captured on an
+ * explicit stream and replayed (per-launch counters reset on the device;
+ * after one eager call, so lazily allocated workspace exists); capturing a
+ * multi-rank schedule returns TF_ERR_CONFIG.  Arrays are indexed by global rank;
  * entries for ranks not local to this process are ignored except a_shard,
  * whose peer entries must be the heap mappings tf_heap_alloc returned. */
 typedef struct {

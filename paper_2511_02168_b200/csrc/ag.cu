@@ -49,6 +49,7 @@ extern "C" tf_status tf_ag_gemm_async(tf_world* tw, tf_ag_variant variant,
   if (sh.bn == 0) sh.bn = 16;
   if (sh.bk == 0) sh.bk = 16;
   auto s = resolve_streams(w, streams);
+  TFB_CHECK(refuse_multi_rank_capture(w, s, "tf_ag_gemm"));
   TFB_CHECK(order_after_legacy(w, streams));
   if (sh.dtype == TF_F32) return ag_exact_run(w, variant, sh, a_shard, b, c, gathered_opt, s);
   return ag_bf16_run(w, variant, sh, a_shard, b, c, gathered_opt, s);

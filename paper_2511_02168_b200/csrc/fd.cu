@@ -1292,6 +1292,7 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
     return set_error(TF_ERR_CONFIG, "run_fd: unknown variant");
   const tf_fd_shape& sh = *shape;
   auto st = resolve_streams(w, streams);
+  TFB_CHECK(refuse_multi_rank_capture(w, st, "tf_flash_decode"));
   TFB_CHECK(order_after_legacy(w, streams));
   const int W = w->W, d = sh.head_dim, G = sh.batch * sh.kv_heads, gs = sh.q_heads / sh.kv_heads;
   const size_t len = sh.kv_len / W;

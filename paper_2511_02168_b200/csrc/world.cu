@@ -134,6 +134,23 @@ tf_status ensure_scratch(World* w, int r, int slot, size_t bytes, void** out) {
   return TF_OK;
 }
 
+tf_status refuse_multi_rank_capture(World* w, const std::vector<cudaStream_t>& s, const char* what) {
+  if (w->W == 1) return TF_OK;
+  for (int r = 0; r < w->W; ++r) {
+    if (!w->ranks[r].local) continue;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s[r], &cs) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (cs != cudaStreamCaptureStatusNone)
+      return set_error(TF_ERR_CONFIG, std::string(what) +
+                                          ": graph capture of a multi-rank schedule is unsupported (its flag "
+                                          "epochs are host state; a replay would wait on stale values)");
+  }
+  return TF_OK;
+}
+
 tf_status order_after_legacy(World* w, void* const* streams) {
   for (int r = 0; r < w->W; ++r) {
     if (!w->ranks[r].local || (streams && streams[r])) continue;

@@ -151,6 +151,10 @@ std::vector<cudaStream_t> resolve_streams(World* w, void* const* streams);
 // after everything already issued on the legacy default stream, where a
 // caller typically produced the inputs (torch, cudaMemcpy, ...).
 tf_status order_after_legacy(World* w, void* const* streams);
+// Multi-rank schedules bake host state (flag epochs, board epochs) into
+// their launches, so a captured graph would replay stale waits: refuse
+// (TF_ERR_CONFIG) when W > 1 and any rank's stream is capturing.
+tf_status refuse_multi_rank_capture(World* w, const std::vector<cudaStream_t>& s, const char* what);
 // Grow-only device scratch of rank r (slot < 3); first use allocates.
 tf_status ensure_scratch(World* w, int r, int slot, size_t bytes, void** out);
 // Wait for local streams and turn the device error record into a status.
