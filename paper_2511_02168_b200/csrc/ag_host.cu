@@ -54,6 +54,11 @@ struct Trace {
   cudaEvent_t t0 = nullptr;
   std::vector<std::pair<std::string, cudaEvent_t>> ev;
   void start(cudaStream_t s) {
+    // Only the latest call is traced: drop what earlier (async) calls marked.
+    for (auto& pe : ev) cudaEventDestroy(pe.second);
+    ev.clear();
+    if (t0) cudaEventDestroy(t0);
+    t0 = nullptr;
     on = std::getenv("TFB_HOST_TRACE") != nullptr;
     if (!on) return;
     cudaEventCreate(&t0);
@@ -75,6 +80,7 @@ struct Trace {
       cudaEventDestroy(e);
     }
     cudaEventDestroy(t0);
+    t0 = nullptr;
     ev.clear();
     on = false;
   }
