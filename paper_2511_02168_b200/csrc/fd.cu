@@ -1052,12 +1052,14 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
       if (threadIdx.x == 0) {
         // This sub-item's rows before the count (system scope only when a
         // destination inbox is on another device).
-        if (P.push) {
+        // direct (W = 1): the rows are the final output, read only after the
+        // launch retires, so the count and flags need no ordering.
+        if (P.push && !P.direct) {
           if (P.local_dst == (P.W >= 64 ? ~0ull : ((1ull << P.W) - 1))) __threadfence();
           else __threadfence_system();
         }
-        s_last = atom_add_acq_rel_gpu(reinterpret_cast<unsigned long long*>(P.gtick + size_t(lr) * G + g), 1ull) ==
-                 uint64_t(nhc) - 1;
+        unsigned long long* gt = reinterpret_cast<unsigned long long*>(P.gtick + size_t(lr) * G + g);
+        s_last = (P.direct ? atomicAdd(gt, 1ull) : atom_add_acq_rel_gpu(gt, 1ull)) == uint64_t(nhc) - 1;
       }
       __syncthreads();
       if (!P.push || !s_last) continue;
@@ -1066,7 +1068,8 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
         uint64_t* f = P.flags_all[threadIdx.x] + size_t(R.rank) * G + g;
         if (P.events_all[threadIdx.x])  // this source's rows of g are in dst's inbox
           P.events_all[threadIdx.x][(size_t(R.rank) * G + g) * 2] = globaltimer_ns();
-        if ((P.local_dst >> threadIdx.x) & 1ull) red_release_gpu(f, 1);
+        if (P.direct) atomicAdd(reinterpret_cast<unsigned long long*>(f), 1ull);
+        else if ((P.local_dst >> threadIdx.x) & 1ull) red_release_gpu(f, 1);
         else red_release_sys(f, 1);
       }
       stamp(3);
