@@ -464,18 +464,6 @@ __device__ void fast_split(const FdParams& P, int lr, int g, int sp, float* wsro
   const __nv_bfloat16* V = static_cast<const __nv_bfloat16*>(R.v) + (size_t(b) * P.Hkv + kvh) * P.len * 128;
   const __nv_bfloat16* Q = static_cast<const __nv_bfloat16*>(R.q) + (size_t(b) * P.Hq + kvh * 8) * 128;
   if (threadIdx.x == 0) sm.bad = 0;
-  // Warm L2 with the split's first 256 keys of K and V (two interleaved
-  // tiles per warp, 128 KB) while q is fetched: the first tiles' loads then
-  // hit L2 instead of starting a DRAM round trip after the q barrier.
-  {
-    const size_t bytes = min(k1 - k0, size_t(256)) * 256;
-    const char* kb0 = reinterpret_cast<const char*>(K + k0 * 128);
-    const char* vb0 = reinterpret_cast<const char*>(V + k0 * 128);
-    for (size_t off = size_t(threadIdx.x) * 128; off < bytes; off += size_t(blockDim.x) * 128) {
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(kb0 + off));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(vb0 + off));
-    }
-  }
   for (int i = threadIdx.x; i < 8 * 16; i += blockDim.x) sm.q[i] = reinterpret_cast<const uint4*>(Q)[i];
   __syncthreads();
   trace_at(P, 12);
