@@ -3,7 +3,10 @@ kernels' edge handling -- ragged M/N tiles, split-K, tail slices, skinny
 and wide M, odd world sizes, GQA groupings, short and ragged KV splits).
 AG: bf16 vs an fp64 product (4e-3 normalised), fp32 bitwise vs the oracle's
 reference::gemm; FD: fp32 head-relative error vs the oracle (1e-5) and
-bitwise agreement of every schedule and rank."""
+bitwise agreement of every schedule and rank.  TFB_FUZZ_SCALE=k runs k times
+as many cases (the first ones are always the default set)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -11,9 +14,10 @@ import paper_2511_02168_b200 as tf
 
 pytestmark = pytest.mark.gpu
 V = tf.fd.Variant
+SCALE = max(1, int(os.environ.get("TFB_FUZZ_SCALE", "1")))
 
 
-def _ag_cases(n=14):
+def _ag_cases(n=14 * SCALE):
     rng = np.random.default_rng(2024)
     out = []
     for _ in range(n):
@@ -41,7 +45,7 @@ def test_ag_bf16_random_shapes(oracle, w, m, n, k):
             assert np.array_equal(g.view(np.uint32), p.a.view(np.uint32))
 
 
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(6 * SCALE))
 def test_ag_fp32_random_shapes_bitwise(oracle, seed):
     rng = np.random.default_rng(seed)
     w = int(rng.choice([1, 2, 3, 4]))
@@ -55,7 +59,7 @@ def test_ag_fp32_random_shapes_bitwise(oracle, seed):
             assert np.array_equal(c.view(np.uint32), want.view(np.uint32)), (fn.__name__, seed)
 
 
-def _fd_cases(n=10):
+def _fd_cases(n=10 * SCALE):
     rng = np.random.default_rng(77)
     out = []
     for _ in range(n):
