@@ -155,10 +155,20 @@ tf_status tf_signal_soak(tf_world* w, uint64_t seed, int rounds,
  *                    the reference's TileSpec (tilemath.hpp:78-88).
  *   dtype TF_BF16 -> tcgen05/TMEM tensor-core path, fp32 accumulate, bf16 C;
  *                    requires kw % 64 == 0, n % 8 == 0 (TMA strides).
- * a_shard[r] must be a symmetric-heap region (peers read or push it).
+ * a_shard[r] must be a symmetric-heap region (peers read or push it), and
+ * every rank's shard must be complete before any rank's call starts: the
+ * reference fences the placement (RankCtx::setup_fence after fill_shard,
+ * ag_gemm.hpp:189-191, 232-233; fabric.hpp:586-592) outside the timed
+ * schedule, and so does this API -- fill the shards, then tf_world_barrier
+ * (or, across processes, the launcher's own barrier after a device sync),
+ * then call.  PULL reads peer shards with no further fence.
  * gathered_opt[r] (m x k, dtype of A) receives the gathered operand, bit for
  * bit the logical A (the reference's inbox/stage, ag_gemm.hpp:139,234); pass
- * NULL to let the world use an internal heap buffer.  streams: per-rank
+ * NULL to let the world use an internal heap buffer (double-buffered where
+ * peers write it).  A caller buffer is a single buffer, so PUSH then enters a
+ * world barrier before its producers run (no peer may store into a buffer
+ * its owner is still reading); use tf_ag_gathered instead to inspect the
+ * internal operand without it.  streams: per-rank
  * cudaStream_t or NULL (world streams, ordered after the work already
  * issued on the legacy default stream -- where callers usually produce the
  * inputs; with explicit streams the caller owns the ordering).  CUDA-graph
@@ -181,6 +191,13 @@ tf_status tf_ag_gemm_async(tf_world* w, tf_ag_variant variant,
                            const tf_ag_shape* shape, void* const* a_shard,
                            const void* const* b, void* const* c,
                            void* const* gathered_opt, void* const* streams);
+/* The gathered operand of the last All-Gather+GEMM run on `rank`, m x k
+ * row-major (dtype of A) into dst (host or device, >= m*k*esz bytes): the
+ * inbox/stage that run's GEMM consumed, with the blocks a schedule reads in
+ * place (PULL's own shard; every block of an fp32 PULL, which stages
+ * nothing, ag_gemm.hpp:185-222) taken from the shards.  The placement check
+ * of ag_gemm_test.cpp:113-169.  Waits for the world's streams first. */
+tf_status tf_ag_gathered(tf_world* w, int rank, void* dst, size_t bytes);
 /* Host-buffer All-Gather+GEMM: the reference's calling convention, where
  * AgGemmProblem holds host vectors and AgGemmRun returns host C
  * (ag_gemm.hpp:47-99, 134-305).  a_host[r]: rank r's m x kw shard, b_host[r]:

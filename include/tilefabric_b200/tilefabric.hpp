@@ -203,7 +203,7 @@ inline AgGemmProblem make_problem(std::uint64_t seed, std::size_t m, std::size_t
 struct AgGemmRun {  // ag_gemm.hpp:85-92
   std::vector<std::vector<float>> c;                 // per rank, m x n
   std::vector<std::vector<std::uint64_t>> flag_counts;  // push only
-  std::vector<std::vector<float>> gathered;          // per rank, m x k (baseline/push)
+  std::vector<std::vector<float>> gathered;          // per rank, m x k: the operand the GEMM consumed
   std::uint64_t launches = 0;                        // kernels this run launched
   std::vector<tf_taxes> taxes;                       // per rank, measured on the device
 };
@@ -221,7 +221,6 @@ inline AgGemmRun run(tf_ag_variant variant, const AgGemmProblem& p, const WorldC
   b200::World w(W, cfg.device_list(), heap, cfg.watchdog_secs);
   w.apply(cfg);
   auto shards = w.heap("ag.a", esz * p.m * kw);
-  auto gathered = w.heap("ag.gathered", esz * p.m * p.k);
   std::vector<void*> B(W), C(W);
   auto pack = [&](const float* src, std::size_t n) {
     std::vector<uint8_t> out(n * esz);
@@ -243,10 +242,15 @@ inline AgGemmRun run(tf_ag_variant variant, const AgGemmProblem& p, const WorldC
     w.put(B[r], hb.data(), hb.size());
     C[r] = w.device(r, esz * p.m * p.n);
   }
+  // setup_fence (ag_gemm.hpp:189-191, fabric.hpp:586-592): every shard is
+  // placed before any rank's schedule reads or pushes it; untimed, so the
+  // tax meter starts after it.
+  b200::check(tf_world_barrier(w.w, -1));
+  b200::check(tf_tax_reset(w.w));
   tf_ag_shape sh{p.m, p.n, p.k, p.tiles.bm, p.tiles.bn, p.tiles.bk, bf ? TF_BF16 : TF_F32};
   const std::uint64_t l0 = tf_launch_count(w.w);
   b200::check(tf_ag_gemm(w.w, variant, &sh, shards.data(), const_cast<const void* const*>(B.data()),
-                         C.data(), variant == TF_AG_PULL ? nullptr : gathered.data(), nullptr));
+                         C.data(), nullptr, nullptr));
   AgGemmRun out;
   out.launches = tf_launch_count(w.w) - l0;
   out.taxes = w.taxes();
@@ -261,7 +265,16 @@ inline AgGemmRun run(tf_ag_variant variant, const AgGemmProblem& p, const WorldC
   };
   for (int r = 0; r < W; ++r) {
     out.c.push_back(unpack(C[r], p.m * p.n));
-    if (variant != TF_AG_PULL) out.gathered.push_back(unpack(gathered[r], p.m * p.k));
+    {
+      // The operand rank r's GEMM consumed (tf_ag_gathered), every schedule.
+      std::vector<uint8_t> raw(esz * p.m * p.k);
+      b200::check(tf_ag_gathered(w.w, r, raw.data(), raw.size()));
+      std::vector<float> f(p.m * p.k);
+      for (std::size_t i = 0; i < f.size(); ++i)
+        f[i] = bf ? b200::from_bf16(reinterpret_cast<uint16_t*>(raw.data())[i])
+                  : reinterpret_cast<float*>(raw.data())[i];
+      out.gathered.push_back(std::move(f));
+    }
     if (variant == TF_AG_PUSH) {
       std::size_t cnt = 0;
       b200::check(tf_ag_flag_counts(w.w, r, nullptr, 0, &cnt));

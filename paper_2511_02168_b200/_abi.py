@@ -114,6 +114,7 @@ SIGNATURES = {
     "tf_ag_events": (C.c_int, [_P, C.c_int, C.POINTER(C.c_uint64), C.c_size_t, C.POINTER(C.c_size_t)]),
     "tf_fd_events": (C.c_int, [_P, C.c_int, C.POINTER(C.c_uint64), C.c_size_t, C.POINTER(C.c_size_t)]),
     "tf_ag_gemm_host_async": (C.c_int, [_P, C.c_int, C.POINTER(AgShape), _PP, _PP, _PP, _PP]),
+    "tf_ag_gathered": (C.c_int, [_P, C.c_int, _P, C.c_size_t]),
     "tf_ag_flag_counts": (C.c_int, [_P, C.c_int, C.POINTER(C.c_uint64), C.c_size_t,
                                     C.POINTER(C.c_size_t)]),
     "tf_flash_decode": (C.c_int, [_P, C.c_int, C.POINTER(FdShape), _PP, _PP, _PP, _PP, _PP, _PP]),

@@ -96,3 +96,25 @@ extern "C" tf_status tf_ag_events(tf_world* tw, int rank, uint64_t* out, size_t 
   TFB_CUDA(cudaMemcpy(out, w->ptr(rank, w->ag_events_off), n * sizeof(uint64_t), cudaMemcpyDefault));
   return TF_OK;
 }
+
+// The gathered operand of the last AG run on `rank`, m x k row-major into
+// dst (host or device): the placement check (ag_gemm_test.cpp:113-169,
+// the inbox/stage equals the logical A).  Blocks until the rank is idle.
+extern "C" tf_status tf_ag_gathered(tf_world* tw, int rank, void* dst, size_t bytes) {
+  if (!tw || !dst) return set_error(TF_ERR_CONFIG, "tf_ag_gathered: NULL argument");
+  World* w = &tw->impl;
+  if (rank < 0 || rank >= w->W || !w->ranks[rank].local)
+    return set_error(TF_ERR_BOUNDS, "tf_ag_gathered: rank " + std::to_string(rank) + " is not local");
+  if (w->ag_src.empty()) return set_error(TF_ERR_CONFIG, "tf_ag_gathered: no All-Gather+GEMM run yet");
+  const size_t m = w->ag_m, kw = w->ag_kw, esz = w->ag_esz, k = kw * size_t(w->W);
+  if (bytes < m * k * esz)
+    return set_error(TF_ERR_BOUNDS, "tf_ag_gathered: need " + std::to_string(m * k * esz) + " bytes");
+  TFB_CUDA(cudaSetDevice(w->ranks[rank].device));
+  TFB_CHECK(sync_and_check(w, resolve_streams(w, nullptr)));
+  for (int s = 0; s < w->W; ++s) {
+    const World::AgBlock& b = w->ag_src[rank][s];
+    TFB_CUDA(cudaMemcpy2D(static_cast<char*>(dst) + size_t(s) * kw * esz, k * esz,
+                          static_cast<const char*>(b.p), b.pitch * esz, kw * esz, m, cudaMemcpyDefault));
+  }
+  return TF_OK;
+}

@@ -140,7 +140,11 @@ tf_status ag_exact_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh,
   SrcTable shards{};
   for (int s = 0; s < W; ++s) shards.p[s] = static_cast<const float*>(a_shard[s]);
 
+  w->record_ag(m, kw, 4);
   if (variant == TF_AG_PULL) {
+    // No staged operand (ag_gemm.hpp:185-222): every block is read in place.
+    for (int r = 0; r < W; ++r)
+      for (int s = 0; s < W; ++s) w->ag_src[r][s] = {a_shard[s], kw};
     for (int r = 0; r < W; ++r) {
       if (!w->ranks[r].local) continue;
       cudaSetDevice(w->ranks[r].device);
@@ -154,23 +158,40 @@ tf_status ag_exact_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh,
     return TF_OK;
   }
 
-  // baseline and push both stage the gathered operand per rank.
+  // baseline and push both stage the gathered operand per rank.  PUSH's
+  // internal inbox is written by peers, so it is double-buffered by the
+  // flag epoch's parity: a fast peer's run N+1 lands in the other buffer
+  // while this rank's run N still reads its inbox (the bf16 path does the
+  // same, ag_sm100.cu).  A caller-supplied buffer is single: PUSH then
+  // enters a world barrier first, so no peer stores into it before every
+  // rank finished its previous run.
+  const int n_kb = int((kw + bk - 1) / bk);
+  BoardEntry fb{};
+  if (variant == TF_AG_PUSH) {
+    TFB_CHECK(board_next_epoch(w, "ag.flags", W, n_kb, &fb));
+    w->ag_flags = FlagSnapshot{w->board_names[fb.id], size_t(W) * n_kb, fb.epoch};
+  }
   std::vector<float*> stage(W, nullptr);
   size_t stage_off = 0;
-  bool internal = false;
+  bool internal = false, caller = false;
   for (int r = 0; r < W; ++r) {
     if (gathered && gathered[r]) {
       stage[r] = static_cast<float*>(gathered[r]);
+      caller = true;
     } else {
       internal = true;
     }
   }
   if (internal) {
-    TFB_CHECK(heap_get(w, variant == TF_AG_PUSH ? "ag.inbox" : "ag.stage",
-                       sizeof(float) * m * k, &stage_off));
+    const bool push = variant == TF_AG_PUSH;
+    TFB_CHECK(heap_get(w, push ? "ag.inbox" : "ag.stage", sizeof(float) * m * k * (push ? 2 : 1), &stage_off));
+    const size_t half = push ? size_t(fb.epoch & 1) * m * k : 0;
     for (int r = 0; r < W; ++r)
-      if (!(gathered && gathered[r])) stage[r] = reinterpret_cast<float*>(w->ptr(r, stage_off));
+      if (!(gathered && gathered[r])) stage[r] = reinterpret_cast<float*>(w->ptr(r, stage_off)) + half;
   }
+  if (variant == TF_AG_PUSH && caller && W > 1) TFB_CHECK(world_barrier(w, streams));
+  for (int r = 0; r < W; ++r)
+    for (int s = 0; s < W; ++s) w->ag_src[r][s] = {stage[r] + size_t(s) * kw, k};
 
   for (int r = 0; r < W; ++r)
     if (w->ranks[r].local) w->stage(r, sizeof(float) * m * k);  // the gathered copy lands in HBM
@@ -203,11 +224,7 @@ tf_status ag_exact_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh,
   }
 
   // push
-  const int n_kb = int((kw + bk - 1) / bk);
-  BoardEntry fb;
-  TFB_CHECK(board_next_epoch(w, "ag.flags", W, n_kb, &fb));
   const uint64_t epoch = fb.epoch;
-  w->ag_flags = FlagSnapshot{w->board_names[fb.id], size_t(W) * n_kb, epoch};
   DstTable dt{};
   for (int d = 0; d < W; ++d) {
     dt.inbox[d] = stage[d];

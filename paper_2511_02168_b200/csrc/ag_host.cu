@@ -85,7 +85,9 @@ struct Trace {
     on = false;
   }
 };
-Trace g_trace;
+// Debug timeline (TFB_HOST_TRACE); per host thread, so concurrent worlds on
+// different threads never share it.
+thread_local Trace g_trace;
 
 }  // namespace
 
@@ -146,6 +148,8 @@ extern "C" tf_status tf_ag_gemm_host_async(tf_world* tw, tf_ag_variant variant, 
       return set_error(TF_ERR_CONFIG, "tf_ag_gemm_host: a/b/c for local rank " + std::to_string(r) +
                                           " is NULL");
   auto s = resolve_streams(w, streams);
+  TFB_CHECK(refuse_multi_rank_capture(w, s, "tf_ag_gemm_host"));
+  TFB_CHECK(order_after_legacy(w, streams));
   g_trace.start(s[w->first_local]);
   const int tr = w->first_local;
 

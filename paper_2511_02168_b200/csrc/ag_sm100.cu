@@ -42,6 +42,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -84,6 +85,7 @@ struct AgTcParams {
   const uint64_t* ready;  // [num_m][W] local board; nullptr: ungated
   uint64_t epoch;
   int gather;             // gather warps active (PULL)
+  int gather_own;         // PULL into a caller's gathered buffer: also place the own shard (placement check)
   __nv_bfloat16* inbox;   // local inbox, m x k
   uint64_t* ready_w;      // writable view of `ready` (gather)
   unsigned long long* events;  // event log (tf_world_set_events): [num_m][W] x {store, first load} %globaltimer
@@ -560,7 +562,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ===== gather (PULL): peer shard chunks -> local inbox + ready flags =====
     const int gt = threadIdx.x - 6 * 32;  // 0..GATHER_T-1
     __shared__ unsigned int s_chunk;
-    const unsigned total = unsigned(p.num_m) * p.W;
+    // Remote shards only: the TMA producer reads the rank's own k-range
+    // straight from its shard, so copying it into the inbox would be a
+    // wasted m x kw read + write per call.  A caller-supplied gathered
+    // buffer (placement check) gets the own shard too, last.
+    const int nsrc = p.W - 1 + p.gather_own;
+    const unsigned total = unsigned(p.num_m) * unsigned(nsrc);
     const int vec_per_row = p.kw / 8;  // 16-byte vectors per shard row
     for (;;) {
       if (gt == 0) s_chunk = atomicAdd(&p.ctr[0], 1u);
@@ -568,8 +575,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const unsigned c = s_chunk;
       named_bar(1, GATHER_T);
       if (c >= total) break;
-      const int mb = int(c / p.W);
-      const int src = (p.own + 1 + int(c % p.W)) % p.W;  // own shard last
+      const int mb = int(c / nsrc);
+      const int src = (p.own + 1 + int(c % nsrc)) % p.W;
       const int r0 = mb * BM, rows = min(BM, p.M - r0);
       const uint4* s = reinterpret_cast<const uint4*>(p.peer_shard[src] + size_t(r0) * p.kw);
       const int nvec = rows * vec_per_row;
@@ -933,8 +940,12 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
     }
     if (!lay.split_k) ks = 1;
     while (ks > 1) {
-      static int max_active[3][9] = {};
-      int& ma = max_active[shp.id][ks];
+      // Per (shape, split, device) occupancy cache; atomics so concurrent
+      // worlds on other host threads never race on it (a stale read only
+      // recomputes the same value).
+      static std::atomic<int> max_active[3][9][16];
+      std::atomic<int>& slot = max_active[shp.id][ks][dev & 15];
+      int ma = slot.load(std::memory_order_relaxed);
       if (ma == 0) {
         TFB_CUDA(cudaFuncSetAttribute(shp.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(shp.smem)));
         cudaLaunchConfig_t qc{};
@@ -952,6 +963,7 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
           cudaGetLastError();
           ma = -1;
         }
+        slot.store(ma, std::memory_order_relaxed);
       }
       if (ma > 0 && unsigned(tiles) <= unsigned(ma)) break;
       if (std::getenv("TFB_KSPLIT_FORCE")) break;
@@ -989,10 +1001,10 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   p.ldc = int(ldc);
   auto kern = shp->kern;
   const size_t smem = shp->smem;
-  static bool attr_set[3][64] = {};
-  if (!attr_set[shp->id][dev & 63]) {
+  static std::atomic<bool> attr_set[3][64];  // idempotent attribute, set once per (shape, device)
+  if (!attr_set[shp->id][dev & 63].load(std::memory_order_acquire)) {
     TFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr_set[shp->id][dev & 63] = true;
+    attr_set[shp->id][dev & 63].store(true, std::memory_order_release);
   }
   const unsigned pair_tiles = unsigned((p.num_m + CG - 1) / CG) * unsigned(p.num_n) * unsigned(p.ksplit);
   if (const char* e = std::getenv("TFB_GRID")) grid_cap = std::min(grid_cap, unsigned(std::atoi(e)));
@@ -1038,13 +1050,11 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   {
-    static int last_gm[64] = {};
+    // TFB_GROUP_M (profiling knob) lives in a __constant__ per device.
+    static std::atomic<int> last_gm[64];
     int gm = 0;
     if (const char* e = std::getenv("TFB_GROUP_M")) gm = std::atoi(e);
-    if (last_gm[dev & 63] != gm) {
-      TFB_CUDA(cudaMemcpyToSymbol(g_group_m, &gm, sizeof(int)));
-      last_gm[dev & 63] = gm;
-    }
+    if (last_gm[dev & 63].exchange(gm) != gm) TFB_CUDA(cudaMemcpyToSymbol(g_group_m, &gm, sizeof(int)));
   }
   // B as 4-D (64 columns, K rows, 4 chunks of a 256-column group, N/256
   // groups): one box (64, BK, CPH, NH) is a CTA's whole B stage.
@@ -1088,9 +1098,11 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
   const int num_m = int((m + BM - 1) / BM);
   const unsigned sms = unsigned(w->sm_count);
 
+  if (!lay.inbox_complete) w->record_ag(m, kw, 2);
   if (W == 1) {
     // No exchange: the fused kernel degenerates to the GEMM over the shard.
     if (!w->ranks[0].local) return TF_OK;
+    if (!lay.inbox_complete) w->ag_src[0][0] = {a_shard[0], kw};
     AgTcParams proto{};
     TFB_CHECK(launch_skew(w, 0, streams[0]));
     TFB_CHECK(launch_gemm(w, 0, sh, a_shard[0], nullptr, b[0], c[0], nullptr, 0, 0, 0, proto,
@@ -1121,6 +1133,12 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
     if (gathered && gathered[r]) return static_cast<__nv_bfloat16*>(gathered[r]);
     return reinterpret_cast<__nv_bfloat16*>(w->ptr(r, inbox_off)) + size_t(parity) * m * k;
   };
+  if (!lay.inbox_complete)
+    for (int r = 0; r < W; ++r)
+      for (int s = 0; s < W; ++s)
+        w->ag_src[r][s] = (variant == TF_AG_PULL && s == r && !(gathered && gathered[r]))
+                              ? World::AgBlock{a_shard[r], kw}  // read in place by the TMA producer
+                              : World::AgBlock{inbox_of(r) + size_t(s) * kw, k};
   auto ready_of = [&](int r) { return reinterpret_cast<uint64_t*>(w->ptr(r, rb.offset)); };
   auto ctr_of = [&](int r, int slot) { return reinterpret_cast<unsigned int*>(w->ptr(r, ctr_off)) + slot * 4; };
   // Event log (tf_world_set_events; debug, untimed): per (m-block, source)
@@ -1190,6 +1208,7 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
       AgTcParams proto{};
       for (int s = 0; s < W; ++s) proto.peer_shard[s] = static_cast<const __nv_bfloat16*>(a_shard[s]);
       proto.inbox = inbox_of(r);
+      proto.gather_own = (gathered && gathered[r]) ? 1 : 0;
       proto.ready_w = ready_of(r);
       proto.ctr = ctr_of(r, 0);
       proto.events = events_of(r);
@@ -1200,6 +1219,12 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
     return TF_OK;
   }
 
+  // PUSH into caller-supplied gathered buffers (single, not parity-buffered
+  // like the internal inbox): a world barrier first, so no peer stores into
+  // a buffer whose owner may still be reading it from its previous run.
+  bool caller = false;
+  for (int r = 0; r < W && gathered; ++r) caller |= gathered[r] != nullptr;
+  if (caller) TFB_CHECK(world_barrier(w, streams));
   // PUSH: producers first on the side streams (they never wait), then the
   // gated GEMMs with a few SMs left for the producers.  Ranks sharing a
   // device (loopback) split its SMs: every rank's GEMM and producer CTAs

@@ -11,7 +11,8 @@
 
 namespace tfb {
 
-// One record per world, in host-mapped pinned memory.  The first failing
+// One record per device of a world, in device memory (cheap for spinning
+// kernels to poll; the host reads it after a sync).  The first failing
 // thread wins the CAS on `code`; everyone else spinning sees code != 0 and
 // bails out (the device analogue of World::abort, fabric.hpp:352-363).
 struct DevErr {

@@ -43,10 +43,13 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 
+#include "sm100.cuh"
 #include "world.hpp"
 
 namespace tfb {
@@ -102,8 +105,30 @@ struct FdParams {
   unsigned long long* trace;  // TFB_TRACE: [grid][16] %globaltimer stamps per CTA (else null)
   float* inbox_all[64];       // every rank's inbox (this parity), this process' view
   uint64_t* flags_all[64];    // every rank's flag board
+  // TMA-fed split kernel (fd_stream_kernel): host-built item table of ONE
+  // rank, entry = {g, split j, first key, end key} (item i of the launch is
+  // table entry i / nlocal of local rank i % nlocal); per group split count;
+  // per (lr, g) fold claim state (0 free, 1 folded inline by the last
+  // split's CTA, 2 taken by the fold phase; reset by the last CTA).
+  const uint4* items;
+  unsigned nitems;
+  const int* gS;
+  unsigned* fstate;
   FdRank r[kMaxLocal];
 };
+
+__device__ __forceinline__ int split_count(const FdParams& P, int lr, int g) {
+  (void)lr;  // every rank cuts the same splits
+  return P.gS ? P.gS[g] : P.S;
+}
+
+__device__ __forceinline__ void consumer_bar() {  // the 8 consumer warps of fd_stream_kernel
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+__device__ __forceinline__ void cta_bar(bool named) {
+  if (named) consumer_bar();
+  else __syncthreads();
+}
 
 // ---- combine monoid on wire rows (tilemath.hpp:186-220) -------------------
 // One implementation for every fold so all schedules agree bit for bit.
@@ -758,18 +783,22 @@ __device__ __forceinline__ float4 ldcg4(const float* p) {
 // pushing, else the published partial) and, W = 1 fused (`direct`), the
 // finalized output o / l (tilemath.hpp:225-239) -- bitwise what fold_group
 // would compute from the single source.
+// Eight warps do the work (a 9-warp fd_stream_kernel block: warp 8 only
+// joins the barriers); `named`: the caller is the consumer warps alone.
 template <int EL, int RB>
 __device__ __forceinline__ void fold_heads(const FdParams& P, int lr, int g, int h0, int hc, float* s_wm,
-                                        float* s_L, float* s_O) {
-  const int d = P.d, wrl = ws_row(d), gs = P.gs, S = P.S, W = P.W, Hq = P.Hq, Hkv = P.Hkv, row_len = d + 2;
-  const int G = P.B * Hkv;
+                                        float* s_L, float* s_O, bool named = false) {
+  const int G = P.B * P.Hkv;
+  const int d = P.d, wrl = ws_row(d), gs = P.gs, S = split_count(P, lr, g), W = P.W, Hq = P.Hq, Hkv = P.Hkv,
+            row_len = d + 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool act = warp < 8;
   const int rank = P.r[lr].rank;
   const int direct = P.direct, push = P.push, out_bf16 = P.out_bf16;
   void* const out = P.r[lr].out;
   float* const pub = P.r[lr].pub;
   const int b = g / Hkv, kvh = g % Hkv;
-  const float* grp = P.ws + ((size_t(lr) * G + g) * S) * gs * wrl;
+  const float* grp = P.ws + ((size_t(lr) * G + g) * P.S) * gs * wrl;  // P.S: the layout's row stride
   const size_t base_src = size_t(rank) * P.B * Hq * row_len;
   const int wph = hc >= 8 ? 1 : 8 / hc;
   // Fold rows r0, r0 + step, ... of head h into (L, O[EL]) with max M.
@@ -882,6 +911,7 @@ __device__ __forceinline__ void fold_heads(const FdParams& P, int lr, int g, int
   };
   if (wph == 1) {
     // Whole heads per warp.
+    if (!act) return;
     for (int hh = warp; hh < hc; hh += 8) {
       const int h = h0 + hh;
       float L, O[EL], M;
@@ -904,26 +934,28 @@ __device__ __forceinline__ void fold_heads(const FdParams& P, int lr, int g, int
   // partials in ascending warp order: M = max m_w, L = sum L_w e^(m_w - M),
   // O = sum O_w e^(m_w - M).
   const int hh = warp / wph, j = warp % wph, h = h0 + hh;
-  float L, O[EL], Mw;
-  if ((S + wph - 1) / wph <= RB) {
-    float v[RB][EL];
-    float2 ml[RB];
-    one_batch(h, j, wph, v, ml);
-    Mw = batch_max(ml);
-    sum_batch(v, ml, Mw, L, O);
-  } else {
-    Mw = row_max(h, j, wph);
-    fold_rows(h, j, wph, Mw, L, O);
-  }
-  if (lane == 0) {
-    s_wm[warp] = Mw;
-    s_L[warp] = L;
-  }
+  if (act) {
+    float L, O[EL], Mw;
+    if ((S + wph - 1) / wph <= RB) {
+      float v[RB][EL];
+      float2 ml[RB];
+      one_batch(h, j, wph, v, ml);
+      Mw = batch_max(ml);
+      sum_batch(v, ml, Mw, L, O);
+    } else {
+      Mw = row_max(h, j, wph);
+      fold_rows(h, j, wph, Mw, L, O);
+    }
+    if (lane == 0) {
+      s_wm[warp] = Mw;
+      s_L[warp] = L;
+    }
 #pragma unroll
-  for (int x = 0; x < EL; ++x)
-    if (lane + 32 * x < d) s_O[warp * d + lane + 32 * x] = O[x];
-  __syncthreads();
-  if (j == 0) {
+    for (int x = 0; x < EL; ++x)
+      if (lane + 32 * x < d) s_O[warp * d + lane + 32 * x] = O[x];
+  }
+  cta_bar(named);
+  if (act && j == 0) {
     float M = -INFINITY;
     for (int y = 0; y < wph; ++y)
       if (s_L[warp + y] != 0.0f) M = fmaxf(M, s_wm[warp + y]);
@@ -941,67 +973,31 @@ __device__ __forceinline__ void fold_heads(const FdParams& P, int lr, int g, int
     }
     emit(h, M, LL, OO);
   }
-  __syncthreads();
+  cta_bar(named);
 }
 
-// ---- the persistent kernel ------------------------------------------------
-// MODE: 0 generic split, 1 fast split with bf16 P, 2 fast split with hi/lo P.
-template <int MODE>
-__global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __grid_constant__ FdParams P) {
-  __shared__ unsigned int s_item;
-  __shared__ int s_last, s_src;
-  __shared__ FastSmem fsm;
-  __shared__ float s_wm[8], s_fL[8], s_fO[8 * 256];
+// The phases after the splits are computed (both attention kernels):
+// split-fold sub-items -> push + flags -> cross-rank fold (fused) ->
+// owner-combine collection, then the last CTA resets the per-launch counts.
+// Every thread of the block calls it; eight warps do fold work.
+struct PostShared {
+  unsigned* item;
+  int* last;
+  int* src;
+  float *wm, *fL, *fO;
+};
+__device__ __noinline__ void fd_post_phases(const FdParams& P, unsigned ranks_mask, unsigned long long* tr,
+                                            PostShared sh) {
+  unsigned& s_item = *sh.item;
+  int& s_last = *sh.last;
+  int& s_src = *sh.src;
+  float* s_wm = sh.wm;
+  float* s_fL = sh.fL;
+  float* s_fO = sh.fO;
   const int G = P.B * P.Hkv;
-  const unsigned total = unsigned(P.nlocal) * G * P.S;
-  const int d = P.d, row_len = d + 2, wrl = ws_row(d);
-  unsigned long long* tr = P.trace ? P.trace + size_t(blockIdx.x) * 16 : nullptr;
   auto stamp = [&](int i) {
     if (tr && threadIdx.x == 0) tr[i] = globaltimer_ns();
   };
-  stamp(0);
-  unsigned ranks_mask = 0;  // local ranks this CTA computed for
-  __shared__ unsigned long long s_t0;  // CTA entry time (straggler model)
-  if (threadIdx.x == 0) s_t0 = globaltimer_ns();
-  if (tr && threadIdx.x == 0)
-    for (int i = 1; i < 16; ++i)
-      if (i != 12 && i != 13) tr[i] = 0;
-  for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(&P.ctr[0], 1u);
-    __syncthreads();
-    const unsigned item = s_item;
-    __syncthreads();
-    if (item >= total) break;
-    const int sp = item % P.S;
-    const int g = (item / P.S) % G;
-    const int lr = item / (unsigned(P.S) * G);
-    ranks_mask |= 1u << lr;
-    if (P.r[lr].skew_ns) {  // straggler model: this rank's compute starts late
-      if (threadIdx.x == 0)
-        while (globaltimer_ns() - s_t0 < P.r[lr].skew_ns) __nanosleep(1000);
-      __syncthreads();
-    }
-    float* grp = P.ws + ((size_t(lr) * G + g) * P.S) * P.gs * wrl;
-    float* wsrow = grp + size_t(sp) * P.gs * wrl;
-    if (MODE == 2) fast_split<true>(P, lr, g, sp, wsrow, fsm);
-    else if (MODE == 1) fast_split<false>(P, lr, g, sp, wsrow, fsm);
-    else generic_split(P, lr, g, sp, wsrow);
-    stamp(1);
-    if (tr && threadIdx.x == 0) {
-      unsigned smid;
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      tr[14] = smid;
-      tr[15] = item;
-    }
-    // Publish the split: bar.sync orders every thread's ws stores before
-    // thread 0's release (cumulative), which the split-fold acquires.
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();  // every thread's ws rows (ordered by the barrier) before the count
-      red_release_gpu(P.done + size_t(lr) * G + g, 1);
-    }
-  }
-  stamp(2);
   // Split-fold phase: sub-items (group, hc heads) of every local rank this
   // CTA computed for, each waiting for its group's S splits.  Every compute
   // item has been claimed by a CTA that never blocks before publishing it,
@@ -1032,7 +1028,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
         // Intra-rank completion counter: a local spin, not a fabric signal
         // (not counted as a signal wait in the tax meter).
         const uint64_t* c = P.done + size_t(lr) * G + g;
-        const uint64_t want = uint64_t(P.S);
+        const uint64_t want = uint64_t(split_count(P, lr, g));
         const uint64_t t0 = globaltimer_ns();
         int ok = 1;
         for (unsigned polls = 0; ld_acquire_gpu(c) < want; ++polls) {
@@ -1048,9 +1044,13 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
             }
           }
         }
+        // A group the stream kernel already folded inline (its last split's
+        // CTA, while compute items remained) is skipped here.
+        if (ok && P.fstate && atomicCAS(&P.fstate[size_t(lr) * G + g], 0u, 2u) == 1u) ok = 2;
         s_last = ok;
       }
       __syncthreads();
+      if (s_last == 2) continue;
       if (!s_last) break;  // an error elsewhere (e.g. NumericError) ends the launch
       stamp(9);
       if (P.d <= 128) fold_heads<4, 8>(P, lr, g, hb * P.hc, P.hc, s_wm, s_fL, s_fO);
@@ -1158,6 +1158,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       P.done[i] = 0;
       P.gtick[i] = 0;
+      if (P.fstate) P.fstate[i] = 0;
     }
     if (threadIdx.x == 0) {
       P.ctr[0] = 0;
@@ -1168,6 +1169,460 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
     }
     __threadfence();
   }
+}
+
+// ---- the persistent kernel ------------------------------------------------
+// MODE: 0 generic split, 1 fast split with bf16 P, 2 fast split with hi/lo P.
+template <int MODE>
+__global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __grid_constant__ FdParams P) {
+  __shared__ unsigned int s_item;
+  __shared__ int s_last, s_src;
+  __shared__ FastSmem fsm;
+  __shared__ float s_wm[8], s_fL[8], s_fO[8 * 256];
+  const int G = P.B * P.Hkv;
+  const unsigned total = unsigned(P.nlocal) * G * P.S;
+  const int d = P.d, row_len = d + 2, wrl = ws_row(d);
+  unsigned long long* tr = P.trace ? P.trace + size_t(blockIdx.x) * 16 : nullptr;
+  auto stamp = [&](int i) {
+    if (tr && threadIdx.x == 0) tr[i] = globaltimer_ns();
+  };
+  stamp(0);
+  unsigned ranks_mask = 0;  // local ranks this CTA computed for
+  __shared__ unsigned long long s_t0;  // CTA entry time (straggler model)
+  if (threadIdx.x == 0) s_t0 = globaltimer_ns();
+  if (tr && threadIdx.x == 0)
+    for (int i = 1; i < 16; ++i)
+      if (i != 12 && i != 13) tr[i] = 0;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(&P.ctr[0], 1u);
+    __syncthreads();
+    const unsigned item = s_item;
+    __syncthreads();
+    if (item >= total) break;
+    const int sp = item % P.S;
+    const int g = (item / P.S) % G;
+    const int lr = item / (unsigned(P.S) * G);
+    ranks_mask |= 1u << lr;
+    if (P.r[lr].skew_ns) {  // straggler model: this rank's compute starts late
+      if (threadIdx.x == 0)
+        while (globaltimer_ns() - s_t0 < P.r[lr].skew_ns) __nanosleep(1000);
+      __syncthreads();
+    }
+    float* grp = P.ws + ((size_t(lr) * G + g) * P.S) * P.gs * wrl;
+    float* wsrow = grp + size_t(sp) * P.gs * wrl;
+    if (MODE == 2) fast_split<true>(P, lr, g, sp, wsrow, fsm);
+    else if (MODE == 1) fast_split<false>(P, lr, g, sp, wsrow, fsm);
+    else generic_split(P, lr, g, sp, wsrow);
+    stamp(1);
+    if (tr && threadIdx.x == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      tr[14] = smid;
+      tr[15] = item;
+    }
+    // Publish the split: bar.sync orders every thread's ws stores before
+    // thread 0's release (cumulative), which the split-fold acquires.
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();  // every thread's ws rows (ordered by the barrier) before the count
+      red_release_gpu(P.done + size_t(lr) * G + g, 1);
+    }
+  }
+  stamp(2);
+  fd_post_phases(P, ranks_mask, tr, PostShared{&s_item, &s_last, &s_src, s_wm, s_fL, s_fO});
+}
+
+// ---- TMA-fed split partials (bf16 K/V, d = 128, 8 q-heads per KV head) ----
+// One CTA per SM, 9 warps.  Warp 8 (one lane) is the producer: it claims
+// items (a split of a group: keys [k0, k1) of one KV stream) from a global
+// counter, in the order of a host-built table, and streams each item's K and
+// V through a kStreamStages-deep shared-memory ring with TMA
+// (cp.async.bulk.tensor, 64 keys x 128 d of K and of V per stage, 128-byte
+// swizzle) plus the group's 8 q rows with a 1-D bulk copy on the item's
+// first stage.  Warps 0-7 consume: warp c takes 16-key tile (c & 3) of every
+// stage whose sequence number has parity c >> 2, so each warp's tiles of an
+// item are a fixed set (the partial is schedule-independent, bitwise).  The
+// math is the register decode of fast_warp_range, fed from smem: S^T =
+// K.Q^T with mma.m16n8k16 over ldmatrix'd K, exp2-domain online softmax with
+// warp-shuffle max/sum, O^T += V^T.P^T with ldmatrix.trans'd V.  When the
+// stage sequence moves to the next item the 8 warps merge their partials
+// (max first, ascending warp order) into the item's split row and publish
+// it while the producer keeps the ring full; the CTA that completes a
+// group's last split while items remain folds the whole group right there
+// (fold claim), so only the last groups' folds are left for the tail.
+constexpr int kStreamStages = 4;
+constexpr int kStreamConsumers = 8;
+constexpr int kStreamThreads = 32 * (kStreamConsumers + 1);
+constexpr int kStageKV = 2 * 64 * 128 * 2;  // K + V of 64 keys, bf16
+constexpr int kORow = 132;                   // padded merge row (conflict-free stores)
+
+struct FdMaps {
+  CUtensorMap k[kMaxLocal];  // per local rank: [B*Hkv*len keys][2 halves][64 d] bf16 view, box 64 x 64 x 2
+  CUtensorMap v[kMaxLocal];
+};
+
+struct StreamSmem {
+  uint8_t kv[kStreamStages][kStageKV];  // 1024-aligned: [K half0 | K half1 | V half0 | V half1], 8 KB each
+  uint8_t q[kStreamStages][8 * 128 * 2];
+  float o[kStreamConsumers][8 * kORow];
+  float m[kStreamConsumers][8], l[kStreamConsumers][8], wa[8][kStreamConsumers];
+  float hm[8], hl[8];
+  int meta[kStreamStages][4];  // item (-1: end), keys in stage, lr << 24 | g, split j
+  uint64_t full[kStreamStages], empty[kStreamStages];
+  int bad, inline_fold;
+  unsigned ranks_mask;
+};
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(sm100::smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(sm100::smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   sm100::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(sm100::smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+               : "r"(addr));
+}
+// Zero the bf16 halves of a V^T fragment register whose key is >= n.
+__device__ __forceinline__ uint32_t mask_keys(uint32_t x, int key_lo, int n) {
+  return (key_lo < n ? (x & 0xffffu) : 0u) | (key_lo + 1 < n ? (x & 0xffff0000u) : 0u);
+}
+
+// Producer: lane 0 of warp kStreamConsumers.
+__device__ void stream_producer(const FdParams& P, const FdMaps& M, StreamSmem& sm) {
+  const int G = P.B * P.Hkv;
+  unsigned seq = 0, skewed = 0;
+  const uint64_t t0 = globaltimer_ns();
+  for (;;) {
+    const unsigned it = atomicAdd(&P.ctr[0], 1u);
+    const bool end = it >= P.nitems;
+    const int lr = end ? 0 : int(it % unsigned(P.nlocal));
+    uint4 e = end ? make_uint4(0, 0, 0, 0) : P.items[it / unsigned(P.nlocal)];
+    e.x |= unsigned(lr) << 24;
+    const int g = int(e.x & 0xffffffu);
+    const int b = g / P.Hkv, kvh = g % P.Hkv;
+    const unsigned row0 = unsigned(g) * unsigned(P.len);  // [B][Hkv][len] rows: (b * Hkv + kvh) * len
+    if (!end && P.r[lr].skew_ns && !((skewed >> lr) & 1u)) {  // straggler model: the rank starts late
+      while (globaltimer_ns() - t0 < P.r[lr].skew_ns) __nanosleep(1000);
+      skewed |= 1u << lr;
+    }
+    for (unsigned key = e.z;; key += 64) {
+      if (!end && key >= e.w) break;
+      const int st = int(seq % kStreamStages);
+      sm100::mbar_wait(&sm.empty[st], ((seq / kStreamStages) & 1u) ^ 1u);
+      volatile int* mt = sm.meta[st];
+      mt[0] = end ? -1 : int(it);
+      mt[1] = end ? 0 : int(min(64u, e.w - key));
+      mt[2] = int(e.x);
+      mt[3] = int(e.y);
+      ++seq;
+      if (end) {
+        sm100::mbar_arrive(&sm.full[st]);
+        return;
+      }
+      const bool first = key == e.z;
+      sm100::mbar_arrive_expect_tx(&sm.full[st], kStageKV + (first ? 2048u : 0u));
+      tma_load_3d(sm.kv[st], &M.k[lr], &sm.full[st], 0, int(row0 + key), 0);
+      tma_load_3d(sm.kv[st] + kStageKV / 2, &M.v[lr], &sm.full[st], 0, int(row0 + key), 0);
+      if (first)
+        bulk_load(sm.q[st], static_cast<const __nv_bfloat16*>(P.r[lr].q) + (size_t(b) * P.Hq + kvh * 8) * 128, 2048,
+                  &sm.full[st]);
+    }
+    (void)G;
+  }
+}
+
+// The 8 consumer warps' partials of one item -> its split row (ws), then the
+// split is published; returns (to every consumer thread) whether this CTA
+// folds the group inline.
+__device__ __forceinline__ void stream_finish_item(const FdParams& P, StreamSmem& sm, int lrg, int j, float m0,
+                                                   float m1, float l0, float l1, const float (&o)[8][4], int badl) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, t = lane & 3;
+  const int G = P.B * P.Hkv;
+  const int lr = lrg >> 24, g = lrg & 0xffffff;
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+  }
+  if (gq == 0) {
+    sm.m[warp][2 * t] = m0;
+    sm.m[warp][2 * t + 1] = m1;
+    sm.l[warp][2 * t] = l0;
+    sm.l[warp][2 * t + 1] = l1;
+  }
+  float* ow = sm.o[warp];
+#pragma unroll
+  for (int db = 0; db < 8; ++db) {
+    const int dA = 16 * db + gq;
+    ow[(2 * t) * kORow + dA] = o[db][0];
+    ow[(2 * t + 1) * kORow + dA] = o[db][1];
+    ow[(2 * t) * kORow + dA + 8] = o[db][2];
+    ow[(2 * t + 1) * kORow + dA + 8] = o[db][3];
+  }
+  if (badl) sm.bad = 1;
+  consumer_bar();
+  // Max-first fold of the warp partials (log2 domain), ascending warp order
+  // (the fold of fast_split): per head M = max m_w over warps with l_w != 0.
+  if (threadIdx.x < 8) {
+    const int h = threadIdx.x;
+    float Mx = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kStreamConsumers; ++w)
+      if (sm.l[w][h] != 0.0f) Mx = fmaxf(Mx, sm.m[w][h]);
+    float L = 0.0f;
+#pragma unroll
+    for (int w = 0; w < kStreamConsumers; ++w) {
+      const float bl = sm.l[w][h];
+      const float a = bl != 0.0f ? exp2f(sm.m[w][h] - Mx) : 0.0f;
+      sm.wa[h][w] = a;
+      L = __fadd_rn(L, __fmul_rn(bl, a));
+    }
+    sm.hm[h] = Mx;
+    sm.hl[h] = L;
+  }
+  consumer_bar();
+  const int wrl = ws_row(128);
+  float* wsrow = P.ws + ((size_t(lr) * G + g) * P.S + j) * 8 * wrl;
+  for (int e = threadIdx.x; e < 8 * 128; e += 32 * kStreamConsumers) {
+    const int h = e >> 7, dd = e & 127;
+    float acc = 0.0f;
+#pragma unroll
+    for (int w = 0; w < kStreamConsumers; ++w) {
+      const float a = sm.wa[h][w];
+      acc = __fadd_rn(acc, a != 0.0f ? __fmul_rn(sm.o[w][h * kORow + dd], a) : 0.0f);
+    }
+    float* row = wsrow + size_t(h) * wrl;
+    if (dd == 0) {
+      row[0] = sm.hm[h] * kLn2;
+      row[1] = sm.hl[h];
+    }
+    row[kWsO + dd] = acc;
+  }
+  consumer_bar();
+  if (threadIdx.x == 0) {
+    if (sm.bad) {
+      raise_err(P.err, TF_ERR_NUMERIC, kNumeric, P.r[lr].rank, -1, 0, 0, 0, 0,
+                (uint64_t((g % P.Hkv) * 8) << 32) | uint64_t(size_t(P.r[lr].rank) * P.len));
+      sm.bad = 0;
+    }
+    sm.ranks_mask |= 1u << lr;
+    // Publish (release: every consumer's ws stores, ordered by the barrier)
+    // and take the group's completion ticket in one RMW: the CTA whose split
+    // completes the group sees every other split (acquire).
+    __threadfence();
+    const uint64_t before = atom_add_acq_rel_gpu(reinterpret_cast<unsigned long long*>(P.done + size_t(lr) * G + g), 1ull);
+    int fold = 0;
+    if (before + 1 == uint64_t(split_count(P, lr, g)) && P.fstate &&
+        *reinterpret_cast<volatile unsigned*>(&P.ctr[0]) < P.nitems)  // items left: fold now, off the tail
+      fold = atomicCAS(&P.fstate[size_t(lr) * G + g], 0u, 1u) == 0u;
+    sm.inline_fold = fold;
+  }
+  consumer_bar();
+}
+
+// Inline group fold by the consumer warps (split rows -> the rank's wire
+// rows / direct output, then the group's flags) -- the sub-item fold of
+// fd_post_phases for all gs heads at once.
+__device__ void stream_fold_group(const FdParams& P, int lr, int g, float* s_wm, float* s_fL, float* s_fO) {
+  fold_heads<4, 8>(P, lr, g, 0, P.gs, s_wm, s_fL, s_fO, /*named=*/true);
+  const int G = P.B * P.Hkv;
+  const FdRank& R = P.r[lr];
+  consumer_bar();
+  if (!P.push) return;
+  if (threadIdx.x == 0) {
+    if (!P.direct) {
+      if (P.local_dst == (P.W >= 64 ? ~0ull : ((1ull << P.W) - 1))) __threadfence();
+      else __threadfence_system();
+    }
+  }
+  consumer_bar();
+  if (threadIdx.x < P.W && (!P.owner || int(threadIdx.x) == g % P.W)) {
+    uint64_t* f = P.flags_all[threadIdx.x] + size_t(R.rank) * G + g;
+    if (P.events_all[threadIdx.x]) P.events_all[threadIdx.x][(size_t(R.rank) * G + g) * 2] = globaltimer_ns();
+    if (P.direct) atomicAdd(reinterpret_cast<unsigned long long*>(f), 1ull);
+    else if ((P.local_dst >> threadIdx.x) & 1ull) red_release_gpu(f, 1);
+    else red_release_sys(f, 1);
+  }
+}
+
+template <bool HILO>
+__device__ void stream_consumer(const FdParams& P, StreamSmem& sm, float* s_wm, float* s_fL, float* s_fO) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, t = lane & 3;
+  const int tl = warp & 3;
+  const unsigned sel = unsigned(warp >> 2);
+  const float sl2 = P.scale * kLog2e;
+  // Lane-constant parts of the ldmatrix addresses (128-byte swizzle: the
+  // 16-byte chunk index is XORed with the key row's low 3 bits).
+  const uint32_t krow = uint32_t(tl * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * 128;
+  const uint32_t vrow = uint32_t(tl * 16 + (lane & 7) + ((lane >> 4) & 1) * 8) * 128;
+  const int khi = lane >> 4, vhi = (lane >> 3) & 1, sw = lane & 7;
+  int cur = -1, cur_lrg = 0, cur_j = 0;
+  float o[8][4];
+  uint32_t qb[8][2];
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
+  int badl = 0;
+  for (unsigned seq = 0;; ++seq) {
+    const int st = int(seq % kStreamStages);
+    sm100::mbar_wait(&sm.full[st], (seq / kStreamStages) & 1u);
+    const volatile int* mt = sm.meta[st];
+    const int item = mt[0], nk = mt[1], lrg = mt[2], j = mt[3];
+    if (item != cur) {
+      if (cur >= 0) {
+        stream_finish_item(P, sm, cur_lrg, cur_j, m0, m1, l0, l1, o, badl);
+        if (sm.inline_fold) stream_fold_group(P, cur_lrg >> 24, cur_lrg & 0xffffff, s_wm, s_fL, s_fO);
+      }
+      if (item < 0) {
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&sm.empty[st]);
+        break;
+      }
+      cur = item;
+      cur_lrg = lrg;
+      cur_j = j;
+      const uint32_t* qs = reinterpret_cast<const uint32_t*>(sm.q[st]);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        qb[kk][0] = qs[gq * 64 + 8 * kk + t];
+        qb[kk][1] = qs[gq * 64 + 8 * kk + 4 + t];
+      }
+#pragma unroll
+      for (int x = 0; x < 8; ++x) o[x][0] = o[x][1] = o[x][2] = o[x][3] = 0.0f;
+      m0 = m1 = -INFINITY;
+      l0 = l1 = 0.0f;
+      badl = 0;
+    }
+    const int n = nk - tl * 16;  // valid keys of this warp's tile
+    if ((seq & 1u) == sel && n > 0) {
+      const uint32_t kb = sm100::smem_u32(sm.kv[st]), vb = kb + kStageKV / 2;
+      float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4(kb + (kk >> 2) * 8192 + krow + ((((2 * kk + khi) & 7) ^ sw) << 4), a0, a1, a2, a3);
+        mma_bf16(s, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+      }
+      const bool va = gq < n, vbk = gq + 8 < n;
+      const float x0 = va ? s[0] * sl2 : -INFINITY, x1 = va ? s[1] * sl2 : -INFINITY;
+      const float x2 = vbk ? s[2] * sl2 : -INFINITY, x3 = vbk ? s[3] * sl2 : -INFINITY;
+      badl |= (va && !(fabsf(x0) < INFINITY && fabsf(x1) < INFINITY)) ||
+              (vbk && !(fabsf(x2) < INFINITY && fabsf(x3) < INFINITY));
+      float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+      }
+      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+      const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);
+      m0 = mn0;
+      m1 = mn1;
+      const float e0 = exp2f(x0 - mn0), e1 = exp2f(x1 - mn1);
+      const float e2 = exp2f(x2 - mn0), e3 = exp2f(x3 - mn1);
+      const __nv_bfloat162 p01 = __floats2bfloat162_rn(e0, e1);
+      const __nv_bfloat162 p23 = __floats2bfloat162_rn(e2, e3);
+      __nv_bfloat162 r01, r23;
+      if (HILO) {
+        r01 = __floats2bfloat162_rn(e0 - __low2float(p01), e1 - __high2float(p01));
+        r23 = __floats2bfloat162_rn(e2 - __low2float(p23), e3 - __high2float(p23));
+        l0 = l0 * al0 + (e0 + e2);
+        l1 = l1 * al1 + (e1 + e3);
+      } else {
+        l0 = l0 * al0 + (__low2float(p01) + __low2float(p23));
+        l1 = l1 * al1 + (__high2float(p01) + __high2float(p23));
+      }
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        o[x][0] *= al0;
+        o[x][1] *= al1;
+        o[x][2] *= al0;
+        o[x][3] *= al1;
+      }
+      const uint32_t pb0 = movtrans(*reinterpret_cast<const uint32_t*>(&p01));
+      const uint32_t pb1 = movtrans(*reinterpret_cast<const uint32_t*>(&p23));
+      uint32_t rb0 = 0, rb1 = 0;
+      if (HILO) {
+        rb0 = movtrans(*reinterpret_cast<const uint32_t*>(&r01));
+        rb1 = movtrans(*reinterpret_cast<const uint32_t*>(&r23));
+      }
+#pragma unroll
+      for (int db = 0; db < 8; ++db) {
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4_t(vb + (db >> 2) * 8192 + vrow + ((((2 * db + vhi) & 7) ^ sw) << 4), a0, a1, a2, a3);
+        if (n < 16) {  // keys past the item: P is 0 there, and V must not be Inf/NaN either
+          a0 = mask_keys(a0, 2 * t, n);
+          a1 = mask_keys(a1, 2 * t, n);
+          a2 = mask_keys(a2, 8 + 2 * t, n);
+          a3 = mask_keys(a3, 8 + 2 * t, n);
+        }
+        mma_bf16(o[db], a0, a1, a2, a3, pb0, pb1);
+        if (HILO) mma_bf16(o[db], a0, a1, a2, a3, rb0, rb1);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) sm100::mbar_arrive(&sm.empty[st]);
+  }
+}
+
+template <bool HILO>
+__global__ void __launch_bounds__(kStreamThreads, 1)
+    fd_stream_kernel(const __grid_constant__ FdParams P, const __grid_constant__ FdMaps M) {
+  extern __shared__ uint8_t fd_smem_raw[];
+  StreamSmem& sm = *reinterpret_cast<StreamSmem*>((reinterpret_cast<uintptr_t>(fd_smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ unsigned int s_item;
+  __shared__ int s_last, s_src;
+  __shared__ float s_wm[8], s_fL[8], s_fO[8 * 256];
+  unsigned long long* tr = P.trace ? P.trace + size_t(blockIdx.x) * 16 : nullptr;
+  if (tr && threadIdx.x == 0) {
+    tr[0] = globaltimer_ns();
+    for (int i = 1; i < 16; ++i) tr[i] = 0;
+  }
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStreamStages; ++i) {
+      sm100::mbar_init(&sm.full[i], 1);
+      sm100::mbar_init(&sm.empty[i], kStreamConsumers);
+    }
+    sm.bad = 0;
+    sm.ranks_mask = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x == 32 * kStreamConsumers) {
+    for (int i = 0; i < P.nlocal; ++i) {
+      sm100::tma_prefetch(&M.k[i]);
+      sm100::tma_prefetch(&M.v[i]);
+    }
+  }
+  __syncthreads();
+  if (warp == kStreamConsumers) {
+    if ((threadIdx.x & 31) == 0) stream_producer(P, M, sm);
+  } else {
+    stream_consumer<HILO>(P, sm, s_wm, s_fL, s_fO);
+    if (tr && threadIdx.x == 0) tr[1] = globaltimer_ns();
+  }
+  __syncthreads();
+  if (tr && threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tr[14] = smid;
+    tr[2] = globaltimer_ns();
+  }
+  fd_post_phases(P, sm.ranks_mask, tr, PostShared{&s_item, &s_last, &s_src, s_wm, s_fL, s_fO});
 }
 
 // Push this rank's published rows into every inbox slot `self` and signal
@@ -1261,6 +1716,96 @@ static int choose_splits(const tf_fd_shape& s, size_t len, int sms) {
   return int(S);
 }
 
+// ---- fd_stream_kernel host side ------------------------------------------
+using FdEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static FdEncodeFn fd_encode_fn() {
+  static std::atomic<FdEncodeFn> fn{nullptr};
+  FdEncodeFn f = fn.load();
+  if (!f) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      f = reinterpret_cast<FdEncodeFn>(p);
+    fn.store(f);
+  }
+  return f;
+}
+
+// K or V of one rank, [rows = B * Hkv * len][128] bf16, viewed as
+// (64 d, rows, 2 halves) with strides (2 B, 256 B, 128 B): a box of
+// (64, 64, 2) lands in smem as [half][64 keys][128 B], swizzled by 128 B, so
+// ldmatrix reads 8 key rows of one 16-byte d chunk conflict-free.
+static tf_status fd_kv_map(CUtensorMap* m, const void* base, size_t rows) {
+  FdEncodeFn enc = fd_encode_fn();
+  if (!enc) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {64, rows, 2};
+  cuuint64_t strides[2] = {256, 128};
+  cuuint32_t box[3] = {64, 64, 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled (flash decode K/V) failed (" + std::to_string(int(r)) + ")");
+  return TF_OK;
+}
+
+// Item table of fd_stream_kernel: a fixed function of the shape and the
+// grid, so every run cuts the same splits (bitwise-reproducible partials
+// whatever CTA computes them).  Guided sizes: each item takes
+// remaining/grid keys (rounded up to 64, at least min_keys), the (rank,
+// group) streams taking turns, so the first items are each about a CTA's
+// fair share and the last ones are small -- CTAs that claim dynamically
+// finish within about one small item of each other.
+struct FdPlan {
+  std::vector<uint4> items;
+  std::vector<int> gS;
+  int S_max = 1;
+};
+static FdPlan fd_plan(int G, size_t len, unsigned grid) {
+  const int nlocal = 1;
+  FdPlan pl;
+  size_t min_keys = 256;
+  if (const char* e = std::getenv("TFB_FD_MINKEYS")) min_keys = std::max<size_t>(64, std::strtoull(e, nullptr, 10));
+  const bool group_major = std::getenv("TFB_FD_GROUP_MAJOR") != nullptr;
+  const size_t ng = size_t(nlocal) * G;
+  pl.gS.assign(ng, 0);
+  std::vector<size_t> pos(ng, 0);
+  size_t rem = ng * len;
+  size_t gi = 0;
+  while (rem > 0) {
+    if (pos[gi] < len) {
+      size_t sz = (rem + grid - 1) / grid;
+      sz = std::max(min_keys, (sz + 63) / 64 * 64);
+      sz = std::min(sz, len - pos[gi]);
+      const unsigned lr = unsigned(gi / G), g = unsigned(gi % G);
+      pl.items.push_back(make_uint4((lr << 24) | g, unsigned(pl.gS[gi]++), unsigned(pos[gi]), unsigned(pos[gi] + sz)));
+      pos[gi] += sz;
+      rem -= sz;
+      if (group_major && pos[gi] < len) continue;
+    }
+    gi = (gi + 1) % ng;
+  }
+  for (int v : pl.gS) pl.S_max = std::max(pl.S_max, v);
+  return pl;
+}
+
+static bool fd_stream_ok(const tf_fd_shape& s, World* w, const void* const* q, const void* const* k,
+                         const void* const* v) {
+  if (std::getenv("TFB_FD_LEGACY")) return false;  // A/B: the register-streaming kernel
+  if (!fast_ok(s)) return false;
+  const size_t len = s.kv_len / size_t(w->W);
+  if (size_t(s.batch) * s.kv_heads * len >= (size_t(1) << 31)) return false;
+  for (int r = 0; r < w->W; ++r)
+    if (w->ranks[r].local &&
+        ((reinterpret_cast<uintptr_t>(q[r]) | reinterpret_cast<uintptr_t>(k[r]) | reinterpret_cast<uintptr_t>(v[r])) & 15))
+      return false;  // TMA needs 16-byte aligned bases
+  return true;
+}
+
 static tf_status fd_validate(World* w, const tf_fd_shape* s, const void* const* q,
                              const void* const* k, const void* const* v, void* const* out) {
   if (!s || !q || !k || !v || !out) return set_error(TF_ERR_CONFIG, "tf_flash_decode: NULL argument");
@@ -1286,6 +1831,8 @@ void fd_preload() {  // see ag_exact_preload
   cudaFuncGetAttributes(&a, fd_attention_kernel<0>);
   cudaFuncGetAttributes(&a, fd_attention_kernel<1>);
   cudaFuncGetAttributes(&a, fd_attention_kernel<2>);
+  cudaFuncGetAttributes(&a, fd_stream_kernel<false>);
+  cudaFuncGetAttributes(&a, fd_stream_kernel<true>);
   cudaFuncGetAttributes(&a, fd_push_kernel);
   cudaFuncGetAttributes(&a, fd_gather_kernel);
   cudaFuncGetAttributes(&a, fd_fold_kernel);
@@ -1313,14 +1860,29 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   const size_t len = sh.kv_len / W;
   const size_t row_floats = size_t(sh.batch) * sh.q_heads * (d + 2);
   const bool fast = fast_ok(sh);
-  const int S = choose_splits(sh, len, w->sm_count);
+  // TMA-fed kernel (fd_stream_kernel) with a guided item table, else the
+  // register-streaming kernel with S equal splits per group.
+  const bool stream = fd_stream_ok(sh, w, q, k_shard, v_shard);
+  FdPlan plan;
+  if (stream) plan = fd_plan(G, len, unsigned(w->sm_count));
+  const int S = stream ? plan.S_max : choose_splits(sh, len, w->sm_count);
   const size_t split_len = (len + S - 1) / S;
-  const int S_eff = int((len + split_len - 1) / split_len);
+  const int S_eff = stream ? plan.S_max : int((len + split_len - 1) / split_len);
 
   // Boards: per (src, group) for fused, per src otherwise (fd.flags is
   // W x 1 in the reference, flash_decode.hpp:357).
   const bool fused = variant == TF_FD_FUSED || variant == TF_FD_FUSED_BY_ARRIVAL || variant == TF_FD_FUSED_OWNER;
   const bool owner = variant == TF_FD_FUSED_OWNER && W > 1;
+  if (fused) {
+    // The fused schedule runs every co-located rank in ONE persistent grid
+    // (its waits need every local producer resident): at most kMaxLocal
+    // ranks per device fit in a launch's parameters.
+    std::map<int, int> per_dev;
+    for (int r = 0; r < W; ++r)
+      if (w->ranks[r].local && ++per_dev[w->ranks[r].device] > kMaxLocal)
+        return set_error(TF_ERR_CONFIG, "run_fused: at most " + std::to_string(kMaxLocal) +
+                                            " ranks may share a device (loopback world)");
+  }
   BoardEntry fb;
   // Only schedules that signal advance the board's epoch: every rank (every
   // process, in an IPC world) must agree on "run e waits for >= e".
@@ -1362,9 +1924,38 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   TFB_CHECK(heap_get(w, "fd.tickets[" + std::to_string(G) + "x" + std::to_string(S_eff) + "]",
                      sizeof(unsigned long long) * (nlocal_max * G * 3 + kMaxLocal), &tick_off));  // done | gtick | claims | sfc
   TFB_CHECK(heap_get(w, "fd.ctr", 64, &ctr_off));
+  // Stream kernel tables: the item plan (uploaded once per geometry, before
+  // any launch uses it) and the per-(rank, group) fold claims.
+  size_t items_off = 0, fstate_off = 0;
+  if (stream) {
+    const std::string key = std::to_string(G) + "x" + std::to_string(len) + "@" + std::to_string(w->sm_count);
+    const size_t tbytes = plan.items.size() * sizeof(uint4) + size_t(G) * sizeof(int);
+    TFB_CHECK(heap_get(w, "fd.items[" + key + "]", tbytes, &items_off));
+    TFB_CHECK(heap_get(w, "fd.fstate[" + std::to_string(G) + "]", sizeof(unsigned) * kMaxLocal * G, &fstate_off));
+    uint64_t& up = w->epochs["fd.items.uploaded@" + std::to_string(items_off)];
+    if (!up) {
+      std::vector<uint8_t> host(tbytes);
+      std::memcpy(host.data(), plan.items.data(), plan.items.size() * sizeof(uint4));
+      std::memcpy(host.data() + plan.items.size() * sizeof(uint4), plan.gS.data(), size_t(G) * sizeof(int));
+      for (int r = 0; r < W; ++r) {
+        if (!w->ranks[r].local) continue;
+        TFB_CUDA(cudaSetDevice(w->ranks[r].device));
+        TFB_CUDA(cudaMemcpy(w->ptr(r, items_off), host.data(), tbytes, cudaMemcpyHostToDevice));
+      }
+      up = 1;
+    }
+  }
   // Tickets are epoch-valued per (group, split-count) geometry.
   const uint64_t tepoch = ++w->epochs["fd.tickets@" + std::to_string(tick_off)];
-  const int parity = int(fb.epoch & 1);
+  // Inbox parity: one counter per inbox shared by every schedule that
+  // writes it (the fused and the per-source boards have separate epochs, so
+  // keying the parity on either let a fused run and a following
+  // fine-waits run land in the same buffer).  Every rank issues the same
+  // call sequence, so every rank agrees on it; consecutive pushing runs
+  // alternate buffers, and a peer is at most one run ahead.
+  int parity = 0;
+  if (variant != TF_FD_BSP)
+    parity = int(++w->epochs[std::string(owner ? "fd.inbox.owner" : "fd.inbox") + "@" + std::to_string(inbox_off)] & 1);
 
   auto inbox_of = [&](int r) -> float* {
     if (inbox_opt && inbox_opt[r]) return static_cast<float*>(inbox_opt[r]);
@@ -1464,11 +2055,61 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
         Q.direct = fold_inline && W == 1;
         Q.by_arrival = variant == TF_FD_FUSED_BY_ARRIVAL;
         Q.owner = owner;
+        if (stream) {
+          Q.items = reinterpret_cast<const uint4*>(w->ptr(lead, items_off));
+          Q.gS = reinterpret_cast<const int*>(Q.items + plan.items.size());
+          Q.nitems = unsigned(plan.items.size()) * unsigned(Q.nlocal);
+          Q.fstate = reinterpret_cast<unsigned*>(w->ptr(lead, fstate_off));
+        }
         cudaSetDevice(kv.first);
-        const unsigned items = unsigned(Q.nlocal) * G * S_eff;
+        // Every co-located rank's inputs may come from its own stream: the
+        // shared launch on st[lead] is ordered after all of them.
+        for (int i = 1; i < Q.nlocal; ++i) {
+          const int r = rs[c0 + i];
+          if (st[r] == st[lead]) continue;
+          cudaEvent_t ev;
+          TFB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+          TFB_CUDA(cudaEventRecord(ev, st[r]));
+          TFB_CUDA(cudaStreamWaitEvent(st[lead], ev, 0));
+          cudaEventDestroy(ev);
+        }
         // Tensor-core split with bf16 P for bf16 output, hi/lo P when the
         // caller asked for fp32 output; the generic split otherwise.
-        const int mode = !fast ? 0 : (sh.out_dtype == TF_F32 ? 2 : 1);
+        const bool hilo = sh.out_dtype == TF_F32 || std::getenv("TFB_FD_HILO");
+        if (stream) {
+          FdMaps maps{};
+          for (int i = 0; i < Q.nlocal; ++i) {
+            const int r = rs[c0 + i];
+            const size_t rows = size_t(sh.batch) * sh.kv_heads * len;
+            TFB_CHECK(fd_kv_map(&maps.k[i], k_shard[r], rows));
+            TFB_CHECK(fd_kv_map(&maps.v[i], v_shard[r], rows));
+          }
+          const void* kfn = hilo ? reinterpret_cast<const void*>(fd_stream_kernel<true>)
+                                 : reinterpret_cast<const void*>(fd_stream_kernel<false>);
+          const size_t smem = sizeof(StreamSmem) + 1024;
+          static std::atomic<bool> attr[2][64];
+          if (!attr[hilo][kv.first & 63].load()) {
+            TFB_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            attr[hilo][kv.first & 63].store(true);
+          }
+          const unsigned grid = std::max(1u, std::min(Q.nitems, unsigned(w->sm_count)));
+          if (hilo) fd_stream_kernel<true><<<grid, kStreamThreads, smem, st[lead]>>>(Q, maps);
+          else fd_stream_kernel<false><<<grid, kStreamThreads, smem, st[lead]>>>(Q, maps);
+          TFB_CUDA(cudaGetLastError());
+          ++w->launches;
+          for (int i = 1; i < Q.nlocal; ++i) {
+            const int r = rs[c0 + i];
+            if (st[r] == st[lead]) continue;
+            cudaEvent_t ev;
+            TFB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            TFB_CUDA(cudaEventRecord(ev, st[lead]));
+            TFB_CUDA(cudaStreamWaitEvent(st[r], ev, 0));
+            cudaEventDestroy(ev);
+          }
+          continue;
+        }
+        const unsigned items = unsigned(Q.nlocal) * G * S_eff;
+        const int mode = !fast ? 0 : (hilo ? 2 : 1);
         const void* kfn = mode == 0 ? reinterpret_cast<const void*>(fd_attention_kernel<0>)
                         : mode == 1 ? reinterpret_cast<const void*>(fd_attention_kernel<1>)
                                     : reinterpret_cast<const void*>(fd_attention_kernel<2>);

@@ -238,9 +238,14 @@ __global__ void barrier_kernel(uint64_t* const* cells, int self, int W, uint64_t
   const uint64_t target = epoch * uint64_t(W);
   if (!wait_geq(cells[self], target, watchdog_ns, err, kWaitBarrier, self, board, 0, 0,
                 epoch - 1)) {
-    // Rewrite observed/expected as "arrived of W" for the message.
+    // Rewrite observed/expected as "arrived of W" for the message.  The raw
+    // cell counts every generation's arrivals; a cell still short of the
+    // previous generations (a rank that never arrived at an earlier barrier
+    // either) reads as 0 arrivals, never as a wrapped subtraction.
     if (err->kind == kWaitBarrier && err->rank == self) {
-      err->observed = err->observed - (epoch - 1) * uint64_t(W);
+      const uint64_t base = (epoch - 1) * uint64_t(W);
+      const uint64_t seen = err->observed;
+      err->observed = seen >= base ? (seen - base < uint64_t(W) ? seen - base : uint64_t(W)) : 0;
       err->expected = uint64_t(W);
     }
   }

@@ -86,6 +86,22 @@ struct World {
   uint64_t ag_epoch = 0;
   uint64_t fd_epoch = 0;
   FlagSnapshot ag_flags, fd_flags;
+  // Where the last AG run's gathered operand lives, per rank r and source
+  // block s: (pointer to the block's first element, row pitch in elements)
+  // -- the inbox/stage the GEMM consumed, or the owner's shard where the
+  // schedule reads it in place (tf_ag_gathered).
+  struct AgBlock {
+    const void* p = nullptr;
+    size_t pitch = 0;
+  };
+  std::vector<std::vector<AgBlock>> ag_src;
+  size_t ag_m = 0, ag_kw = 0, ag_esz = 0;
+  void record_ag(size_t m, size_t kw, size_t esz) {
+    ag_m = m;
+    ag_kw = kw;
+    ag_esz = esz;
+    ag_src.assign(W, std::vector<AgBlock>(W));
+  }
   // Event log (tf_world_set_events): the last pull/push run's per-chunk
   // store / first-load timestamps, [num_m][W][2] u64 in every rank's heap.
   bool events = false;

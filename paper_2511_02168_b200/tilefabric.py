@@ -245,7 +245,6 @@ class ag:  # namespace tilefabric::ag
         heap = esz * p.m * kw + 2 * esz * p.m * p.k + (8 << 20)
         with World.from_config(cfg, heap) as w:
             shards = w.alloc("ag.a", esz * p.m * kw)
-            gathered = w.alloc("ag.gathered", esz * p.m * p.k)
             A = torch.from_numpy(np.ascontiguousarray(p.a, np.float32))
             bufs_b, bufs_c = [], []
             for r in range(W):
@@ -256,22 +255,24 @@ class ag:  # namespace tilefabric::ag
                 bufs_b.append(torch.from_numpy(np.ascontiguousarray(p.b, np.float32)).to(tdt).to(dev))
                 bufs_c.append(torch.empty((p.m, p.n), dtype=tdt, device=dev))
             torch.cuda.synchronize()
+            w.barrier()  # setup_fence (ag_gemm.hpp:189-191): every shard placed before any rank reads it
+            w.tax_reset()  # untimed, like the reference's: the tax meter starts after it
             shape = _abi.AgShape(p.m, p.n, p.k, p.tiles.bm, p.tiles.bn, p.tiles.bk, dtype)
             before = w.launches()
             _abi.check(w.lib.tf_ag_gemm(
                 w.handle, variant, C.byref(shape), _abi.ptr_array(shards),
                 _abi.ptr_array([b.data_ptr() for b in bufs_b]),
-                _abi.ptr_array([c.data_ptr() for c in bufs_c]),
-                _abi.ptr_array(gathered) if variant != _abi.TF_AG_PULL else None, None))
+                _abi.ptr_array([c.data_ptr() for c in bufs_c]), None, None))
             launches = w.launches() - before
             taxes = [w.taxes(r) for r in range(W)]
             cs = [c.float().cpu().numpy() for c in bufs_c]
+            # The operand each rank's GEMM consumed (inbox / stage, and the
+            # blocks read in place), every schedule including PULL.
             gath = []
-            if variant != _abi.TF_AG_PULL:
-                for r in range(W):
-                    g = torch.empty((p.m, p.k), dtype=tdt, device=torch.device("cuda", w.devices[r]))
-                    w.memcpy(g.data_ptr(), gathered[r], g.numel() * esz)
-                    gath.append(g.float().cpu().numpy())
+            for r in range(W):
+                g = torch.empty((p.m, p.k), dtype=tdt)
+                _abi.check(w.lib.tf_ag_gathered(w.handle, r, g.data_ptr(), g.numel() * esz))
+                gath.append(g.float().numpy())
             flags = []
             if variant == _abi.TF_AG_PUSH:
                 for r in range(W):
