@@ -56,6 +56,7 @@ namespace tfb {
 namespace {
 
 constexpr int kMaxLocal = 16;  // local ranks per launch (loopback worlds)
+constexpr int kFoldRB = 16;    // rows per warp per load batch in the split folds
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -783,8 +784,54 @@ __device__ __forceinline__ float4 ldcg4(const float* p) {
 // pushing, else the published partial) and, W = 1 fused (`direct`), the
 // finalized output o / l (tilemath.hpp:225-239) -- bitwise what fold_group
 // would compute from the single source.
-// Eight warps do the work (a 9-warp fd_stream_kernel block: warp 8 only
-// joins the barriers); `named`: the caller is the consumer warps alone.
+// One head's rank partial [M | L | O] -> the wire rows (every inbox when
+// pushing, else the published partial) and, W = 1 fused (direct), the
+// finalized output O / L (tilemath.hpp:225-239, 244-258).  One warp.
+template <int EL>
+__device__ __forceinline__ void emit_wire_row(const FdParams& P, int lr, int g, int h, float M, float L,
+                                              const float (&O)[EL], int lane) {
+  const int d = P.d, gs = P.gs, W = P.W, Hq = P.Hq, Hkv = P.Hkv, row_len = d + 2;
+  const int rank = P.r[lr].rank;
+  const int b = g / Hkv, kvh = g % Hkv;
+  const size_t base_src = size_t(rank) * P.B * Hq * row_len;
+  const size_t off = (size_t(b) * Hq + kvh * gs + h) * row_len;
+  const int hq = kvh * gs + h;
+  if (P.push) {
+    for (int dst = 0; dst < W; ++dst) {
+      if (P.owner && dst != g % W) continue;  // owner-combine: the group's owner only
+      float* r = P.inbox_all[dst] + base_src + off;
+      if (lane == 0) {
+        r[0] = M;
+        r[1] = L;
+      }
+#pragma unroll
+      for (int x = 0; x < EL; ++x)
+        if (lane + 32 * x < d) r[2 + lane + 32 * x] = O[x];
+    }
+  } else {
+    float* r = P.r[lr].pub + off;
+    if (lane == 0) {
+      r[0] = M;
+      r[1] = L;
+    }
+#pragma unroll
+    for (int x = 0; x < EL; ++x)
+      if (lane + 32 * x < d) r[2 + lane + 32 * x] = O[x];
+  }
+  if (P.direct) {
+    if (L == 0.0f) {
+      if (lane == 0) raise_err(P.err, TF_ERR_EMPTY_ATTENTION, kEmpty, rank, -1, 0, 0, 0, 0, uint64_t(hq));
+      return;
+    }
+    const size_t ooff = (size_t(b) * Hq + hq) * d;
+#pragma unroll
+    for (int x = 0; x < EL; ++x)
+      if (lane + 32 * x < d) store_out(P.r[lr].out, ooff + lane + 32 * x, O[x] / L, P.out_bf16);
+  }
+}
+
+// Eight warps do the work (a 10-warp fd_stream_kernel block: warps 8-9
+// only join the barriers); `named`: the caller is the consumer warps alone.
 template <int EL, int RB>
 __device__ __forceinline__ void fold_heads(const FdParams& P, int lr, int g, int h0, int hc, float* s_wm,
                                         float* s_L, float* s_O, bool named = false) {
@@ -839,42 +886,7 @@ __device__ __forceinline__ void fold_heads(const FdParams& P, int lr, int g, int
     }
     return M;
   };
-  auto emit = [&](int h, float M, float L, const float (&O)[EL]) {
-    const size_t off = (size_t(b) * Hq + kvh * gs + h) * row_len;
-    const int hq = kvh * gs + h;
-    if (push) {
-      for (int dst = 0; dst < W; ++dst) {
-        if (P.owner && dst != g % W) continue;  // owner-combine: the group's owner only
-        float* r = P.inbox_all[dst] + base_src + off;
-        if (lane == 0) {
-          r[0] = M;
-          r[1] = L;
-        }
-#pragma unroll
-        for (int x = 0; x < EL; ++x)
-          if (lane + 32 * x < d) r[2 + lane + 32 * x] = O[x];
-      }
-    } else {
-      float* r = pub + off;
-      if (lane == 0) {
-        r[0] = M;
-        r[1] = L;
-      }
-#pragma unroll
-      for (int x = 0; x < EL; ++x)
-        if (lane + 32 * x < d) r[2 + lane + 32 * x] = O[x];
-    }
-    if (direct) {
-      if (L == 0.0f) {
-        if (lane == 0) raise_err(P.err, TF_ERR_EMPTY_ATTENTION, kEmpty, rank, -1, 0, 0, 0, 0, uint64_t(hq));
-        return;
-      }
-      const size_t ooff = (size_t(b) * Hq + hq) * d;
-#pragma unroll
-      for (int x = 0; x < EL; ++x)
-        if (lane + 32 * x < d) store_out(out, ooff + lane + 32 * x, O[x] / L, out_bf16);
-    }
-  };
+  auto emit = [&](int h, float M, float L, const float (&O)[EL]) { emit_wire_row<EL>(P, lr, g, h, M, L, O, lane); };
   // One load batch (every row of this warp's share in flight at once, m/l
   // and o together): the common case, one L2 round trip per sub-item.
   auto one_batch = [&](int h, int r0, int step, float (&v)[RB][EL], float2 (&ml)[RB]) {
@@ -1053,7 +1065,7 @@ __device__ __noinline__ void fd_post_phases(const FdParams& P, unsigned ranks_ma
       if (s_last == 2) continue;
       if (!s_last) break;  // an error elsewhere (e.g. NumericError) ends the launch
       stamp(9);
-      if (P.d <= 128) fold_heads<4, 8>(P, lr, g, hb * P.hc, P.hc, s_wm, s_fL, s_fO);
+      if (P.d <= 128) fold_heads<4, kFoldRB>(P, lr, g, hb * P.hc, P.hc, s_wm, s_fL, s_fO);
       else fold_heads<8, 4>(P, lr, g, hb * P.hc, P.hc, s_wm, s_fL, s_fO);
       stamp(8);
       // The last sub-item of a group releases its flags to every rank
@@ -1233,26 +1245,32 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
 }
 
 // ---- TMA-fed split partials (bf16 K/V, d = 128, 8 q-heads per KV head) ----
-// One CTA per SM, 9 warps.  Warp 8 (one lane) is the producer: it claims
-// items (a split of a group: keys [k0, k1) of one KV stream) from a global
-// counter, in the order of a host-built table, and streams each item's K and
-// V through a kStreamStages-deep shared-memory ring with TMA
-// (cp.async.bulk.tensor, 64 keys x 128 d of K and of V per stage, 128-byte
-// swizzle) plus the group's 8 q rows with a 1-D bulk copy on the item's
-// first stage.  Warps 0-7 consume: warp c takes 16-key tile (c & 3) of every
-// stage whose sequence number has parity c >> 2, so each warp's tiles of an
-// item are a fixed set (the partial is schedule-independent, bitwise).  The
-// math is the register decode of fast_warp_range, fed from smem: S^T =
-// K.Q^T with mma.m16n8k16 over ldmatrix'd K, exp2-domain online softmax with
-// warp-shuffle max/sum, O^T += V^T.P^T with ldmatrix.trans'd V.  When the
-// stage sequence moves to the next item the 8 warps merge their partials
-// (max first, ascending warp order) into the item's split row and publish
-// it while the producer keeps the ring full; the CTA that completes a
-// group's last split while items remain folds the whole group right there
-// (fold claim), so only the last groups' folds are left for the tail.
+// One CTA per SM, 10 warps:
+//   warp 8  producer (one lane): walks the items this CTA claims (its first
+//           item is blockIdx.x, the rest come from a global counter, each
+//           claim issued one item ahead so its latency hides behind the
+//           streaming) and streams every item's K and V through a
+//           kStreamStages-deep smem ring with TMA (cp.async.bulk.tensor, 64
+//           keys x 128 d of K and of V per stage, 128-byte swizzle), plus
+//           the group's 8 q rows (1-D bulk copy) on the item's first stage.
+//   warps 0-7  consumers: warp c takes 16-key tile (c & 3) of the stages
+//           whose index inside their item has parity c >> 2 -- a function
+//           of the item alone, so an item's partial is the same bits on any
+//           CTA.  The math is the register decode of fast_warp_range fed from
+//           smem: S^T = K.Q^T with mma.m16n8k16 on ldmatrix'd K, exp2-domain
+//           online softmax with warp-shuffle max/sum, O^T += V^T.P^T on
+//           ldmatrix.trans'd V.  At an item boundary each warp drops its
+//           partial into one of two merge slots and goes straight on.
+//   warp 9  merger: folds the 8 warp partials of each finished item (max
+//           first, ascending warp order) into the item's split row,
+//           publishes it (release + completion ticket), and -- when its item
+//           completed a group while compute items remain -- folds that whole
+//           group right away (the post-phase fold's exact arithmetic), so
+//           only the last groups' folds are left for the tail.
 constexpr int kStreamStages = 4;
 constexpr int kStreamConsumers = 8;
-constexpr int kStreamThreads = 32 * (kStreamConsumers + 1);
+constexpr int kProducerWarp = kStreamConsumers, kMergerWarp = kStreamConsumers + 1;
+constexpr int kStreamThreads = 32 * (kStreamConsumers + 2);
 constexpr int kStageKV = 2 * 64 * 128 * 2;  // K + V of 64 keys, bf16
 constexpr int kORow = 132;                   // padded merge row (conflict-free stores)
 
@@ -1264,12 +1282,12 @@ struct FdMaps {
 struct StreamSmem {
   uint8_t kv[kStreamStages][kStageKV];  // 1024-aligned: [K half0 | K half1 | V half0 | V half1], 8 KB each
   uint8_t q[kStreamStages][8 * 128 * 2];
-  float o[kStreamConsumers][8 * kORow];
-  float m[kStreamConsumers][8], l[kStreamConsumers][8], wa[8][kStreamConsumers];
-  float hm[8], hl[8];
-  int meta[kStreamStages][4];  // item (-1: end), keys in stage, lr << 24 | g, split j
-  uint64_t full[kStreamStages], empty[kStreamStages];
-  int bad, inline_fold;
+  float mo[2][kStreamConsumers][8 * kORow];  // merge slots: per warp o[head][d]
+  float mm[2][kStreamConsumers][8], ml[2][kStreamConsumers][8];
+  int mbad[2][kStreamConsumers];
+  int minfo[2][2];             // lr << 24 | g (-1: end), split j
+  int meta[kStreamStages][4];  // item (-1: end), keys | stage-in-item << 8, lr << 24 | g, split j
+  uint64_t full[kStreamStages], empty[kStreamStages], mfull[2], mempty[2];
   unsigned ranks_mask;
 };
 
@@ -1302,18 +1320,23 @@ __device__ __forceinline__ uint32_t mask_keys(uint32_t x, int key_lo, int n) {
   return (key_lo < n ? (x & 0xffffu) : 0u) | (key_lo + 1 < n ? (x & 0xffff0000u) : 0u);
 }
 
-// Producer: lane 0 of warp kStreamConsumers.
+__device__ __forceinline__ uint4 stream_item(const FdParams& P, unsigned it) {
+  uint4 e = P.items[it / unsigned(P.nlocal)];
+  e.x |= (it % unsigned(P.nlocal)) << 24;
+  return e;
+}
+
+// Producer: lane 0 of kProducerWarp.
 __device__ void stream_producer(const FdParams& P, const FdMaps& M, StreamSmem& sm) {
-  const int G = P.B * P.Hkv;
   unsigned seq = 0, skewed = 0;
   const uint64_t t0 = globaltimer_ns();
+  unsigned it = blockIdx.x;  // first item: static; later ones claimed one item ahead
+  uint4 e = it < P.nitems ? stream_item(P, it) : make_uint4(0, 0, 0, 0);
   for (;;) {
-    const unsigned it = atomicAdd(&P.ctr[0], 1u);
     const bool end = it >= P.nitems;
-    const int lr = end ? 0 : int(it % unsigned(P.nlocal));
-    uint4 e = end ? make_uint4(0, 0, 0, 0) : P.items[it / unsigned(P.nlocal)];
-    e.x |= unsigned(lr) << 24;
-    const int g = int(e.x & 0xffffffu);
+    unsigned next = 0;
+    if (!end) next = gridDim.x + atomicAdd(&P.ctr[0], 1u);
+    const int lr = int(e.x >> 24), g = int(e.x & 0xffffffu);
     const int b = g / P.Hkv, kvh = g % P.Hkv;
     const unsigned row0 = unsigned(g) * unsigned(P.len);  // [B][Hkv][len] rows: (b * Hkv + kvh) * len
     if (!end && P.r[lr].skew_ns && !((skewed >> lr) & 1u)) {  // straggler model: the rank starts late
@@ -1326,7 +1349,7 @@ __device__ void stream_producer(const FdParams& P, const FdMaps& M, StreamSmem& 
       sm100::mbar_wait(&sm.empty[st], ((seq / kStreamStages) & 1u) ^ 1u);
       volatile int* mt = sm.meta[st];
       mt[0] = end ? -1 : int(it);
-      mt[1] = end ? 0 : int(min(64u, e.w - key));
+      mt[1] = end ? 0 : int(min(64u, e.w - key)) | int(((key - e.z) >> 6) << 8);
       mt[2] = int(e.x);
       mt[3] = int(e.y);
       ++seq;
@@ -1342,30 +1365,30 @@ __device__ void stream_producer(const FdParams& P, const FdMaps& M, StreamSmem& 
         bulk_load(sm.q[st], static_cast<const __nv_bfloat16*>(P.r[lr].q) + (size_t(b) * P.Hq + kvh * 8) * 128, 2048,
                   &sm.full[st]);
     }
-    (void)G;
+    it = next;
+    if (it < P.nitems) e = stream_item(P, it);
   }
 }
 
-// The 8 consumer warps' partials of one item -> its split row (ws), then the
-// split is published; returns (to every consumer thread) whether this CTA
-// folds the group inline.
-__device__ __forceinline__ void stream_finish_item(const FdParams& P, StreamSmem& sm, int lrg, int j, float m0,
-                                                   float m1, float l0, float l1, const float (&o)[8][4], int badl) {
+// Consumer warp -> merge slot (no CTA-wide barrier: the merger folds it).
+__device__ __forceinline__ void stream_drop_partial(StreamSmem& sm, unsigned nitem, int lrg, int j, float m0,
+                                                    float m1, float l0, float l1, const float (&o)[8][4],
+                                                    int badl) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, t = lane & 3;
-  const int G = P.B * P.Hkv;
-  const int lr = lrg >> 24, g = lrg & 0xffffff;
+  const int bsl = int(nitem & 1u);
+  sm100::mbar_wait(&sm.mempty[bsl], ((nitem >> 1) & 1u) ^ 1u);
 #pragma unroll
   for (int off = 4; off < 32; off <<= 1) {
     l0 += __shfl_xor_sync(0xffffffffu, l0, off);
     l1 += __shfl_xor_sync(0xffffffffu, l1, off);
   }
   if (gq == 0) {
-    sm.m[warp][2 * t] = m0;
-    sm.m[warp][2 * t + 1] = m1;
-    sm.l[warp][2 * t] = l0;
-    sm.l[warp][2 * t + 1] = l1;
+    sm.mm[bsl][warp][2 * t] = m0;
+    sm.mm[bsl][warp][2 * t + 1] = m1;
+    sm.ml[bsl][warp][2 * t] = l0;
+    sm.ml[bsl][warp][2 * t + 1] = l1;
   }
-  float* ow = sm.o[warp];
+  float* ow = sm.mo[bsl][warp];
 #pragma unroll
   for (int db = 0; db < 8; ++db) {
     const int dA = 16 * db + gq;
@@ -1374,94 +1397,20 @@ __device__ __forceinline__ void stream_finish_item(const FdParams& P, StreamSmem
     ow[(2 * t) * kORow + dA + 8] = o[db][2];
     ow[(2 * t + 1) * kORow + dA + 8] = o[db][3];
   }
-  if (badl) sm.bad = 1;
-  consumer_bar();
-  // Max-first fold of the warp partials (log2 domain), ascending warp order
-  // (the fold of fast_split): per head M = max m_w over warps with l_w != 0.
-  if (threadIdx.x < 8) {
-    const int h = threadIdx.x;
-    float Mx = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < kStreamConsumers; ++w)
-      if (sm.l[w][h] != 0.0f) Mx = fmaxf(Mx, sm.m[w][h]);
-    float L = 0.0f;
-#pragma unroll
-    for (int w = 0; w < kStreamConsumers; ++w) {
-      const float bl = sm.l[w][h];
-      const float a = bl != 0.0f ? exp2f(sm.m[w][h] - Mx) : 0.0f;
-      sm.wa[h][w] = a;
-      L = __fadd_rn(L, __fmul_rn(bl, a));
-    }
-    sm.hm[h] = Mx;
-    sm.hl[h] = L;
-  }
-  consumer_bar();
-  const int wrl = ws_row(128);
-  float* wsrow = P.ws + ((size_t(lr) * G + g) * P.S + j) * 8 * wrl;
-  for (int e = threadIdx.x; e < 8 * 128; e += 32 * kStreamConsumers) {
-    const int h = e >> 7, dd = e & 127;
-    float acc = 0.0f;
-#pragma unroll
-    for (int w = 0; w < kStreamConsumers; ++w) {
-      const float a = sm.wa[h][w];
-      acc = __fadd_rn(acc, a != 0.0f ? __fmul_rn(sm.o[w][h * kORow + dd], a) : 0.0f);
-    }
-    float* row = wsrow + size_t(h) * wrl;
-    if (dd == 0) {
-      row[0] = sm.hm[h] * kLn2;
-      row[1] = sm.hl[h];
-    }
-    row[kWsO + dd] = acc;
-  }
-  consumer_bar();
-  if (threadIdx.x == 0) {
-    if (sm.bad) {
-      raise_err(P.err, TF_ERR_NUMERIC, kNumeric, P.r[lr].rank, -1, 0, 0, 0, 0,
-                (uint64_t((g % P.Hkv) * 8) << 32) | uint64_t(size_t(P.r[lr].rank) * P.len));
-      sm.bad = 0;
-    }
-    sm.ranks_mask |= 1u << lr;
-    // Publish (release: every consumer's ws stores, ordered by the barrier)
-    // and take the group's completion ticket in one RMW: the CTA whose split
-    // completes the group sees every other split (acquire).
-    __threadfence();
-    const uint64_t before = atom_add_acq_rel_gpu(reinterpret_cast<unsigned long long*>(P.done + size_t(lr) * G + g), 1ull);
-    int fold = 0;
-    if (before + 1 == uint64_t(split_count(P, lr, g)) && P.fstate &&
-        *reinterpret_cast<volatile unsigned*>(&P.ctr[0]) < P.nitems)  // items left: fold now, off the tail
-      fold = atomicCAS(&P.fstate[size_t(lr) * G + g], 0u, 1u) == 0u;
-    sm.inline_fold = fold;
-  }
-  consumer_bar();
-}
-
-// Inline group fold by the consumer warps (split rows -> the rank's wire
-// rows / direct output, then the group's flags) -- the sub-item fold of
-// fd_post_phases for all gs heads at once.
-__device__ void stream_fold_group(const FdParams& P, int lr, int g, float* s_wm, float* s_fL, float* s_fO) {
-  fold_heads<4, 8>(P, lr, g, 0, P.gs, s_wm, s_fL, s_fO, /*named=*/true);
-  const int G = P.B * P.Hkv;
-  const FdRank& R = P.r[lr];
-  consumer_bar();
-  if (!P.push) return;
-  if (threadIdx.x == 0) {
-    if (!P.direct) {
-      if (P.local_dst == (P.W >= 64 ? ~0ull : ((1ull << P.W) - 1))) __threadfence();
-      else __threadfence_system();
+  const int any_bad = __any_sync(0xffffffffu, badl);
+  if (lane == 0) {
+    sm.mbad[bsl][warp] = any_bad;
+    if (warp == 0) {
+      sm.minfo[bsl][0] = lrg;
+      sm.minfo[bsl][1] = j;
     }
   }
-  consumer_bar();
-  if (threadIdx.x < P.W && (!P.owner || int(threadIdx.x) == g % P.W)) {
-    uint64_t* f = P.flags_all[threadIdx.x] + size_t(R.rank) * G + g;
-    if (P.events_all[threadIdx.x]) P.events_all[threadIdx.x][(size_t(R.rank) * G + g) * 2] = globaltimer_ns();
-    if (P.direct) atomicAdd(reinterpret_cast<unsigned long long*>(f), 1ull);
-    else if ((P.local_dst >> threadIdx.x) & 1ull) red_release_gpu(f, 1);
-    else red_release_sys(f, 1);
-  }
+  __syncwarp();
+  if (lane == 0) sm100::mbar_arrive(&sm.mfull[bsl]);  // release: this warp's slot writes
 }
 
 template <bool HILO>
-__device__ void stream_consumer(const FdParams& P, StreamSmem& sm, float* s_wm, float* s_fL, float* s_fO) {
+__device__ void stream_consumer(const FdParams& P, StreamSmem& sm) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, t = lane & 3;
   const int tl = warp & 3;
@@ -1473,6 +1422,7 @@ __device__ void stream_consumer(const FdParams& P, StreamSmem& sm, float* s_wm, 
   const uint32_t vrow = uint32_t(tl * 16 + (lane & 7) + ((lane >> 4) & 1) * 8) * 128;
   const int khi = lane >> 4, vhi = (lane >> 3) & 1, sw = lane & 7;
   int cur = -1, cur_lrg = 0, cur_j = 0;
+  unsigned nitem = 0;
   float o[8][4];
   uint32_t qb[8][2];
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
@@ -1480,16 +1430,21 @@ __device__ void stream_consumer(const FdParams& P, StreamSmem& sm, float* s_wm, 
   for (unsigned seq = 0;; ++seq) {
     const int st = int(seq % kStreamStages);
     sm100::mbar_wait(&sm.full[st], (seq / kStreamStages) & 1u);
+    if (seq == 0 && P.trace && threadIdx.x == 0) P.trace[size_t(blockIdx.x) * 16 + 10] = globaltimer_ns();
     const volatile int* mt = sm.meta[st];
-    const int item = mt[0], nk = mt[1], lrg = mt[2], j = mt[3];
+    const int item = mt[0], nk = mt[1] & 0xff, sidx = mt[1] >> 8, lrg = mt[2], j = mt[3];
     if (item != cur) {
-      if (cur >= 0) {
-        stream_finish_item(P, sm, cur_lrg, cur_j, m0, m1, l0, l1, o, badl);
-        if (sm.inline_fold) stream_fold_group(P, cur_lrg >> 24, cur_lrg & 0xffffff, s_wm, s_fL, s_fO);
-      }
+      if (cur >= 0) stream_drop_partial(sm, nitem++, cur_lrg, cur_j, m0, m1, l0, l1, o, badl);
       if (item < 0) {
+        // End marker for the merger, in the next slot.
+        const int bsl = int(nitem & 1u);
+        sm100::mbar_wait(&sm.mempty[bsl], ((nitem >> 1) & 1u) ^ 1u);
+        if (lane == 0 && warp == 0) sm.minfo[bsl][0] = -1;
         __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(&sm.empty[st]);
+        if (lane == 0) {
+          sm100::mbar_arrive(&sm.mfull[bsl]);
+          sm100::mbar_arrive(&sm.empty[st]);
+        }
         break;
       }
       cur = item;
@@ -1508,7 +1463,7 @@ __device__ void stream_consumer(const FdParams& P, StreamSmem& sm, float* s_wm, 
       badl = 0;
     }
     const int n = nk - tl * 16;  // valid keys of this warp's tile
-    if ((seq & 1u) == sel && n > 0) {
+    if ((unsigned(sidx) & 1u) == sel && n > 0) {
       const uint32_t kb = sm100::smem_u32(sm.kv[st]), vb = kb + kStageKV / 2;
       float s[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -1579,6 +1534,164 @@ __device__ void stream_consumer(const FdParams& P, StreamSmem& sm, float* s_wm, 
   }
 }
 
+// One warp folds a whole group's split rows exactly as fd_post_phases'
+// fold_heads<4, kFoldRB> sub-items do (same per-warp row sets, same
+// ascending sums, same combine), then emits and releases the group's flags.
+__device__ void warp_fold_group(const FdParams& P, int lr, int g) {
+  const int G = P.B * P.Hkv, gs = P.gs, S = split_count(P, lr, g);
+  const int lane = threadIdx.x & 31;
+  const int wrl = ws_row(128);
+  const int wph = P.hc >= 8 ? 1 : 8 / P.hc;
+  const float* grp = P.ws + ((size_t(lr) * G + g) * P.S) * gs * wrl;
+  for (int h = 0; h < gs; ++h) {
+    float Mj[8], Lj[8], Oj[8][4];
+    for (int jj = 0; jj < wph; ++jj) {
+      float Mw = -INFINITY;
+      for (int i = jj; i < S; i += wph) {
+        const float* row = grp + (size_t(i) * gs + h) * wrl;
+        if (__ldcg(row + 1) != 0.0f) Mw = fmaxf(Mw, __ldcg(row));
+      }
+      float L = 0.0f, O[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int i = jj; i < S; i += wph) {
+        const float* row = grp + (size_t(i) * gs + h) * wrl;
+        const float m = __ldcg(row), l = __ldcg(row + 1);
+        const float w = l != 0.0f ? expf(m - Mw) : 0.0f;
+        L = __fadd_rn(L, __fmul_rn(l, w));
+#pragma unroll
+        for (int x = 0; x < 4; ++x) O[x] = __fadd_rn(O[x], __fmul_rn(__ldcg(row + kWsO + lane + 32 * x), w));
+      }
+      Mj[jj] = Mw;
+      Lj[jj] = L;
+#pragma unroll
+      for (int x = 0; x < 4; ++x) Oj[jj][x] = O[x];
+    }
+    float M, LL, OO[4];
+    if (wph == 1) {
+      M = Mj[0];
+      LL = Lj[0];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) OO[x] = Oj[0][x];
+    } else {
+      M = -INFINITY;
+      for (int y = 0; y < wph; ++y)
+        if (Lj[y] != 0.0f) M = fmaxf(M, Mj[y]);
+      LL = 0.0f;
+#pragma unroll
+      for (int x = 0; x < 4; ++x) OO[x] = 0.0f;
+      for (int y = 0; y < wph; ++y) {
+        if (Lj[y] == 0.0f) continue;
+        const float a = expf(Mj[y] - M);
+        LL = __fadd_rn(LL, __fmul_rn(Lj[y], a));
+#pragma unroll
+        for (int x = 0; x < 4; ++x) OO[x] = __fadd_rn(OO[x], __fmul_rn(Oj[y][x], a));
+      }
+    }
+    emit_wire_row<4>(P, lr, g, h, M, LL, OO, lane);
+  }
+  if (!P.push) return;
+  __syncwarp();
+  if (lane == 0 && !P.direct) {
+    if (P.local_dst == (P.W >= 64 ? ~0ull : ((1ull << P.W) - 1))) __threadfence();
+    else __threadfence_system();
+  }
+  __syncwarp();
+  const FdRank& R = P.r[lr];
+  for (int dst = lane; dst < P.W; dst += 32) {
+    if (P.owner && dst != g % P.W) continue;
+    uint64_t* f = P.flags_all[dst] + size_t(R.rank) * G + g;
+    if (P.events_all[dst]) P.events_all[dst][(size_t(R.rank) * G + g) * 2] = globaltimer_ns();
+    if (P.direct) atomicAdd(reinterpret_cast<unsigned long long*>(f), 1ull);
+    else if ((P.local_dst >> dst) & 1ull) red_release_gpu(f, 1);
+    else red_release_sys(f, 1);
+  }
+}
+
+// Merger warp (kMergerWarp).
+__device__ void stream_merger(const FdParams& P, StreamSmem& sm) {
+  const int lane = threadIdx.x & 31;
+  const int G = P.B * P.Hkv;
+  const int wrl = ws_row(128);
+  unsigned long long* tr = P.trace ? P.trace + size_t(blockIdx.x) * 16 : nullptr;
+  for (unsigned n = 0;; ++n) {
+    const int bsl = int(n & 1u);
+    sm100::mbar_wait(&sm.mfull[bsl], (n >> 1) & 1u);
+    const uint64_t tm = tr ? globaltimer_ns() : 0;
+    const int lrg = sm.minfo[bsl][0], j = sm.minfo[bsl][1];
+    if (lrg < 0) break;
+    const int lr = lrg >> 24, g = lrg & 0xffffff;
+    // Lane h < 8: head h's max over the warps with l != 0, its per-warp
+    // weights exp2(m_w - M) and L (the fold of fast_split, max first).
+    float wreg[kStreamConsumers];
+    float Mx = -INFINITY, L = 0.0f;
+    if (lane < 8) {
+#pragma unroll
+      for (int w = 0; w < kStreamConsumers; ++w)
+        if (sm.ml[bsl][w][lane] != 0.0f) Mx = fmaxf(Mx, sm.mm[bsl][w][lane]);
+#pragma unroll
+      for (int w = 0; w < kStreamConsumers; ++w) {
+        const float bl = sm.ml[bsl][w][lane];
+        wreg[w] = bl != 0.0f ? exp2f(sm.mm[bsl][w][lane] - Mx) : 0.0f;
+        L = __fadd_rn(L, __fmul_rn(bl, wreg[w]));
+      }
+    } else {
+#pragma unroll
+      for (int w = 0; w < kStreamConsumers; ++w) wreg[w] = 0.0f;
+    }
+    float* wsrow = P.ws + ((size_t(lr) * G + g) * P.S + j) * 8 * wrl;
+#pragma unroll 1
+    for (int h = 0; h < 8; ++h) {
+      float wa[kStreamConsumers];
+#pragma unroll
+      for (int w = 0; w < kStreamConsumers; ++w) wa[w] = __shfl_sync(0xffffffffu, wreg[w], h);
+      const float hm = __shfl_sync(0xffffffffu, Mx, h), hl = __shfl_sync(0xffffffffu, L, h);
+      float* row = wsrow + size_t(h) * wrl;
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const int dd = lane + 32 * x;
+        float acc = 0.0f;
+#pragma unroll
+        for (int w = 0; w < kStreamConsumers; ++w)
+          acc = __fadd_rn(acc, wa[w] != 0.0f ? __fmul_rn(sm.mo[bsl][w][h * kORow + dd], wa[w]) : 0.0f);
+        row[kWsO + dd] = acc;
+      }
+      if (lane == 0) {
+        row[0] = hm * kLn2;
+        row[1] = hl;
+      }
+    }
+    int bad = 0;
+#pragma unroll
+    for (int w = 0; w < kStreamConsumers; ++w) bad |= sm.mbad[bsl][w];
+    __syncwarp();
+    if (lane == 0) sm100::mbar_arrive(&sm.mempty[bsl]);  // slot free for the consumers
+    int fold = 0;
+    if (lane == 0) {
+      if (bad)
+        raise_err(P.err, TF_ERR_NUMERIC, kNumeric, P.r[lr].rank, -1, 0, 0, 0, 0,
+                  (uint64_t((g % P.Hkv) * 8) << 32) | uint64_t(size_t(P.r[lr].rank) * P.len));
+      sm.ranks_mask |= 1u << lr;
+      // Publish the split row (release, cumulative over the warp's stores
+      // ordered by __syncwarp) and take the group's completion ticket: the
+      // CTA whose split completes the group has seen every other split.
+      const uint64_t before =
+          atom_add_acq_rel_gpu(reinterpret_cast<unsigned long long*>(P.done + size_t(lr) * G + g), 1ull);
+      if (before + 1 == uint64_t(split_count(P, lr, g)) &&
+          gridDim.x + *reinterpret_cast<volatile unsigned*>(&P.ctr[0]) < P.nitems)  // items left: fold off the tail
+        fold = atomicCAS(&P.fstate[size_t(lr) * G + g], 0u, 1u) == 0u;
+    }
+    fold = __shfl_sync(0xffffffffu, fold, 0);
+    if (fold) {
+      __threadfence();  // acquire side of the ticket for every lane's loads
+      warp_fold_group(P, lr, g);
+    }
+    if (tr && lane == 0) {
+      tr[11] += 1;
+      tr[12] += globaltimer_ns() - tm;
+      tr[13] += fold;
+    }
+  }
+}
+
 template <bool HILO>
 __global__ void __launch_bounds__(kStreamThreads, 1)
     fd_stream_kernel(const __grid_constant__ FdParams P, const __grid_constant__ FdMaps M) {
@@ -1598,21 +1711,26 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       sm100::mbar_init(&sm.full[i], 1);
       sm100::mbar_init(&sm.empty[i], kStreamConsumers);
     }
-    sm.bad = 0;
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&sm.mfull[i], kStreamConsumers);
+      sm100::mbar_init(&sm.mempty[i], 1);
+    }
     sm.ranks_mask = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (threadIdx.x == 32 * kStreamConsumers) {
+  if (threadIdx.x == 32 * kProducerWarp) {
     for (int i = 0; i < P.nlocal; ++i) {
       sm100::tma_prefetch(&M.k[i]);
       sm100::tma_prefetch(&M.v[i]);
     }
   }
   __syncthreads();
-  if (warp == kStreamConsumers) {
+  if (warp == kProducerWarp) {
     if ((threadIdx.x & 31) == 0) stream_producer(P, M, sm);
+  } else if (warp == kMergerWarp) {
+    stream_merger(P, sm);
   } else {
-    stream_consumer<HILO>(P, sm, s_wm, s_fL, s_fO);
+    stream_consumer<HILO>(P, sm);
     if (tr && threadIdx.x == 0) tr[1] = globaltimer_ns();
   }
   __syncthreads();
@@ -1918,9 +2036,9 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   const size_t ws_floats = size_t(nlocal_max) * G * S_eff * gs * ws_row(d);
   TFB_CHECK(heap_get(w, "fd.ws[" + std::to_string(ws_floats) + "]", sizeof(float) * ws_floats, &ws_off));
   // Split-fold granularity: hc heads per sub-item, a power of two dividing
-  // gs, as many as keep a warp's share at <= 8 rows (one load batch).
+  // gs, as many as keep a warp's share at <= kFoldRB rows (one load batch).
   int hc = 1;
-  while (hc * 2 <= 32 && gs % (hc * 2) == 0 && S_eff * hc * 2 <= 64) hc *= 2;
+  while (hc * 2 <= 32 && gs % (hc * 2) == 0 && S_eff * hc * 2 <= 8 * kFoldRB) hc *= 2;
   TFB_CHECK(heap_get(w, "fd.tickets[" + std::to_string(G) + "x" + std::to_string(S_eff) + "]",
                      sizeof(unsigned long long) * (nlocal_max * G * 3 + kMaxLocal), &tick_off));  // done | gtick | claims | sfc
   TFB_CHECK(heap_get(w, "fd.ctr", 64, &ctr_off));
