@@ -998,6 +998,9 @@ struct PostShared {
   int* src;
   float *wm, *fL, *fO;
 };
+// TAG: one instance per calling kernel, so each is register-allocated
+// under its own caller's budget.
+template <int TAG>
 __device__ __noinline__ void fd_post_phases(const FdParams& P, unsigned ranks_mask, unsigned long long* tr,
                                             PostShared sh) {
   unsigned& s_item = *sh.item;
@@ -1241,7 +1244,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
     }
   }
   stamp(2);
-  fd_post_phases(P, ranks_mask, tr, PostShared{&s_item, &s_last, &s_src, s_wm, s_fL, s_fO});
+  fd_post_phases<0>(P, ranks_mask, tr, PostShared{&s_item, &s_last, &s_src, s_wm, s_fL, s_fO});
 }
 
 // ---- TMA-fed split partials (bf16 K/V, d = 128, 8 q-heads per KV head) ----
@@ -1286,6 +1289,8 @@ struct StreamSmem {
   float mm[2][kStreamConsumers][8], ml[2][kStreamConsumers][8];
   int mbad[2][kStreamConsumers];
   int minfo[2][2];             // lr << 24 | g (-1: end), split j
+  int freq[2];                 // per merge slot: lr << 24 | g whose last split that item was (-1: none)
+  int fold_go;                 // consumer thread 0's fold claim, broadcast over the named barrier
   int meta[kStreamStages][4];  // item (-1: end), keys | stage-in-item << 8, lr << 24 | g, split j
   uint64_t full[kStreamStages], empty[kStreamStages], mfull[2], mempty[2];
   unsigned ranks_mask;
@@ -1370,13 +1375,50 @@ __device__ void stream_producer(const FdParams& P, const FdMaps& M, StreamSmem& 
   }
 }
 
+// Inline group fold by the 8 consumer warps (split rows -> the rank's wire
+// rows / direct output, then the group's flags): the post-phase sub-item
+// fold for all gs heads at once, bitwise the same rows.
+__device__ void stream_fold_group(const FdParams& P, int lr, int g, float* s_wm, float* s_fL, float* s_fO) {
+  __threadfence();  // the claim's acquire side for every thread's row loads
+  fold_heads<4, kFoldRB>(P, lr, g, 0, P.gs, s_wm, s_fL, s_fO, /*named=*/true);
+  const int G = P.B * P.Hkv;
+  const FdRank& R = P.r[lr];
+  if (!P.push) return;
+  if (threadIdx.x == 0 && !P.direct) {
+    if (P.local_dst == (P.W >= 64 ? ~0ull : ((1ull << P.W) - 1))) __threadfence();
+    else __threadfence_system();
+  }
+  consumer_bar();
+  if (threadIdx.x < P.W && (!P.owner || int(threadIdx.x) == g % P.W)) {
+    uint64_t* f = P.flags_all[threadIdx.x] + size_t(R.rank) * G + g;
+    if (P.events_all[threadIdx.x]) P.events_all[threadIdx.x][(size_t(R.rank) * G + g) * 2] = globaltimer_ns();
+    if (P.direct) atomicAdd(reinterpret_cast<unsigned long long*>(f), 1ull);
+    else if ((P.local_dst >> threadIdx.x) & 1ull) red_release_gpu(f, 1);
+    else red_release_sys(f, 1);
+  }
+}
+
 // Consumer warp -> merge slot (no CTA-wide barrier: the merger folds it).
-__device__ __forceinline__ void stream_drop_partial(StreamSmem& sm, unsigned nitem, int lrg, int j, float m0,
-                                                    float m1, float l0, float l1, const float (&o)[8][4],
-                                                    int badl) {
+__device__ __forceinline__ void stream_drop_partial(const FdParams& P, StreamSmem& sm, unsigned nitem, int lrg,
+                                                    int j, float m0, float m1, float l0, float l1,
+                                                    const float (&o)[8][4], int badl, float* s_wm, float* s_fL,
+                                                    float* s_fO) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, t = lane & 3;
   const int bsl = int(nitem & 1u);
   sm100::mbar_wait(&sm.mempty[bsl], ((nitem >> 1) & 1u) ^ 1u);
+  // The merger's verdict on item nitem - 2 (this slot's previous item) is
+  // now visible to every consumer warp alike: did it complete a group?
+  if (nitem >= 2 && sm.freq[bsl] >= 0) {
+    if (threadIdx.x == 0) {
+      const int fr = sm.freq[bsl];
+      const int G = P.B * P.Hkv;
+      sm.fold_go = atomicCAS(&P.fstate[size_t(fr >> 24) * G + (fr & 0xffffff)], 0u, 1u) == 0u ? fr : -1;
+    }
+    consumer_bar();
+    const int fr = sm.fold_go;
+    consumer_bar();
+    if (fr >= 0) stream_fold_group(P, fr >> 24, fr & 0xffffff, s_wm, s_fL, s_fO);
+  }
 #pragma unroll
   for (int off = 4; off < 32; off <<= 1) {
     l0 += __shfl_xor_sync(0xffffffffu, l0, off);
@@ -1410,7 +1452,7 @@ __device__ __forceinline__ void stream_drop_partial(StreamSmem& sm, unsigned nit
 }
 
 template <bool HILO>
-__device__ void stream_consumer(const FdParams& P, StreamSmem& sm) {
+__device__ void stream_consumer(const FdParams& P, StreamSmem& sm, float* s_wm, float* s_fL, float* s_fO) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, t = lane & 3;
   const int tl = warp & 3;
@@ -1434,7 +1476,7 @@ __device__ void stream_consumer(const FdParams& P, StreamSmem& sm) {
     const volatile int* mt = sm.meta[st];
     const int item = mt[0], nk = mt[1] & 0xff, sidx = mt[1] >> 8, lrg = mt[2], j = mt[3];
     if (item != cur) {
-      if (cur >= 0) stream_drop_partial(sm, nitem++, cur_lrg, cur_j, m0, m1, l0, l1, o, badl);
+      if (cur >= 0) stream_drop_partial(P, sm, nitem++, cur_lrg, cur_j, m0, m1, l0, l1, o, badl, s_wm, s_fL, s_fO);
       if (item < 0) {
         // End marker for the merger, in the next slot.
         const int bsl = int(nitem & 1u);
@@ -1534,78 +1576,6 @@ __device__ void stream_consumer(const FdParams& P, StreamSmem& sm) {
   }
 }
 
-// One warp folds a whole group's split rows exactly as fd_post_phases'
-// fold_heads<4, kFoldRB> sub-items do (same per-warp row sets, same
-// ascending sums, same combine), then emits and releases the group's flags.
-__device__ void warp_fold_group(const FdParams& P, int lr, int g) {
-  const int G = P.B * P.Hkv, gs = P.gs, S = split_count(P, lr, g);
-  const int lane = threadIdx.x & 31;
-  const int wrl = ws_row(128);
-  const int wph = P.hc >= 8 ? 1 : 8 / P.hc;
-  const float* grp = P.ws + ((size_t(lr) * G + g) * P.S) * gs * wrl;
-  for (int h = 0; h < gs; ++h) {
-    float Mj[8], Lj[8], Oj[8][4];
-    for (int jj = 0; jj < wph; ++jj) {
-      float Mw = -INFINITY;
-      for (int i = jj; i < S; i += wph) {
-        const float* row = grp + (size_t(i) * gs + h) * wrl;
-        if (__ldcg(row + 1) != 0.0f) Mw = fmaxf(Mw, __ldcg(row));
-      }
-      float L = 0.0f, O[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int i = jj; i < S; i += wph) {
-        const float* row = grp + (size_t(i) * gs + h) * wrl;
-        const float m = __ldcg(row), l = __ldcg(row + 1);
-        const float w = l != 0.0f ? expf(m - Mw) : 0.0f;
-        L = __fadd_rn(L, __fmul_rn(l, w));
-#pragma unroll
-        for (int x = 0; x < 4; ++x) O[x] = __fadd_rn(O[x], __fmul_rn(__ldcg(row + kWsO + lane + 32 * x), w));
-      }
-      Mj[jj] = Mw;
-      Lj[jj] = L;
-#pragma unroll
-      for (int x = 0; x < 4; ++x) Oj[jj][x] = O[x];
-    }
-    float M, LL, OO[4];
-    if (wph == 1) {
-      M = Mj[0];
-      LL = Lj[0];
-#pragma unroll
-      for (int x = 0; x < 4; ++x) OO[x] = Oj[0][x];
-    } else {
-      M = -INFINITY;
-      for (int y = 0; y < wph; ++y)
-        if (Lj[y] != 0.0f) M = fmaxf(M, Mj[y]);
-      LL = 0.0f;
-#pragma unroll
-      for (int x = 0; x < 4; ++x) OO[x] = 0.0f;
-      for (int y = 0; y < wph; ++y) {
-        if (Lj[y] == 0.0f) continue;
-        const float a = expf(Mj[y] - M);
-        LL = __fadd_rn(LL, __fmul_rn(Lj[y], a));
-#pragma unroll
-        for (int x = 0; x < 4; ++x) OO[x] = __fadd_rn(OO[x], __fmul_rn(Oj[y][x], a));
-      }
-    }
-    emit_wire_row<4>(P, lr, g, h, M, LL, OO, lane);
-  }
-  if (!P.push) return;
-  __syncwarp();
-  if (lane == 0 && !P.direct) {
-    if (P.local_dst == (P.W >= 64 ? ~0ull : ((1ull << P.W) - 1))) __threadfence();
-    else __threadfence_system();
-  }
-  __syncwarp();
-  const FdRank& R = P.r[lr];
-  for (int dst = lane; dst < P.W; dst += 32) {
-    if (P.owner && dst != g % P.W) continue;
-    uint64_t* f = P.flags_all[dst] + size_t(R.rank) * G + g;
-    if (P.events_all[dst]) P.events_all[dst][(size_t(R.rank) * G + g) * 2] = globaltimer_ns();
-    if (P.direct) atomicAdd(reinterpret_cast<unsigned long long*>(f), 1ull);
-    else if ((P.local_dst >> dst) & 1ull) red_release_gpu(f, 1);
-    else red_release_sys(f, 1);
-  }
-}
-
 // Merger warp (kMergerWarp).
 __device__ void stream_merger(const FdParams& P, StreamSmem& sm) {
   const int lane = threadIdx.x & 31;
@@ -1638,32 +1608,39 @@ __device__ void stream_merger(const FdParams& P, StreamSmem& sm) {
       for (int w = 0; w < kStreamConsumers; ++w) wreg[w] = 0.0f;
     }
     float* wsrow = P.ws + ((size_t(lr) * G + g) * P.S + j) * 8 * wrl;
-#pragma unroll 1
+    // 8 heads x 128 d, four consecutive d per lane per head (16-byte smem
+    // and global accesses); each element the ascending-warp weighted sum.
+#pragma unroll 2
     for (int h = 0; h < 8; ++h) {
       float wa[kStreamConsumers];
 #pragma unroll
       for (int w = 0; w < kStreamConsumers; ++w) wa[w] = __shfl_sync(0xffffffffu, wreg[w], h);
       const float hm = __shfl_sync(0xffffffffu, Mx, h), hl = __shfl_sync(0xffffffffu, L, h);
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int w = 0; w < kStreamConsumers; ++w) {
+        const float4 v = *reinterpret_cast<const float4*>(&sm.mo[bsl][w][h * kORow + 4 * lane]);
+        const float a = wa[w];
+        if (a != 0.0f) {
+          acc.x = __fadd_rn(acc.x, __fmul_rn(v.x, a));
+          acc.y = __fadd_rn(acc.y, __fmul_rn(v.y, a));
+          acc.z = __fadd_rn(acc.z, __fmul_rn(v.z, a));
+          acc.w = __fadd_rn(acc.w, __fmul_rn(v.w, a));
+        } else {
+          acc.x = __fadd_rn(acc.x, 0.0f);
+          acc.y = __fadd_rn(acc.y, 0.0f);
+          acc.z = __fadd_rn(acc.z, 0.0f);
+          acc.w = __fadd_rn(acc.w, 0.0f);
+        }
+      }
       float* row = wsrow + size_t(h) * wrl;
-#pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        const int dd = lane + 32 * x;
-        float acc = 0.0f;
-#pragma unroll
-        for (int w = 0; w < kStreamConsumers; ++w)
-          acc = __fadd_rn(acc, wa[w] != 0.0f ? __fmul_rn(sm.mo[bsl][w][h * kORow + dd], wa[w]) : 0.0f);
-        row[kWsO + dd] = acc;
-      }
-      if (lane == 0) {
-        row[0] = hm * kLn2;
-        row[1] = hl;
-      }
+      *reinterpret_cast<float4*>(row + kWsO + 4 * lane) = acc;
+      if (lane == 0) *reinterpret_cast<float2*>(row) = make_float2(hm * kLn2, hl);
     }
     int bad = 0;
 #pragma unroll
     for (int w = 0; w < kStreamConsumers; ++w) bad |= sm.mbad[bsl][w];
     __syncwarp();
-    if (lane == 0) sm100::mbar_arrive(&sm.mempty[bsl]);  // slot free for the consumers
     int fold = 0;
     if (lane == 0) {
       if (bad)
@@ -1675,14 +1652,13 @@ __device__ void stream_merger(const FdParams& P, StreamSmem& sm) {
       // CTA whose split completes the group has seen every other split.
       const uint64_t before =
           atom_add_acq_rel_gpu(reinterpret_cast<unsigned long long*>(P.done + size_t(lr) * G + g), 1ull);
-      if (before + 1 == uint64_t(split_count(P, lr, g)) &&
-          gridDim.x + *reinterpret_cast<volatile unsigned*>(&P.ctr[0]) < P.nitems)  // items left: fold off the tail
-        fold = atomicCAS(&P.fstate[size_t(lr) * G + g], 0u, 1u) == 0u;
-    }
-    fold = __shfl_sync(0xffffffffu, fold, 0);
-    if (fold) {
-      __threadfence();  // acquire side of the ticket for every lane's loads
-      warp_fold_group(P, lr, g);
+      // Completed a group while compute items remain: ask the consumer
+      // warps to fold it at their next-but-one item boundary, off the tail
+      // (they claim it there; at the end, the fold phase takes it instead).
+      fold = before + 1 == uint64_t(split_count(P, lr, g)) &&
+             gridDim.x + *reinterpret_cast<volatile unsigned*>(&P.ctr[0]) < P.nitems;
+      sm.freq[bsl] = fold ? lrg : -1;
+      sm100::mbar_arrive(&sm.mempty[bsl]);  // slot (and its fold request) to the consumers
     }
     if (tr && lane == 0) {
       tr[11] += 1;
@@ -1716,6 +1692,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       sm100::mbar_init(&sm.mempty[i], 1);
     }
     sm.ranks_mask = 0;
+    sm.freq[0] = sm.freq[1] = -1;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (threadIdx.x == 32 * kProducerWarp) {
@@ -1730,7 +1707,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   } else if (warp == kMergerWarp) {
     stream_merger(P, sm);
   } else {
-    stream_consumer<HILO>(P, sm);
+    stream_consumer<HILO>(P, sm, s_wm, s_fL, s_fO);
     if (tr && threadIdx.x == 0) tr[1] = globaltimer_ns();
   }
   __syncthreads();
@@ -1740,7 +1717,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     tr[14] = smid;
     tr[2] = globaltimer_ns();
   }
-  fd_post_phases(P, sm.ranks_mask, tr, PostShared{&s_item, &s_last, &s_src, s_wm, s_fL, s_fO});
+  fd_post_phases<1>(P, sm.ranks_mask, tr, PostShared{&s_item, &s_last, &s_src, s_wm, s_fL, s_fO});
 }
 
 // Push this rank's published rows into every inbox slot `self` and signal
