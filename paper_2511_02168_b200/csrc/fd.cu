@@ -646,6 +646,147 @@ __device__ __noinline__ bool fold_group_batched(const FdParams& P, int lr, int g
     return true;
   }
 
+// d = 128 split fold, latency-lean: per warp, pass 1 reads its rows' (m, l)
+// lane-parallel (one load per 32 rows) for the max, pass 2 streams the o
+// rows as float4 per lane in batches of kFoldRB rows, every load of a batch
+// in flight, weights broadcast from the lane that loaded the row.  The same
+// arithmetic as fold_heads (wph warps per head, warp j of a head taking
+// rows j, j + wph, ...; max first; ascending weighted sums; the wph warp
+// partials combined in ascending warp order).  Eight warps work; the
+// others only join the barriers.
+__device__ __forceinline__ float4 ldcg_f4(const float* p) { return __ldcg(reinterpret_cast<const float4*>(p)); }
+
+__device__ __forceinline__ void emit_wire_row4(const FdParams& P, int lr, int g, int h, float M, float L, float4 O,
+                                               int lane) {
+  const int gs = P.gs, W = P.W, Hq = P.Hq, Hkv = P.Hkv, row_len = 130;
+  const int rank = P.r[lr].rank;
+  const int b = g / Hkv, kvh = g % Hkv;
+  const size_t base_src = size_t(rank) * P.B * Hq * row_len;
+  const size_t off = (size_t(b) * Hq + kvh * gs + h) * row_len;
+  const int hq = kvh * gs + h;
+  auto put = [&](float* r) {
+    if (lane == 0) *reinterpret_cast<float2*>(r) = make_float2(M, L);
+    reinterpret_cast<float2*>(r + 2 + 4 * lane)[0] = make_float2(O.x, O.y);
+    reinterpret_cast<float2*>(r + 2 + 4 * lane)[1] = make_float2(O.z, O.w);
+  };
+  if (P.push) {
+    for (int dst = 0; dst < W; ++dst) {
+      if (P.owner && dst != g % W) continue;  // owner-combine: the group's owner only
+      put(P.inbox_all[dst] + base_src + off);
+    }
+  } else {
+    put(P.r[lr].pub + off);
+  }
+  if (P.direct) {
+    if (L == 0.0f) {
+      if (lane == 0) raise_err(P.err, TF_ERR_EMPTY_ATTENTION, kEmpty, rank, -1, 0, 0, 0, 0, uint64_t(hq));
+      return;
+    }
+    const size_t ooff = (size_t(b) * Hq + hq) * 128 + 4 * lane;
+    void* out = P.r[lr].out;
+    store_out(out, ooff + 0, O.x / L, P.out_bf16);
+    store_out(out, ooff + 1, O.y / L, P.out_bf16);
+    store_out(out, ooff + 2, O.z / L, P.out_bf16);
+    store_out(out, ooff + 3, O.w / L, P.out_bf16);
+  }
+}
+
+__device__ __forceinline__ void fold_heads128(const FdParams& P, int lr, int g, int h0, int hc, float* s_wm,
+                                              float* s_L, float* s_O) {
+  const int G = P.B * P.Hkv, gs = P.gs, S = split_count(P, lr, g);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool act = warp < 8;
+  const int wrl = ws_row(128);
+  const float* grp = P.ws + ((size_t(lr) * G + g) * P.S) * gs * wrl;
+  const int wph = hc >= 8 ? 1 : 8 / hc;
+  auto rowp = [&](int h, int i) { return grp + (size_t(i) * gs + h) * wrl; };
+  // Warp's rows j, j + wph, ... of head h -> (Mw, L, O[4 d of this lane]).
+  auto fold_rows = [&](int h, int j, float& Mw, float& L, float4& O) {
+    const int nr = j < S ? (S - j + wph - 1) / wph : 0;
+    Mw = -INFINITY;
+    for (int u0 = 0; u0 < nr; u0 += 32) {
+      float m = -INFINITY;
+      if (u0 + lane < nr) {
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(rowp(h, j + wph * (u0 + lane))));
+        if (ml.y != 0.0f) m = ml.x;
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+      Mw = fmaxf(Mw, m);
+    }
+    L = 0.0f;
+    O = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int u0 = 0; u0 < nr; u0 += 32) {
+      float lw = 0.0f, w = 0.0f;
+      if (u0 + lane < nr) {
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(rowp(h, j + wph * (u0 + lane))));
+        lw = ml.y;
+        w = ml.y != 0.0f ? expf(ml.x - Mw) : 0.0f;
+      }
+      const int cnt = min(32, nr - u0);
+      for (int b0 = 0; b0 < cnt; b0 += kFoldRB) {
+        float4 v[kFoldRB];
+#pragma unroll
+        for (int x = 0; x < kFoldRB; ++x)
+          v[x] = b0 + x < cnt ? ldcg_f4(rowp(h, j + wph * (u0 + b0 + x)) + kWsO + 4 * lane)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int x = 0; x < kFoldRB; ++x) {
+          if (b0 + x >= cnt) break;
+          const float wx = __shfl_sync(0xffffffffu, w, b0 + x), lx = __shfl_sync(0xffffffffu, lw, b0 + x);
+          L = __fadd_rn(L, __fmul_rn(lx, wx));
+          O.x = __fadd_rn(O.x, __fmul_rn(v[x].x, wx));
+          O.y = __fadd_rn(O.y, __fmul_rn(v[x].y, wx));
+          O.z = __fadd_rn(O.z, __fmul_rn(v[x].z, wx));
+          O.w = __fadd_rn(O.w, __fmul_rn(v[x].w, wx));
+        }
+      }
+    }
+  };
+  if (wph == 1) {
+    if (!act) return;
+    for (int hh = warp; hh < hc; hh += 8) {
+      float M, L;
+      float4 O;
+      fold_rows(h0 + hh, 0, M, L, O);
+      emit_wire_row4(P, lr, g, h0 + hh, M, L, O, lane);
+    }
+    return;
+  }
+  const int hh = warp / wph, j = warp % wph, h = h0 + hh;
+  if (act) {
+    float Mw, L;
+    float4 O;
+    fold_rows(h, j, Mw, L, O);
+    if (lane == 0) {
+      s_wm[warp] = Mw;
+      s_L[warp] = L;
+    }
+    reinterpret_cast<float4*>(s_O + warp * 128)[lane] = O;
+  }
+  __syncthreads();
+  if (act && j == 0) {
+    float M = -INFINITY;
+    for (int y = 0; y < wph; ++y)
+      if (s_L[warp + y] != 0.0f) M = fmaxf(M, s_wm[warp + y]);
+    float LL = 0.0f;
+    float4 OO = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int y = 0; y < wph; ++y) {
+      const float ly = s_L[warp + y];
+      if (ly == 0.0f) continue;
+      const float a = expf(s_wm[warp + y] - M);
+      LL = __fadd_rn(LL, __fmul_rn(ly, a));
+      const float4 oy = reinterpret_cast<const float4*>(s_O + (warp + y) * 128)[lane];
+      OO.x = __fadd_rn(OO.x, __fmul_rn(oy.x, a));
+      OO.y = __fadd_rn(OO.y, __fmul_rn(oy.y, a));
+      OO.z = __fadd_rn(OO.z, __fmul_rn(oy.z, a));
+      OO.w = __fadd_rn(OO.w, __fmul_rn(oy.w, a));
+    }
+    emit_wire_row4(P, lr, g, h, M, LL, OO, lane);
+  }
+  __syncthreads();
+}
+
 // ---- cross-rank fold of one (local rank, group) ---------------------------
 // W inbox rows per q-head, folded in ascending source order with a
 // per-source wait right before each fold (flash_decode.hpp:409-418) or --
@@ -1068,7 +1209,8 @@ __device__ __noinline__ void fd_post_phases(const FdParams& P, unsigned ranks_ma
       if (s_last == 2) continue;
       if (!s_last) break;  // an error elsewhere (e.g. NumericError) ends the launch
       stamp(9);
-      if (P.d <= 128) fold_heads<4, kFoldRB>(P, lr, g, hb * P.hc, P.hc, s_wm, s_fL, s_fO);
+      if (P.d == 128) fold_heads128(P, lr, g, hb * P.hc, P.hc, s_wm, s_fL, s_fO);
+      else if (P.d <= 128) fold_heads<4, 8>(P, lr, g, hb * P.hc, P.hc, s_wm, s_fL, s_fO);
       else fold_heads<8, 4>(P, lr, g, hb * P.hc, P.hc, s_wm, s_fL, s_fO);
       stamp(8);
       // The last sub-item of a group releases its flags to every rank
@@ -1265,17 +1407,16 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
 //           ldmatrix.trans'd V.  At an item boundary each warp drops its
 //           partial into one of two merge slots and goes straight on.
 //   warp 9  merger: folds the 8 warp partials of each finished item (max
-//           first, ascending warp order) into the item's split row,
-//           publishes it (release + completion ticket), and -- when its item
-//           completed a group while compute items remain -- folds that whole
-//           group right away (the post-phase fold's exact arithmetic), so
-//           only the last groups' folds are left for the tail.
+//           first, ascending warp order) into the item's split row, frees
+//           the slot, then publishes the row (release onto the group's
+//           completion count).  The fold phase folds the groups' split rows.
 constexpr int kStreamStages = 4;
 constexpr int kStreamConsumers = 8;
 constexpr int kProducerWarp = kStreamConsumers, kMergerWarp = kStreamConsumers + 1;
 constexpr int kStreamThreads = 32 * (kStreamConsumers + 2);
 constexpr int kStageKV = 2 * 64 * 128 * 2;  // K + V of 64 keys, bf16
 constexpr int kORow = 132;                   // padded merge row (conflict-free stores)
+constexpr int kPubMax = 64;                  // merged rows the merger counts in per fence
 
 struct FdMaps {
   CUtensorMap k[kMaxLocal];  // per local rank: [B*Hkv*len keys][2 halves][64 d] bf16 view, box 64 x 64 x 2
@@ -1289,11 +1430,10 @@ struct StreamSmem {
   float mm[2][kStreamConsumers][8], ml[2][kStreamConsumers][8];
   int mbad[2][kStreamConsumers];
   int minfo[2][2];             // lr << 24 | g (-1: end), split j
-  int freq[2];                 // per merge slot: lr << 24 | g whose last split that item was (-1: none)
-  int fold_go;                 // consumer thread 0's fold claim, broadcast over the named barrier
   int meta[kStreamStages][4];  // item (-1: end), keys | stage-in-item << 8, lr << 24 | g, split j
   uint64_t full[kStreamStages], empty[kStreamStages], mfull[2], mempty[2];
   unsigned ranks_mask;
+  int npub, pub[kPubMax];  // merged split rows not yet counted in (lr << 24 | g)
 };
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
@@ -1375,29 +1515,6 @@ __device__ void stream_producer(const FdParams& P, const FdMaps& M, StreamSmem& 
   }
 }
 
-// Inline group fold by the 8 consumer warps (split rows -> the rank's wire
-// rows / direct output, then the group's flags): the post-phase sub-item
-// fold for all gs heads at once, bitwise the same rows.
-__device__ void stream_fold_group(const FdParams& P, int lr, int g, float* s_wm, float* s_fL, float* s_fO) {
-  __threadfence();  // the claim's acquire side for every thread's row loads
-  fold_heads<4, kFoldRB>(P, lr, g, 0, P.gs, s_wm, s_fL, s_fO, /*named=*/true);
-  const int G = P.B * P.Hkv;
-  const FdRank& R = P.r[lr];
-  if (!P.push) return;
-  if (threadIdx.x == 0 && !P.direct) {
-    if (P.local_dst == (P.W >= 64 ? ~0ull : ((1ull << P.W) - 1))) __threadfence();
-    else __threadfence_system();
-  }
-  consumer_bar();
-  if (threadIdx.x < P.W && (!P.owner || int(threadIdx.x) == g % P.W)) {
-    uint64_t* f = P.flags_all[threadIdx.x] + size_t(R.rank) * G + g;
-    if (P.events_all[threadIdx.x]) P.events_all[threadIdx.x][(size_t(R.rank) * G + g) * 2] = globaltimer_ns();
-    if (P.direct) atomicAdd(reinterpret_cast<unsigned long long*>(f), 1ull);
-    else if ((P.local_dst >> threadIdx.x) & 1ull) red_release_gpu(f, 1);
-    else red_release_sys(f, 1);
-  }
-}
-
 // Consumer warp -> merge slot (no CTA-wide barrier: the merger folds it).
 __device__ __forceinline__ void stream_drop_partial(const FdParams& P, StreamSmem& sm, unsigned nitem, int lrg,
                                                     int j, float m0, float m1, float l0, float l1,
@@ -1406,19 +1523,6 @@ __device__ __forceinline__ void stream_drop_partial(const FdParams& P, StreamSme
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, t = lane & 3;
   const int bsl = int(nitem & 1u);
   sm100::mbar_wait(&sm.mempty[bsl], ((nitem >> 1) & 1u) ^ 1u);
-  // The merger's verdict on item nitem - 2 (this slot's previous item) is
-  // now visible to every consumer warp alike: did it complete a group?
-  if (nitem >= 2 && sm.freq[bsl] >= 0) {
-    if (threadIdx.x == 0) {
-      const int fr = sm.freq[bsl];
-      const int G = P.B * P.Hkv;
-      sm.fold_go = atomicCAS(&P.fstate[size_t(fr >> 24) * G + (fr & 0xffffff)], 0u, 1u) == 0u ? fr : -1;
-    }
-    consumer_bar();
-    const int fr = sm.fold_go;
-    consumer_bar();
-    if (fr >= 0) stream_fold_group(P, fr >> 24, fr & 0xffffff, s_wm, s_fL, s_fO);
-  }
 #pragma unroll
   for (int off = 4; off < 32; off <<= 1) {
     l0 += __shfl_xor_sync(0xffffffffu, l0, off);
@@ -1576,6 +1680,15 @@ __device__ void stream_consumer(const FdParams& P, StreamSmem& sm, float* s_wm, 
   }
 }
 
+// Merger lane 0: fence once, then count every merged split row in.
+__device__ __forceinline__ void stream_publish(const FdParams& P, StreamSmem& sm) {
+  const int G = P.B * P.Hkv;
+  __threadfence();  // the merger warp's row stores (ordered by __syncwarp) before the counts
+  for (int i = 0; i < sm.npub; ++i)
+    atomicAdd(reinterpret_cast<unsigned long long*>(P.done + size_t(sm.pub[i] >> 24) * G + (sm.pub[i] & 0xffffff)), 1ull);
+  sm.npub = 0;
+}
+
 // Merger warp (kMergerWarp).
 __device__ void stream_merger(const FdParams& P, StreamSmem& sm) {
   const int lane = threadIdx.x & 31;
@@ -1587,7 +1700,11 @@ __device__ void stream_merger(const FdParams& P, StreamSmem& sm) {
     sm100::mbar_wait(&sm.mfull[bsl], (n >> 1) & 1u);
     const uint64_t tm = tr ? globaltimer_ns() : 0;
     const int lrg = sm.minfo[bsl][0], j = sm.minfo[bsl][1];
-    if (lrg < 0) break;
+    if (lrg < 0) {
+      __syncwarp();
+      if (lane == 0) stream_publish(P, sm);
+      break;
+    }
     const int lr = lrg >> 24, g = lrg & 0xffffff;
     // Lane h < 8: head h's max over the warps with l != 0, its per-warp
     // weights exp2(m_w - M) and L (the fold of fast_split, max first).
@@ -1641,29 +1758,21 @@ __device__ void stream_merger(const FdParams& P, StreamSmem& sm) {
 #pragma unroll
     for (int w = 0; w < kStreamConsumers; ++w) bad |= sm.mbad[bsl][w];
     __syncwarp();
-    int fold = 0;
     if (lane == 0) {
+      sm100::mbar_arrive(&sm.mempty[bsl]);  // slot free: the consumers never wait on the publish below
       if (bad)
         raise_err(P.err, TF_ERR_NUMERIC, kNumeric, P.r[lr].rank, -1, 0, 0, 0, 0,
                   (uint64_t((g % P.Hkv) * 8) << 32) | uint64_t(size_t(P.r[lr].rank) * P.len));
       sm.ranks_mask |= 1u << lr;
-      // Publish the split row (release, cumulative over the warp's stores
-      // ordered by __syncwarp) and take the group's completion ticket: the
-      // CTA whose split completes the group has seen every other split.
-      const uint64_t before =
-          atom_add_acq_rel_gpu(reinterpret_cast<unsigned long long*>(P.done + size_t(lr) * G + g), 1ull);
-      // Completed a group while compute items remain: ask the consumer
-      // warps to fold it at their next-but-one item boundary, off the tail
-      // (they claim it there; at the end, the fold phase takes it instead).
-      fold = before + 1 == uint64_t(split_count(P, lr, g)) &&
-             gridDim.x + *reinterpret_cast<volatile unsigned*>(&P.ctr[0]) < P.nitems;
-      sm.freq[bsl] = fold ? lrg : -1;
-      sm100::mbar_arrive(&sm.mempty[bsl]);  // slot (and its fold request) to the consumers
+      // Publish later: the row's completion count goes up after one fence
+      // for a batch of rows (the fold phase starts only when the compute
+      // is over anyway), so the merger never waits out a release per item.
+      sm.pub[sm.npub++] = lrg;
+      if (sm.npub == kPubMax) stream_publish(P, sm);
     }
     if (tr && lane == 0) {
       tr[11] += 1;
       tr[12] += globaltimer_ns() - tm;
-      tr[13] += fold;
     }
   }
 }
@@ -1692,7 +1801,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       sm100::mbar_init(&sm.mempty[i], 1);
     }
     sm.ranks_mask = 0;
-    sm.freq[0] = sm.freq[1] = -1;
+    sm.npub = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (threadIdx.x == 32 * kProducerWarp) {
@@ -1851,10 +1960,9 @@ static tf_status fd_kv_map(CUtensorMap* m, const void* base, size_t rows) {
 // Item table of fd_stream_kernel: a fixed function of the shape and the
 // grid, so every run cuts the same splits (bitwise-reproducible partials
 // whatever CTA computes them).  Guided sizes: each item takes
-// remaining/grid keys (rounded up to 64, at least min_keys), the (rank,
-// group) streams taking turns, so the first items are each about a CTA's
-// fair share and the last ones are small -- CTAs that claim dynamically
-// finish within about one small item of each other.
+// remaining / (div * grid) keys (rounded up to 64, at least min_keys), the
+// groups taking turns, so items shrink as the work runs out and CTAs that
+// claim dynamically finish within about one small item of each other.
 struct FdPlan {
   std::vector<uint4> items;
   std::vector<int> gS;
@@ -1866,6 +1974,11 @@ static FdPlan fd_plan(int G, size_t len, unsigned grid) {
   size_t min_keys = 256;
   if (const char* e = std::getenv("TFB_FD_MINKEYS")) min_keys = std::max<size_t>(64, std::strtoull(e, nullptr, 10));
   const bool group_major = std::getenv("TFB_FD_GROUP_MAJOR") != nullptr;
+  // Items are remaining / (div * grid): a quarter of a CTA's fair share at
+  // most, so a CTA streaming ~15 % slower than the rest (measured spread)
+  // is still rebalanced by the items after its first.
+  int div = 4;
+  if (const char* e = std::getenv("TFB_FD_CHUNKDIV")) div = std::max(1, std::atoi(e));
   const size_t ng = size_t(nlocal) * G;
   pl.gS.assign(ng, 0);
   std::vector<size_t> pos(ng, 0);
@@ -1873,7 +1986,7 @@ static FdPlan fd_plan(int G, size_t len, unsigned grid) {
   size_t gi = 0;
   while (rem > 0) {
     if (pos[gi] < len) {
-      size_t sz = (rem + grid - 1) / grid;
+      size_t sz = (rem + size_t(div) * grid - 1) / (size_t(div) * grid);
       sz = std::max(min_keys, (sz + 63) / 64 * 64);
       sz = std::min(sz, len - pos[gi]);
       const unsigned lr = unsigned(gi / G), g = unsigned(gi % G);
@@ -2154,7 +2267,6 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
           Q.items = reinterpret_cast<const uint4*>(w->ptr(lead, items_off));
           Q.gS = reinterpret_cast<const int*>(Q.items + plan.items.size());
           Q.nitems = unsigned(plan.items.size()) * unsigned(Q.nlocal);
-          Q.fstate = reinterpret_cast<unsigned*>(w->ptr(lead, fstate_off));
         }
         cudaSetDevice(kv.first);
         // Every co-located rank's inputs may come from its own stream: the
