@@ -115,6 +115,7 @@ struct FdParams {
   unsigned nitems;
   const int* gS;
   unsigned* fstate;
+  float* mslots;  // fd_stream_kernel: [grid][kMSlots][8 warps][m[8] l[8] o[8][128]] warp partials
   FdRank r[kMaxLocal];
 };
 
@@ -1410,13 +1411,15 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
 //           first, ascending warp order) into the item's split row, frees
 //           the slot, then publishes the row (release onto the group's
 //           completion count).  The fold phase folds the groups' split rows.
-constexpr int kStreamStages = 4;
+constexpr int kStreamStages = 6;
 constexpr int kStreamConsumers = 8;
 constexpr int kProducerWarp = kStreamConsumers, kMergerWarp = kStreamConsumers + 1;
 constexpr int kStreamThreads = 32 * (kStreamConsumers + 2);
 constexpr int kStageKV = 2 * 64 * 128 * 2;  // K + V of 64 keys, bf16
 constexpr int kORow = 132;                   // padded merge row (conflict-free stores)
 constexpr int kPubMax = 64;                  // merged rows the merger counts in per fence
+constexpr int kMSlots = 4;                   // merge slots per CTA (global scratch, L2-resident)
+constexpr int kMSlotWarp = 16 + 8 * 128;     // floats per warp partial in a slot: m[8] l[8] o[8][128]
 
 struct FdMaps {
   CUtensorMap k[kMaxLocal];  // per local rank: [B*Hkv*len keys][2 halves][64 d] bf16 view, box 64 x 64 x 2
@@ -1426,12 +1429,10 @@ struct FdMaps {
 struct StreamSmem {
   uint8_t kv[kStreamStages][kStageKV];  // 1024-aligned: [K half0 | K half1 | V half0 | V half1], 8 KB each
   uint8_t q[kStreamStages][8 * 128 * 2];
-  float mo[2][kStreamConsumers][8 * kORow];  // merge slots: per warp o[head][d]
-  float mm[2][kStreamConsumers][8], ml[2][kStreamConsumers][8];
-  int mbad[2][kStreamConsumers];
-  int minfo[2][2];             // lr << 24 | g (-1: end), split j
+  int mbad[kMSlots][kStreamConsumers];
+  int minfo[kMSlots][2];       // lr << 24 | g (-1: end), split j
   int meta[kStreamStages][4];  // item (-1: end), keys | stage-in-item << 8, lr << 24 | g, split j
-  uint64_t full[kStreamStages], empty[kStreamStages], mfull[2], mempty[2];
+  uint64_t full[kStreamStages], empty[kStreamStages], mfull[kMSlots], mempty[kMSlots];
   unsigned ranks_mask;
   int npub, pub[kPubMax];  // merged split rows not yet counted in (lr << 24 | g)
 };
@@ -1515,33 +1516,36 @@ __device__ void stream_producer(const FdParams& P, const FdMaps& M, StreamSmem& 
   }
 }
 
-// Consumer warp -> merge slot (no CTA-wide barrier: the merger folds it).
+// Consumer warp -> merge slot (global scratch; no CTA-wide barrier: the
+// merger folds it).  The slot's arrive (release, CTA scope) after
+// __syncwarp orders every lane's stores before the merger's acquire.
+__device__ __forceinline__ float* mslot_warp(const FdParams& P, int bsl, int warp) {
+  return P.mslots + ((size_t(blockIdx.x) * kMSlots + bsl) * kStreamConsumers + warp) * kMSlotWarp;
+}
 __device__ __forceinline__ void stream_drop_partial(const FdParams& P, StreamSmem& sm, unsigned nitem, int lrg,
                                                     int j, float m0, float m1, float l0, float l1,
-                                                    const float (&o)[8][4], int badl, float* s_wm, float* s_fL,
-                                                    float* s_fO) {
+                                                    const float (&o)[8][4], int badl) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, t = lane & 3;
-  const int bsl = int(nitem & 1u);
-  sm100::mbar_wait(&sm.mempty[bsl], ((nitem >> 1) & 1u) ^ 1u);
+  const int bsl = int(nitem % kMSlots);
+  sm100::mbar_wait(&sm.mempty[bsl], ((nitem / kMSlots) & 1u) ^ 1u);
 #pragma unroll
   for (int off = 4; off < 32; off <<= 1) {
     l0 += __shfl_xor_sync(0xffffffffu, l0, off);
     l1 += __shfl_xor_sync(0xffffffffu, l1, off);
   }
+  float* slot = mslot_warp(P, bsl, warp);
   if (gq == 0) {
-    sm.mm[bsl][warp][2 * t] = m0;
-    sm.mm[bsl][warp][2 * t + 1] = m1;
-    sm.ml[bsl][warp][2 * t] = l0;
-    sm.ml[bsl][warp][2 * t + 1] = l1;
+    *reinterpret_cast<float2*>(slot + 2 * t) = make_float2(m0, m1);
+    *reinterpret_cast<float2*>(slot + 8 + 2 * t) = make_float2(l0, l1);
   }
-  float* ow = sm.mo[bsl][warp];
+  float* ow = slot + 16;
 #pragma unroll
   for (int db = 0; db < 8; ++db) {
     const int dA = 16 * db + gq;
-    ow[(2 * t) * kORow + dA] = o[db][0];
-    ow[(2 * t + 1) * kORow + dA] = o[db][1];
-    ow[(2 * t) * kORow + dA + 8] = o[db][2];
-    ow[(2 * t + 1) * kORow + dA + 8] = o[db][3];
+    ow[(2 * t) * 128 + dA] = o[db][0];
+    ow[(2 * t + 1) * 128 + dA] = o[db][1];
+    ow[(2 * t) * 128 + dA + 8] = o[db][2];
+    ow[(2 * t + 1) * 128 + dA + 8] = o[db][3];
   }
   const int any_bad = __any_sync(0xffffffffu, badl);
   if (lane == 0) {
@@ -1552,11 +1556,11 @@ __device__ __forceinline__ void stream_drop_partial(const FdParams& P, StreamSme
     }
   }
   __syncwarp();
-  if (lane == 0) sm100::mbar_arrive(&sm.mfull[bsl]);  // release: this warp's slot writes
+  if (lane == 0) sm100::mbar_arrive(&sm.mfull[bsl]);
 }
 
 template <bool HILO>
-__device__ void stream_consumer(const FdParams& P, StreamSmem& sm, float* s_wm, float* s_fL, float* s_fO) {
+__device__ void stream_consumer(const FdParams& P, StreamSmem& sm) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, t = lane & 3;
   const int tl = warp & 3;
@@ -1580,11 +1584,11 @@ __device__ void stream_consumer(const FdParams& P, StreamSmem& sm, float* s_wm, 
     const volatile int* mt = sm.meta[st];
     const int item = mt[0], nk = mt[1] & 0xff, sidx = mt[1] >> 8, lrg = mt[2], j = mt[3];
     if (item != cur) {
-      if (cur >= 0) stream_drop_partial(P, sm, nitem++, cur_lrg, cur_j, m0, m1, l0, l1, o, badl, s_wm, s_fL, s_fO);
+      if (cur >= 0) stream_drop_partial(P, sm, nitem++, cur_lrg, cur_j, m0, m1, l0, l1, o, badl);
       if (item < 0) {
         // End marker for the merger, in the next slot.
-        const int bsl = int(nitem & 1u);
-        sm100::mbar_wait(&sm.mempty[bsl], ((nitem >> 1) & 1u) ^ 1u);
+        const int bsl = int(nitem % kMSlots);
+        sm100::mbar_wait(&sm.mempty[bsl], ((nitem / kMSlots) & 1u) ^ 1u);
         if (lane == 0 && warp == 0) sm.minfo[bsl][0] = -1;
         __syncwarp();
         if (lane == 0) {
@@ -1696,8 +1700,8 @@ __device__ void stream_merger(const FdParams& P, StreamSmem& sm) {
   const int wrl = ws_row(128);
   unsigned long long* tr = P.trace ? P.trace + size_t(blockIdx.x) * 16 : nullptr;
   for (unsigned n = 0;; ++n) {
-    const int bsl = int(n & 1u);
-    sm100::mbar_wait(&sm.mfull[bsl], (n >> 1) & 1u);
+    const int bsl = int(n % kMSlots);
+    sm100::mbar_wait(&sm.mfull[bsl], (n / kMSlots) & 1u);
     const uint64_t tm = tr ? globaltimer_ns() : 0;
     const int lrg = sm.minfo[bsl][0], j = sm.minfo[bsl][1];
     if (lrg < 0) {
@@ -1706,53 +1710,60 @@ __device__ void stream_merger(const FdParams& P, StreamSmem& sm) {
       break;
     }
     const int lr = lrg >> 24, g = lrg & 0xffffff;
+    const float* slot0 = mslot_warp(P, bsl, 0);
     // Lane h < 8: head h's max over the warps with l != 0, its per-warp
     // weights exp2(m_w - M) and L (the fold of fast_split, max first).
     float wreg[kStreamConsumers];
     float Mx = -INFINITY, L = 0.0f;
     if (lane < 8) {
-#pragma unroll
-      for (int w = 0; w < kStreamConsumers; ++w)
-        if (sm.ml[bsl][w][lane] != 0.0f) Mx = fmaxf(Mx, sm.mm[bsl][w][lane]);
+      float mw[kStreamConsumers], lw[kStreamConsumers];
 #pragma unroll
       for (int w = 0; w < kStreamConsumers; ++w) {
-        const float bl = sm.ml[bsl][w][lane];
-        wreg[w] = bl != 0.0f ? exp2f(sm.mm[bsl][w][lane] - Mx) : 0.0f;
-        L = __fadd_rn(L, __fmul_rn(bl, wreg[w]));
+        mw[w] = __ldcg(slot0 + w * kMSlotWarp + lane);
+        lw[w] = __ldcg(slot0 + w * kMSlotWarp + 8 + lane);
+      }
+#pragma unroll
+      for (int w = 0; w < kStreamConsumers; ++w)
+        if (lw[w] != 0.0f) Mx = fmaxf(Mx, mw[w]);
+#pragma unroll
+      for (int w = 0; w < kStreamConsumers; ++w) {
+        wreg[w] = lw[w] != 0.0f ? exp2f(mw[w] - Mx) : 0.0f;
+        L = __fadd_rn(L, __fmul_rn(lw[w], wreg[w]));
       }
     } else {
 #pragma unroll
       for (int w = 0; w < kStreamConsumers; ++w) wreg[w] = 0.0f;
     }
     float* wsrow = P.ws + ((size_t(lr) * G + g) * P.S + j) * 8 * wrl;
-    // 8 heads x 128 d, four consecutive d per lane per head (16-byte smem
-    // and global accesses); each element the ascending-warp weighted sum.
-#pragma unroll 2
-    for (int h = 0; h < 8; ++h) {
-      float wa[kStreamConsumers];
+    // 8 heads x 128 d, four consecutive d per lane per head (float4 loads
+    // of the warp partials from L2, two heads' loads in flight at a time);
+    // each element the ascending-warp weighted sum.
+#pragma unroll 1
+    for (int h = 0; h < 8; h += 2) {
+      float4 v[2][kStreamConsumers];
 #pragma unroll
-      for (int w = 0; w < kStreamConsumers; ++w) wa[w] = __shfl_sync(0xffffffffu, wreg[w], h);
-      const float hm = __shfl_sync(0xffffffffu, Mx, h), hl = __shfl_sync(0xffffffffu, L, h);
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
-      for (int w = 0; w < kStreamConsumers; ++w) {
-        const float4 v = *reinterpret_cast<const float4*>(&sm.mo[bsl][w][h * kORow + 4 * lane]);
-        const float a = wa[w];
-        if (a != 0.0f) {
-          acc.x = __fadd_rn(acc.x, __fmul_rn(v.x, a));
-          acc.y = __fadd_rn(acc.y, __fmul_rn(v.y, a));
-          acc.z = __fadd_rn(acc.z, __fmul_rn(v.z, a));
-          acc.w = __fadd_rn(acc.w, __fmul_rn(v.w, a));
-        } else {
-          acc.x = __fadd_rn(acc.x, 0.0f);
-          acc.y = __fadd_rn(acc.y, 0.0f);
-          acc.z = __fadd_rn(acc.z, 0.0f);
-          acc.w = __fadd_rn(acc.w, 0.0f);
+        for (int w = 0; w < kStreamConsumers; ++w)
+          v[hh][w] = __ldcg(reinterpret_cast<const float4*>(slot0 + w * kMSlotWarp + 16 + (h + hh) * 128) + lane);
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int hd = h + hh;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int w = 0; w < kStreamConsumers; ++w) {
+          const float a = __shfl_sync(0xffffffffu, wreg[w], hd);
+          const float4 x = v[hh][w];
+          acc.x = __fadd_rn(acc.x, a != 0.0f ? __fmul_rn(x.x, a) : 0.0f);
+          acc.y = __fadd_rn(acc.y, a != 0.0f ? __fmul_rn(x.y, a) : 0.0f);
+          acc.z = __fadd_rn(acc.z, a != 0.0f ? __fmul_rn(x.z, a) : 0.0f);
+          acc.w = __fadd_rn(acc.w, a != 0.0f ? __fmul_rn(x.w, a) : 0.0f);
         }
+        const float hm = __shfl_sync(0xffffffffu, Mx, hd), hl = __shfl_sync(0xffffffffu, L, hd);
+        float* row = wsrow + size_t(hd) * wrl;
+        *reinterpret_cast<float4*>(row + kWsO + 4 * lane) = acc;
+        if (lane == 0) *reinterpret_cast<float2*>(row) = make_float2(hm * kLn2, hl);
       }
-      float* row = wsrow + size_t(h) * wrl;
-      *reinterpret_cast<float4*>(row + kWsO + 4 * lane) = acc;
-      if (lane == 0) *reinterpret_cast<float2*>(row) = make_float2(hm * kLn2, hl);
     }
     int bad = 0;
 #pragma unroll
@@ -1796,7 +1807,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       sm100::mbar_init(&sm.full[i], 1);
       sm100::mbar_init(&sm.empty[i], kStreamConsumers);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kMSlots; ++i) {
       sm100::mbar_init(&sm.mfull[i], kStreamConsumers);
       sm100::mbar_init(&sm.mempty[i], 1);
     }
@@ -1816,7 +1827,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   } else if (warp == kMergerWarp) {
     stream_merger(P, sm);
   } else {
-    stream_consumer<HILO>(P, sm, s_wm, s_fL, s_fO);
+    stream_consumer<HILO>(P, sm);
     if (tr && threadIdx.x == 0) tr[1] = globaltimer_ns();
   }
   __syncthreads();
@@ -2134,12 +2145,14 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   TFB_CHECK(heap_get(w, "fd.ctr", 64, &ctr_off));
   // Stream kernel tables: the item plan (uploaded once per geometry, before
   // any launch uses it) and the per-(rank, group) fold claims.
-  size_t items_off = 0, fstate_off = 0;
+  size_t items_off = 0, fstate_off = 0, mslot_off = 0;
   if (stream) {
     const std::string key = std::to_string(G) + "x" + std::to_string(len) + "@" + std::to_string(w->sm_count);
     const size_t tbytes = plan.items.size() * sizeof(uint4) + size_t(G) * sizeof(int);
     TFB_CHECK(heap_get(w, "fd.items[" + key + "]", tbytes, &items_off));
     TFB_CHECK(heap_get(w, "fd.fstate[" + std::to_string(G) + "]", sizeof(unsigned) * kMaxLocal * G, &fstate_off));
+    TFB_CHECK(heap_get(w, "fd.mslots", sizeof(float) * size_t(w->sm_count) * kMSlots * kStreamConsumers * kMSlotWarp,
+                       &mslot_off));
     uint64_t& up = w->epochs["fd.items.uploaded@" + std::to_string(items_off)];
     if (!up) {
       std::vector<uint8_t> host(tbytes);
@@ -2267,6 +2280,7 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
           Q.items = reinterpret_cast<const uint4*>(w->ptr(lead, items_off));
           Q.gS = reinterpret_cast<const int*>(Q.items + plan.items.size());
           Q.nitems = unsigned(plan.items.size()) * unsigned(Q.nlocal);
+          Q.mslots = reinterpret_cast<float*>(w->ptr(lead, mslot_off));
         }
         cudaSetDevice(kv.first);
         // Every co-located rank's inputs may come from its own stream: the
