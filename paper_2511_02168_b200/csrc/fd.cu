@@ -115,7 +115,6 @@ struct FdParams {
   unsigned nitems;
   const int* gS;
   unsigned* fstate;
-  float* mslots;  // fd_stream_kernel: [grid][kMSlots][8 warps][m[8] l[8] o[8][128]] warp partials
   FdRank r[kMaxLocal];
 };
 
@@ -1181,6 +1180,7 @@ __device__ __noinline__ void fd_post_phases(const FdParams& P, unsigned ranks_ma
         continue;
       }
       const int hb = item % nhc, g = item / nhc;
+      stamp(13);
       if (threadIdx.x == 0) {
         // Intra-rank completion counter: a local spin, not a fabric signal
         // (not counted as a signal wait in the tax meter).
@@ -1232,6 +1232,7 @@ __device__ __noinline__ void fd_post_phases(const FdParams& P, unsigned ranks_ma
         s_last = (P.direct ? atomicAdd(gt, 1ull) : atom_add_acq_rel_gpu(gt, 1ull)) == uint64_t(nhc) - 1;
       }
       __syncthreads();
+      stamp(15);
       if (!P.push || !s_last) continue;
       stamp(7);
       if (threadIdx.x < P.W && (!P.owner || int(threadIdx.x) == g % P.W)) {
@@ -1411,15 +1412,15 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
 //           first, ascending warp order) into the item's split row, frees
 //           the slot, then publishes the row (release onto the group's
 //           completion count).  The fold phase folds the groups' split rows.
-constexpr int kStreamStages = 6;
+constexpr int kStreamStages = 5;
+constexpr int kStageKeys = 64;                  // keys per stage (one 32 KB TMA box of K, one of V)
+constexpr int kTPS = kStageKeys / 16;            // 16-key tiles per stage
 constexpr int kStreamConsumers = 8;
-constexpr int kProducerWarp = kStreamConsumers, kMergerWarp = kStreamConsumers + 1;
-constexpr int kStreamThreads = 32 * (kStreamConsumers + 2);
-constexpr int kStageKV = 2 * 64 * 128 * 2;  // K + V of 64 keys, bf16
+constexpr int kProducerWarp = kStreamConsumers;
+constexpr int kStreamThreads = 32 * (kStreamConsumers + 1);
+constexpr int kStageKV = 2 * kStageKeys * 128 * 2;  // K + V of a stage, bf16
 constexpr int kORow = 132;                   // padded merge row (conflict-free stores)
 constexpr int kPubMax = 64;                  // merged rows the merger counts in per fence
-constexpr int kMSlots = 4;                   // merge slots per CTA (global scratch, L2-resident)
-constexpr int kMSlotWarp = 16 + 8 * 128;     // floats per warp partial in a slot: m[8] l[8] o[8][128]
 
 struct FdMaps {
   CUtensorMap k[kMaxLocal];  // per local rank: [B*Hkv*len keys][2 halves][64 d] bf16 view, box 64 x 64 x 2
@@ -1427,12 +1428,14 @@ struct FdMaps {
 };
 
 struct StreamSmem {
-  uint8_t kv[kStreamStages][kStageKV];  // 1024-aligned: [K half0 | K half1 | V half0 | V half1], 8 KB each
+  uint8_t kv[kStreamStages][kStageKV];  // 1024-aligned: [K half0 | K half1 | V half0 | V half1], kStageKeys x 128 B each
   uint8_t q[kStreamStages][8 * 128 * 2];
-  int mbad[kMSlots][kStreamConsumers];
-  int minfo[kMSlots][2];       // lr << 24 | g (-1: end), split j
-  int meta[kStreamStages][4];  // item (-1: end), keys | stage-in-item << 8, lr << 24 | g, split j
-  uint64_t full[kStreamStages], empty[kStreamStages], mfull[kMSlots], mempty[kMSlots];
+  float mo[kStreamConsumers][8 * kORow];  // the item merge: per warp o[head][d]
+  float mm[kStreamConsumers][8], ml[kStreamConsumers][8], wa[8][kStreamConsumers];
+  float hm[8], hl[8];
+  int bad;
+  int meta[kStreamStages][4];  // item (-1: end), keys | stage-in-item << 9, lr << 24 | g, split j
+  uint64_t full[kStreamStages], empty[kStreamStages];
   unsigned ranks_mask;
   int npub, pub[kPubMax];  // merged split rows not yet counted in (lr << 24 | g)
 };
@@ -1489,13 +1492,13 @@ __device__ void stream_producer(const FdParams& P, const FdMaps& M, StreamSmem& 
       while (globaltimer_ns() - t0 < P.r[lr].skew_ns) __nanosleep(1000);
       skewed |= 1u << lr;
     }
-    for (unsigned key = e.z;; key += 64) {
+    for (unsigned key = e.z;; key += kStageKeys) {
       if (!end && key >= e.w) break;
       const int st = int(seq % kStreamStages);
       sm100::mbar_wait(&sm.empty[st], ((seq / kStreamStages) & 1u) ^ 1u);
       volatile int* mt = sm.meta[st];
       mt[0] = end ? -1 : int(it);
-      mt[1] = end ? 0 : int(min(64u, e.w - key)) | int(((key - e.z) >> 6) << 8);
+      mt[1] = end ? 0 : int(min(unsigned(kStageKeys), e.w - key)) | int(((key - e.z) / kStageKeys) << 9);
       mt[2] = int(e.x);
       mt[3] = int(e.y);
       ++seq;
@@ -1516,55 +1519,108 @@ __device__ void stream_producer(const FdParams& P, const FdMaps& M, StreamSmem& 
   }
 }
 
-// Consumer warp -> merge slot (global scratch; no CTA-wide barrier: the
-// merger folds it).  The slot's arrive (release, CTA scope) after
-// __syncwarp orders every lane's stores before the merger's acquire.
-__device__ __forceinline__ float* mslot_warp(const FdParams& P, int bsl, int warp) {
-  return P.mslots + ((size_t(blockIdx.x) * kMSlots + bsl) * kStreamConsumers + warp) * kMSlotWarp;
+// Consumer thread 0: fence once (after the barrier that ordered every
+// consumer's row stores), then count every merged split row in.
+__device__ __forceinline__ void stream_publish(const FdParams& P, StreamSmem& sm) {
+  const int G = P.B * P.Hkv;
+  __threadfence();  // every consumer's row stores (ordered by the preceding barrier) before the counts
+  for (int i = 0; i < sm.npub; ++i)
+    atomicAdd(reinterpret_cast<unsigned long long*>(P.done + size_t(sm.pub[i] >> 24) * G + (sm.pub[i] & 0xffffff)), 1ull);
+  sm.npub = 0;
 }
-__device__ __forceinline__ void stream_drop_partial(const FdParams& P, StreamSmem& sm, unsigned nitem, int lrg,
-                                                    int j, float m0, float m1, float l0, float l1,
-                                                    const float (&o)[8][4], int badl) {
+
+// The 8 consumer warps' partials of one item -> its split row (the fold of
+// fast_split: per head M = max m_w over warps with l_w != 0, weights
+// exp2(m_w - M), ascending-warp sums).  Three named barriers; the row's
+// completion count is added at the end of the compute (stream_publish), so
+// nothing here waits on the memory system -- the producer keeps filling
+// the ring meanwhile.
+__device__ __forceinline__ void stream_merge_item(const FdParams& P, StreamSmem& sm, int lrg, int j, float m0,
+                                                  float m1, float l0, float l1, const float (&o)[8][4], int badl) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, t = lane & 3;
-  const int bsl = int(nitem % kMSlots);
-  sm100::mbar_wait(&sm.mempty[bsl], ((nitem / kMSlots) & 1u) ^ 1u);
+  const int G = P.B * P.Hkv;
+  const int lr = lrg >> 24, g = lrg & 0xffffff;
 #pragma unroll
   for (int off = 4; off < 32; off <<= 1) {
     l0 += __shfl_xor_sync(0xffffffffu, l0, off);
     l1 += __shfl_xor_sync(0xffffffffu, l1, off);
   }
-  float* slot = mslot_warp(P, bsl, warp);
   if (gq == 0) {
-    *reinterpret_cast<float2*>(slot + 2 * t) = make_float2(m0, m1);
-    *reinterpret_cast<float2*>(slot + 8 + 2 * t) = make_float2(l0, l1);
+    sm.mm[warp][2 * t] = m0;
+    sm.mm[warp][2 * t + 1] = m1;
+    sm.ml[warp][2 * t] = l0;
+    sm.ml[warp][2 * t + 1] = l1;
   }
-  float* ow = slot + 16;
+  float* ow = sm.mo[warp];
 #pragma unroll
   for (int db = 0; db < 8; ++db) {
     const int dA = 16 * db + gq;
-    ow[(2 * t) * 128 + dA] = o[db][0];
-    ow[(2 * t + 1) * 128 + dA] = o[db][1];
-    ow[(2 * t) * 128 + dA + 8] = o[db][2];
-    ow[(2 * t + 1) * 128 + dA + 8] = o[db][3];
+    ow[(2 * t) * kORow + dA] = o[db][0];
+    ow[(2 * t + 1) * kORow + dA] = o[db][1];
+    ow[(2 * t) * kORow + dA + 8] = o[db][2];
+    ow[(2 * t + 1) * kORow + dA + 8] = o[db][3];
   }
-  const int any_bad = __any_sync(0xffffffffu, badl);
-  if (lane == 0) {
-    sm.mbad[bsl][warp] = any_bad;
-    if (warp == 0) {
-      sm.minfo[bsl][0] = lrg;
-      sm.minfo[bsl][1] = j;
+  if (__any_sync(0xffffffffu, badl) && lane == 0) sm.bad = 1;
+  consumer_bar();
+  if (threadIdx.x < 8) {
+    const int h = threadIdx.x;
+    float Mx = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kStreamConsumers; ++w)
+      if (sm.ml[w][h] != 0.0f) Mx = fmaxf(Mx, sm.mm[w][h]);
+    float L = 0.0f;
+#pragma unroll
+    for (int w = 0; w < kStreamConsumers; ++w) {
+      const float bl = sm.ml[w][h];
+      const float a = bl != 0.0f ? exp2f(sm.mm[w][h] - Mx) : 0.0f;
+      sm.wa[h][w] = a;
+      L = __fadd_rn(L, __fmul_rn(bl, a));
     }
+    sm.hm[h] = Mx;
+    sm.hl[h] = L;
   }
-  __syncwarp();
-  if (lane == 0) sm100::mbar_arrive(&sm.mfull[bsl]);
+  consumer_bar();
+  // 256 threads x 4 consecutive d (float4) = 8 heads x 128 d.
+  const int wrl = ws_row(128);
+  float* wsrow = P.ws + ((size_t(lr) * G + g) * P.S + j) * 8 * wrl;
+  {
+    const int h = threadIdx.x >> 5, dd = 4 * lane;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int w = 0; w < kStreamConsumers; ++w) {
+      const float a = sm.wa[h][w];
+      const float4 x = *reinterpret_cast<const float4*>(&sm.mo[w][h * kORow + dd]);
+      acc.x = __fadd_rn(acc.x, a != 0.0f ? __fmul_rn(x.x, a) : 0.0f);
+      acc.y = __fadd_rn(acc.y, a != 0.0f ? __fmul_rn(x.y, a) : 0.0f);
+      acc.z = __fadd_rn(acc.z, a != 0.0f ? __fmul_rn(x.z, a) : 0.0f);
+      acc.w = __fadd_rn(acc.w, a != 0.0f ? __fmul_rn(x.w, a) : 0.0f);
+    }
+    float* row = wsrow + size_t(h) * wrl;
+    *reinterpret_cast<float4*>(row + kWsO + dd) = acc;
+    if (lane == 0) *reinterpret_cast<float2*>(row) = make_float2(sm.hm[h] * kLn2, sm.hl[h]);
+  }
+  consumer_bar();  // the smem merge area is free again
+  if (threadIdx.x == 0) {
+    if (sm.bad) {
+      raise_err(P.err, TF_ERR_NUMERIC, kNumeric, P.r[lr].rank, -1, 0, 0, 0, 0,
+                (uint64_t((g % P.Hkv) * 8) << 32) | uint64_t(size_t(P.r[lr].rank) * P.len));
+      sm.bad = 0;
+    }
+    sm.ranks_mask |= 1u << lr;
+    sm.pub[sm.npub++] = lrg;
+    if (sm.npub == kPubMax) stream_publish(P, sm);
+  }
 }
 
 template <bool HILO>
 __device__ void stream_consumer(const FdParams& P, StreamSmem& sm) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, t = lane & 3;
-  const int tl = warp & 3;
-  const unsigned sel = unsigned(warp >> 2);
+  // Warp c takes 16-key tile c % kTPS of the stages whose index inside
+  // their item is c / kTPS modulo 8 / kTPS.
+  constexpr int kSel = kStreamConsumers / kTPS;
+  const int tl = warp % kTPS;
+  const unsigned sel = unsigned(warp / kTPS);
   const float sl2 = P.scale * kLog2e;
   // Lane-constant parts of the ldmatrix addresses (128-byte swizzle: the
   // 16-byte chunk index is XORed with the key row's low 3 bits).
@@ -1572,7 +1628,6 @@ __device__ void stream_consumer(const FdParams& P, StreamSmem& sm) {
   const uint32_t vrow = uint32_t(tl * 16 + (lane & 7) + ((lane >> 4) & 1) * 8) * 128;
   const int khi = lane >> 4, vhi = (lane >> 3) & 1, sw = lane & 7;
   int cur = -1, cur_lrg = 0, cur_j = 0;
-  unsigned nitem = 0;
   float o[8][4];
   uint32_t qb[8][2];
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
@@ -1582,19 +1637,21 @@ __device__ void stream_consumer(const FdParams& P, StreamSmem& sm) {
     sm100::mbar_wait(&sm.full[st], (seq / kStreamStages) & 1u);
     if (seq == 0 && P.trace && threadIdx.x == 0) P.trace[size_t(blockIdx.x) * 16 + 10] = globaltimer_ns();
     const volatile int* mt = sm.meta[st];
-    const int item = mt[0], nk = mt[1] & 0xff, sidx = mt[1] >> 8, lrg = mt[2], j = mt[3];
+    const int item = mt[0], nk = mt[1] & 0x1ff, sidx = mt[1] >> 9, lrg = mt[2], j = mt[3];
     if (item != cur) {
-      if (cur >= 0) stream_drop_partial(P, sm, nitem++, cur_lrg, cur_j, m0, m1, l0, l1, o, badl);
-      if (item < 0) {
-        // End marker for the merger, in the next slot.
-        const int bsl = int(nitem % kMSlots);
-        sm100::mbar_wait(&sm.mempty[bsl], ((nitem / kMSlots) & 1u) ^ 1u);
-        if (lane == 0 && warp == 0) sm.minfo[bsl][0] = -1;
-        __syncwarp();
-        if (lane == 0) {
-          sm100::mbar_arrive(&sm.mfull[bsl]);
-          sm100::mbar_arrive(&sm.empty[st]);
+      if (cur >= 0) {
+        const uint64_t tm = P.trace ? globaltimer_ns() : 0;
+        stream_merge_item(P, sm, cur_lrg, cur_j, m0, m1, l0, l1, o, badl);
+        if (P.trace && threadIdx.x == 0) {
+          unsigned long long* tr = P.trace + size_t(blockIdx.x) * 16;
+          tr[11] += 1;
+          tr[12] += globaltimer_ns() - tm;
         }
+      }
+      if (item < 0) {
+        if (threadIdx.x == 0) stream_publish(P, sm);
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&sm.empty[st]);
         break;
       }
       cur = item;
@@ -1613,13 +1670,13 @@ __device__ void stream_consumer(const FdParams& P, StreamSmem& sm) {
       badl = 0;
     }
     const int n = nk - tl * 16;  // valid keys of this warp's tile
-    if ((unsigned(sidx) & 1u) == sel && n > 0) {
+    if ((unsigned(sidx) % kSel) == sel && n > 0) {
       const uint32_t kb = sm100::smem_u32(sm.kv[st]), vb = kb + kStageKV / 2;
       float s[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         uint32_t a0, a1, a2, a3;
-        ldsm_x4(kb + (kk >> 2) * 8192 + krow + ((((2 * kk + khi) & 7) ^ sw) << 4), a0, a1, a2, a3);
+        ldsm_x4(kb + (kk >> 2) * (kStageKeys * 128) + krow + ((((2 * kk + khi) & 7) ^ sw) << 4), a0, a1, a2, a3);
         mma_bf16(s, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
       }
       const bool va = gq < n, vbk = gq + 8 < n;
@@ -1668,7 +1725,7 @@ __device__ void stream_consumer(const FdParams& P, StreamSmem& sm) {
 #pragma unroll
       for (int db = 0; db < 8; ++db) {
         uint32_t a0, a1, a2, a3;
-        ldsm_x4_t(vb + (db >> 2) * 8192 + vrow + ((((2 * db + vhi) & 7) ^ sw) << 4), a0, a1, a2, a3);
+        ldsm_x4_t(vb + (db >> 2) * (kStageKeys * 128) + vrow + ((((2 * db + vhi) & 7) ^ sw) << 4), a0, a1, a2, a3);
         if (n < 16) {  // keys past the item: P is 0 there, and V must not be Inf/NaN either
           a0 = mask_keys(a0, 2 * t, n);
           a1 = mask_keys(a1, 2 * t, n);
@@ -1681,110 +1738,6 @@ __device__ void stream_consumer(const FdParams& P, StreamSmem& sm) {
     }
     __syncwarp();
     if (lane == 0) sm100::mbar_arrive(&sm.empty[st]);
-  }
-}
-
-// Merger lane 0: fence once, then count every merged split row in.
-__device__ __forceinline__ void stream_publish(const FdParams& P, StreamSmem& sm) {
-  const int G = P.B * P.Hkv;
-  __threadfence();  // the merger warp's row stores (ordered by __syncwarp) before the counts
-  for (int i = 0; i < sm.npub; ++i)
-    atomicAdd(reinterpret_cast<unsigned long long*>(P.done + size_t(sm.pub[i] >> 24) * G + (sm.pub[i] & 0xffffff)), 1ull);
-  sm.npub = 0;
-}
-
-// Merger warp (kMergerWarp).
-__device__ void stream_merger(const FdParams& P, StreamSmem& sm) {
-  const int lane = threadIdx.x & 31;
-  const int G = P.B * P.Hkv;
-  const int wrl = ws_row(128);
-  unsigned long long* tr = P.trace ? P.trace + size_t(blockIdx.x) * 16 : nullptr;
-  for (unsigned n = 0;; ++n) {
-    const int bsl = int(n % kMSlots);
-    sm100::mbar_wait(&sm.mfull[bsl], (n / kMSlots) & 1u);
-    const uint64_t tm = tr ? globaltimer_ns() : 0;
-    const int lrg = sm.minfo[bsl][0], j = sm.minfo[bsl][1];
-    if (lrg < 0) {
-      __syncwarp();
-      if (lane == 0) stream_publish(P, sm);
-      break;
-    }
-    const int lr = lrg >> 24, g = lrg & 0xffffff;
-    const float* slot0 = mslot_warp(P, bsl, 0);
-    // Lane h < 8: head h's max over the warps with l != 0, its per-warp
-    // weights exp2(m_w - M) and L (the fold of fast_split, max first).
-    float wreg[kStreamConsumers];
-    float Mx = -INFINITY, L = 0.0f;
-    if (lane < 8) {
-      float mw[kStreamConsumers], lw[kStreamConsumers];
-#pragma unroll
-      for (int w = 0; w < kStreamConsumers; ++w) {
-        mw[w] = __ldcg(slot0 + w * kMSlotWarp + lane);
-        lw[w] = __ldcg(slot0 + w * kMSlotWarp + 8 + lane);
-      }
-#pragma unroll
-      for (int w = 0; w < kStreamConsumers; ++w)
-        if (lw[w] != 0.0f) Mx = fmaxf(Mx, mw[w]);
-#pragma unroll
-      for (int w = 0; w < kStreamConsumers; ++w) {
-        wreg[w] = lw[w] != 0.0f ? exp2f(mw[w] - Mx) : 0.0f;
-        L = __fadd_rn(L, __fmul_rn(lw[w], wreg[w]));
-      }
-    } else {
-#pragma unroll
-      for (int w = 0; w < kStreamConsumers; ++w) wreg[w] = 0.0f;
-    }
-    float* wsrow = P.ws + ((size_t(lr) * G + g) * P.S + j) * 8 * wrl;
-    // 8 heads x 128 d, four consecutive d per lane per head (float4 loads
-    // of the warp partials from L2, two heads' loads in flight at a time);
-    // each element the ascending-warp weighted sum.
-#pragma unroll 1
-    for (int h = 0; h < 8; h += 2) {
-      float4 v[2][kStreamConsumers];
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-        for (int w = 0; w < kStreamConsumers; ++w)
-          v[hh][w] = __ldcg(reinterpret_cast<const float4*>(slot0 + w * kMSlotWarp + 16 + (h + hh) * 128) + lane);
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const int hd = h + hh;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int w = 0; w < kStreamConsumers; ++w) {
-          const float a = __shfl_sync(0xffffffffu, wreg[w], hd);
-          const float4 x = v[hh][w];
-          acc.x = __fadd_rn(acc.x, a != 0.0f ? __fmul_rn(x.x, a) : 0.0f);
-          acc.y = __fadd_rn(acc.y, a != 0.0f ? __fmul_rn(x.y, a) : 0.0f);
-          acc.z = __fadd_rn(acc.z, a != 0.0f ? __fmul_rn(x.z, a) : 0.0f);
-          acc.w = __fadd_rn(acc.w, a != 0.0f ? __fmul_rn(x.w, a) : 0.0f);
-        }
-        const float hm = __shfl_sync(0xffffffffu, Mx, hd), hl = __shfl_sync(0xffffffffu, L, hd);
-        float* row = wsrow + size_t(hd) * wrl;
-        *reinterpret_cast<float4*>(row + kWsO + 4 * lane) = acc;
-        if (lane == 0) *reinterpret_cast<float2*>(row) = make_float2(hm * kLn2, hl);
-      }
-    }
-    int bad = 0;
-#pragma unroll
-    for (int w = 0; w < kStreamConsumers; ++w) bad |= sm.mbad[bsl][w];
-    __syncwarp();
-    if (lane == 0) {
-      sm100::mbar_arrive(&sm.mempty[bsl]);  // slot free: the consumers never wait on the publish below
-      if (bad)
-        raise_err(P.err, TF_ERR_NUMERIC, kNumeric, P.r[lr].rank, -1, 0, 0, 0, 0,
-                  (uint64_t((g % P.Hkv) * 8) << 32) | uint64_t(size_t(P.r[lr].rank) * P.len));
-      sm.ranks_mask |= 1u << lr;
-      // Publish later: the row's completion count goes up after one fence
-      // for a batch of rows (the fold phase starts only when the compute
-      // is over anyway), so the merger never waits out a release per item.
-      sm.pub[sm.npub++] = lrg;
-      if (sm.npub == kPubMax) stream_publish(P, sm);
-    }
-    if (tr && lane == 0) {
-      tr[11] += 1;
-      tr[12] += globaltimer_ns() - tm;
-    }
   }
 }
 
@@ -1807,10 +1760,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       sm100::mbar_init(&sm.full[i], 1);
       sm100::mbar_init(&sm.empty[i], kStreamConsumers);
     }
-    for (int i = 0; i < kMSlots; ++i) {
-      sm100::mbar_init(&sm.mfull[i], kStreamConsumers);
-      sm100::mbar_init(&sm.mempty[i], 1);
-    }
+    sm.bad = 0;
     sm.ranks_mask = 0;
     sm.npub = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1824,8 +1774,6 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   __syncthreads();
   if (warp == kProducerWarp) {
     if ((threadIdx.x & 31) == 0) stream_producer(P, M, sm);
-  } else if (warp == kMergerWarp) {
-    stream_merger(P, sm);
   } else {
     stream_consumer<HILO>(P, sm);
     if (tr && threadIdx.x == 0) tr[1] = globaltimer_ns();
@@ -1958,7 +1906,7 @@ static tf_status fd_kv_map(CUtensorMap* m, const void* base, size_t rows) {
   if (!enc) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {64, rows, 2};
   cuuint64_t strides[2] = {256, 128};
-  cuuint32_t box[3] = {64, 64, 2};
+  cuuint32_t box[3] = {64, uint32_t(kStageKeys), 2};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -2145,14 +2093,12 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   TFB_CHECK(heap_get(w, "fd.ctr", 64, &ctr_off));
   // Stream kernel tables: the item plan (uploaded once per geometry, before
   // any launch uses it) and the per-(rank, group) fold claims.
-  size_t items_off = 0, fstate_off = 0, mslot_off = 0;
+  size_t items_off = 0, fstate_off = 0;
   if (stream) {
     const std::string key = std::to_string(G) + "x" + std::to_string(len) + "@" + std::to_string(w->sm_count);
     const size_t tbytes = plan.items.size() * sizeof(uint4) + size_t(G) * sizeof(int);
     TFB_CHECK(heap_get(w, "fd.items[" + key + "]", tbytes, &items_off));
     TFB_CHECK(heap_get(w, "fd.fstate[" + std::to_string(G) + "]", sizeof(unsigned) * kMaxLocal * G, &fstate_off));
-    TFB_CHECK(heap_get(w, "fd.mslots", sizeof(float) * size_t(w->sm_count) * kMSlots * kStreamConsumers * kMSlotWarp,
-                       &mslot_off));
     uint64_t& up = w->epochs["fd.items.uploaded@" + std::to_string(items_off)];
     if (!up) {
       std::vector<uint8_t> host(tbytes);
@@ -2280,7 +2226,6 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
           Q.items = reinterpret_cast<const uint4*>(w->ptr(lead, items_off));
           Q.gS = reinterpret_cast<const int*>(Q.items + plan.items.size());
           Q.nitems = unsigned(plan.items.size()) * unsigned(Q.nlocal);
-          Q.mslots = reinterpret_cast<float*>(w->ptr(lead, mslot_off));
         }
         cudaSetDevice(kv.first);
         // Every co-located rank's inputs may come from its own stream: the

@@ -30,14 +30,14 @@ with tf.World(1, [0], 512 << 20) as w:
     t = w.get(ptr, (4096, 16), np.uint64).astype(np.int64)
     t = t[t[:, 0] > 0]
     t0 = t[:, 0].min()
-    names = {0: "entry", 10: "first-stage", 1: "consumers-done", 2: "post-start", 9: "split-fold-start",
-             8: "split-folded", 7: "flags-released", 4: "fold-phase", 6: "exit"}
+    names = {0: "entry", 10: "first-stage", 1: "consumers-done", 2: "post-start", 13: "subitem-claimed",
+             9: "split-fold-start", 8: "split-folded", 15: "gtick-done", 7: "flags-released", 4: "fold-phase",
+             6: "exit"}
     for i, n in names.items():
         col = t[:, i]
         col = col[col > 0] - t0
         if len(col):
             print(f"{n:16s} n={len(col):4d}  min {col.min()/1e3:7.2f}  p50 {np.median(col)/1e3:7.2f}  "
                   f"max {col.max()/1e3:7.2f} us")
-    print("items/CTA: min %d p50 %d max %d; merge+inline us/CTA: p50 %.2f max %.2f; inline folds total %d" % (
-        t[:, 11].min(), np.median(t[:, 11]), t[:, 11].max(), np.median(t[:, 12]) / 1e3, t[:, 12].max() / 1e3,
-        t[:, 13].sum()))
+    print("items/CTA: min %d p50 %d max %d; merge us/CTA: p50 %.2f max %.2f" % (
+        t[:, 11].min(), np.median(t[:, 11]), t[:, 11].max(), np.median(t[:, 12]) / 1e3, t[:, 12].max() / 1e3))
