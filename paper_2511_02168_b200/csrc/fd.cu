@@ -701,38 +701,45 @@ __device__ __forceinline__ void fold_heads128(const FdParams& P, int lr, int g, 
   const int wph = hc >= 8 ? 1 : 8 / hc;
   auto rowp = [&](int h, int i) { return grp + (size_t(i) * gs + h) * wrl; };
   // Warp's rows j, j + wph, ... of head h -> (Mw, L, O[4 d of this lane]).
+  // Rows are taken 32 at a time: lane u loads row u's (m, l) while the
+  // first kFoldRB rows' o are already in flight; rows past the end load as
+  // zeros with weight 0 (adding +0 leaves every sum's bits unchanged).
   auto fold_rows = [&](int h, int j, float& Mw, float& L, float4& O) {
     const int nr = j < S ? (S - j + wph - 1) / wph : 0;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    // pass 1: the max over every row of the warp (max is order-free)
+    float2 ml0 = make_float2(0.f, 0.f);
+    float4 v[kFoldRB];
+#pragma unroll
+    for (int x = 0; x < kFoldRB; ++x) v[x] = x < nr ? ldcg_f4(rowp(h, j + wph * x) + kWsO + 4 * lane) : z4;
     Mw = -INFINITY;
     for (int u0 = 0; u0 < nr; u0 += 32) {
-      float m = -INFINITY;
-      if (u0 + lane < nr) {
-        const float2 ml = __ldcg(reinterpret_cast<const float2*>(rowp(h, j + wph * (u0 + lane))));
-        if (ml.y != 0.0f) m = ml.x;
-      }
+      float2 ml = make_float2(0.f, 0.f);
+      if (u0 + lane < nr) ml = __ldcg(reinterpret_cast<const float2*>(rowp(h, j + wph * (u0 + lane))));
+      if (u0 == 0) ml0 = ml;
+      float m = ml.y != 0.0f ? ml.x : -INFINITY;
 #pragma unroll
       for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
       Mw = fmaxf(Mw, m);
     }
+    // pass 2: ascending weighted sums, kFoldRB rows per batch
     L = 0.0f;
-    O = make_float4(0.f, 0.f, 0.f, 0.f);
+    O = z4;
     for (int u0 = 0; u0 < nr; u0 += 32) {
-      float lw = 0.0f, w = 0.0f;
-      if (u0 + lane < nr) {
-        const float2 ml = __ldcg(reinterpret_cast<const float2*>(rowp(h, j + wph * (u0 + lane))));
-        lw = ml.y;
-        w = ml.y != 0.0f ? expf(ml.x - Mw) : 0.0f;
+      float2 ml = ml0;
+      if (u0 > 0) {
+        ml = make_float2(0.f, 0.f);
+        if (u0 + lane < nr) ml = __ldcg(reinterpret_cast<const float2*>(rowp(h, j + wph * (u0 + lane))));
       }
-      const int cnt = min(32, nr - u0);
-      for (int b0 = 0; b0 < cnt; b0 += kFoldRB) {
-        float4 v[kFoldRB];
+      const float lw = ml.y, w = ml.y != 0.0f ? expf(ml.x - Mw) : 0.0f;
+      for (int b0 = 0; b0 < 32 && u0 + b0 < nr; b0 += kFoldRB) {
+        if (u0 + b0 > 0) {
 #pragma unroll
-        for (int x = 0; x < kFoldRB; ++x)
-          v[x] = b0 + x < cnt ? ldcg_f4(rowp(h, j + wph * (u0 + b0 + x)) + kWsO + 4 * lane)
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int x = 0; x < kFoldRB; ++x)
+            v[x] = u0 + b0 + x < nr ? ldcg_f4(rowp(h, j + wph * (u0 + b0 + x)) + kWsO + 4 * lane) : z4;
+        }
 #pragma unroll
         for (int x = 0; x < kFoldRB; ++x) {
-          if (b0 + x >= cnt) break;
           const float wx = __shfl_sync(0xffffffffu, w, b0 + x), lx = __shfl_sync(0xffffffffu, lw, b0 + x);
           L = __fadd_rn(L, __fmul_rn(lx, wx));
           O.x = __fadd_rn(O.x, __fmul_rn(v[x].x, wx));
@@ -1479,12 +1486,17 @@ __device__ __forceinline__ uint4 stream_item(const FdParams& P, unsigned it) {
 __device__ void stream_producer(const FdParams& P, const FdMaps& M, StreamSmem& sm) {
   unsigned seq = 0, skewed = 0;
   const uint64_t t0 = globaltimer_ns();
-  unsigned it = blockIdx.x;  // first item: static; later ones claimed one item ahead
+  // First item static (blockIdx.x); later ones claimed two items ahead so
+  // that both the claim and the table-entry load of the next item have
+  // long landed when the current item's last stage is issued.  Claims only
+  // increase, so stopping at the first claim >= nitems loses no item.
+  unsigned it = blockIdx.x;
   uint4 e = it < P.nitems ? stream_item(P, it) : make_uint4(0, 0, 0, 0);
+  unsigned next = it < P.nitems ? gridDim.x + atomicAdd(&P.ctr[0], 1u) : ~0u;
   for (;;) {
     const bool end = it >= P.nitems;
-    unsigned next = 0;
-    if (!end) next = gridDim.x + atomicAdd(&P.ctr[0], 1u);
+    uint4 e_next = make_uint4(0, 0, 0, 0);
+    unsigned next2 = ~0u;
     const int lr = int(e.x >> 24), g = int(e.x & 0xffffffu);
     const int b = g / P.Hkv, kvh = g % P.Hkv;
     const unsigned row0 = unsigned(g) * unsigned(P.len);  // [B][Hkv][len] rows: (b * Hkv + kvh) * len
@@ -1510,12 +1522,20 @@ __device__ void stream_producer(const FdParams& P, const FdMaps& M, StreamSmem& 
       sm100::mbar_arrive_expect_tx(&sm.full[st], kStageKV + (first ? 2048u : 0u));
       tma_load_3d(sm.kv[st], &M.k[lr], &sm.full[st], 0, int(row0 + key), 0);
       tma_load_3d(sm.kv[st] + kStageKV / 2, &M.v[lr], &sm.full[st], 0, int(row0 + key), 0);
-      if (first)
+      if (first) {
         bulk_load(sm.q[st], static_cast<const __nv_bfloat16*>(P.r[lr].q) + (size_t(b) * P.Hq + kvh * 8) * 128, 2048,
                   &sm.full[st]);
+        // The item after next: claimed now, its successor's table entry
+        // loaded now -- neither is waited on before this item is issued.
+        if (next < P.nitems) {
+          e_next = stream_item(P, next);
+          next2 = gridDim.x + atomicAdd(&P.ctr[0], 1u);
+        }
+      }
     }
     it = next;
-    if (it < P.nitems) e = stream_item(P, it);
+    e = e_next;
+    next = next2;
   }
 }
 
