@@ -57,6 +57,7 @@ namespace {
 
 constexpr int kMaxLocal = 16;  // local ranks per launch (loopback worlds)
 constexpr int kFoldRB = 16;    // rows per warp per load batch in the split folds
+constexpr int kTraceSlots = 32;  // TFB_TRACE: %globaltimer stamps per CTA
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -206,7 +207,7 @@ __host__ __device__ __forceinline__ int ws_row(int d) { return d + kWsO; }
 
 // TFB_TRACE phase stamp (slot i of this CTA's 16), for tools/fd_trace.py.
 __device__ __forceinline__ void trace_at(const FdParams& P, int i) {
-  if (P.trace && threadIdx.x == 0) P.trace[size_t(blockIdx.x) * 16 + i] = globaltimer_ns();
+  if (P.trace && threadIdx.x == 0) P.trace[size_t(blockIdx.x) * kTraceSlots + i] = globaltimer_ns();
 }
 
 // ---- generic split partial: one warp per q-head ----------------------------
@@ -504,8 +505,8 @@ __device__ void fast_split(const FdParams& P, int lr, int g, int sp, float* wsro
       lo = min(lo, sm.wend[w]);
       hi = max(hi, sm.wend[w]);
     }
-    P.trace[size_t(blockIdx.x) * 16 + 10] = lo;
-    P.trace[size_t(blockIdx.x) * 16 + 11] = hi;
+    P.trace[size_t(blockIdx.x) * kTraceSlots + 10] = lo;
+    P.trace[size_t(blockIdx.x) * kTraceSlots + 11] = hi;
   }
   if (sm.bad) {
     if (threadIdx.x == 0)
@@ -722,6 +723,7 @@ __device__ __forceinline__ void fold_heads128(const FdParams& P, int lr, int g, 
       for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
       Mw = fmaxf(Mw, m);
     }
+    trace_at(P, 16);
     // pass 2: ascending weighted sums, kFoldRB rows per batch
     L = 0.0f;
     O = z4;
@@ -765,6 +767,7 @@ __device__ __forceinline__ void fold_heads128(const FdParams& P, int lr, int g, 
     float Mw, L;
     float4 O;
     fold_rows(h, j, Mw, L, O);
+    trace_at(P, 17);
     if (lane == 0) {
       s_wm[warp] = Mw;
       s_L[warp] = L;
@@ -772,6 +775,7 @@ __device__ __forceinline__ void fold_heads128(const FdParams& P, int lr, int g, 
     reinterpret_cast<float4*>(s_O + warp * 128)[lane] = O;
   }
   __syncthreads();
+  trace_at(P, 18);
   if (act && j == 0) {
     float M = -INFINITY;
     for (int y = 0; y < wph; ++y)
@@ -1348,7 +1352,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
   const int G = P.B * P.Hkv;
   const unsigned total = unsigned(P.nlocal) * G * P.S;
   const int d = P.d, row_len = d + 2, wrl = ws_row(d);
-  unsigned long long* tr = P.trace ? P.trace + size_t(blockIdx.x) * 16 : nullptr;
+  unsigned long long* tr = P.trace ? P.trace + size_t(blockIdx.x) * kTraceSlots : nullptr;
   auto stamp = [&](int i) {
     if (tr && threadIdx.x == 0) tr[i] = globaltimer_ns();
   };
@@ -1357,7 +1361,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
   __shared__ unsigned long long s_t0;  // CTA entry time (straggler model)
   if (threadIdx.x == 0) s_t0 = globaltimer_ns();
   if (tr && threadIdx.x == 0)
-    for (int i = 1; i < 16; ++i)
+    for (int i = 1; i < kTraceSlots; ++i)
       if (i != 12 && i != 13) tr[i] = 0;
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(&P.ctr[0], 1u);
@@ -1655,7 +1659,7 @@ __device__ void stream_consumer(const FdParams& P, StreamSmem& sm) {
   for (unsigned seq = 0;; ++seq) {
     const int st = int(seq % kStreamStages);
     sm100::mbar_wait(&sm.full[st], (seq / kStreamStages) & 1u);
-    if (seq == 0 && P.trace && threadIdx.x == 0) P.trace[size_t(blockIdx.x) * 16 + 10] = globaltimer_ns();
+    if (seq == 0 && P.trace && threadIdx.x == 0) P.trace[size_t(blockIdx.x) * kTraceSlots + 10] = globaltimer_ns();
     const volatile int* mt = sm.meta[st];
     const int item = mt[0], nk = mt[1] & 0x1ff, sidx = mt[1] >> 9, lrg = mt[2], j = mt[3];
     if (item != cur) {
@@ -1663,7 +1667,7 @@ __device__ void stream_consumer(const FdParams& P, StreamSmem& sm) {
         const uint64_t tm = P.trace ? globaltimer_ns() : 0;
         stream_merge_item(P, sm, cur_lrg, cur_j, m0, m1, l0, l1, o, badl);
         if (P.trace && threadIdx.x == 0) {
-          unsigned long long* tr = P.trace + size_t(blockIdx.x) * 16;
+          unsigned long long* tr = P.trace + size_t(blockIdx.x) * kTraceSlots;
           tr[11] += 1;
           tr[12] += globaltimer_ns() - tm;
         }
@@ -1769,10 +1773,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   __shared__ unsigned int s_item;
   __shared__ int s_last, s_src;
   __shared__ float s_wm[8], s_fL[8], s_fO[8 * 256];
-  unsigned long long* tr = P.trace ? P.trace + size_t(blockIdx.x) * 16 : nullptr;
+  unsigned long long* tr = P.trace ? P.trace + size_t(blockIdx.x) * kTraceSlots : nullptr;
   if (tr && threadIdx.x == 0) {
     tr[0] = globaltimer_ns();
-    for (int i = 1; i < 16; ++i) tr[i] = 0;
+    for (int i = 1; i < kTraceSlots; ++i) tr[i] = 0;
   }
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
@@ -2224,7 +2228,7 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
         Q.ws = reinterpret_cast<float*>(w->ptr(lead, ws_off));
         if (std::getenv("TFB_TRACE")) {
           size_t toff;
-          TFB_CHECK(heap_get(w, "fd.trace", sizeof(unsigned long long) * 16 * 4096, &toff));
+          TFB_CHECK(heap_get(w, "fd.trace", sizeof(unsigned long long) * kTraceSlots * 4096, &toff));
           Q.trace = reinterpret_cast<unsigned long long*>(w->ptr(lead, toff));
         }
         Q.done = reinterpret_cast<uint64_t*>(w->ptr(lead, tick_off));

@@ -18,8 +18,8 @@ with tf.World(1, [0], 512 << 20) as w:
             _abi.ptr_array([v.data_ptr()]), _abi.ptr_array([out.data_ptr()]), None, None)
     for _ in range(3):
         _abi.check(w.lib.tf_flash_decode(*args))
-    ptr = w.alloc("fd.trace", 8 * 16 * 4096)[0]
-    t = w.get(ptr, (4096, 16), np.uint64).astype(np.int64)
+    ptr = w.alloc("fd.trace", 8 * 32 * 4096)[0]
+    t = w.get(ptr, (4096, 32), np.uint64).astype(np.int64)
     t = t[t[:, 0] > 0]
     t0 = t[:, 0].min()
     names = ["entry", "computed", "split-published", "flags+early-fold", "fold-phase", "fold-item", "exit",

@@ -26,12 +26,13 @@ with tf.World(1, [0], 512 << 20) as w:
             _abi.ptr_array([v.data_ptr()]), _abi.ptr_array([out.data_ptr()]), None, None)
     for _ in range(4):
         _abi.check(w.lib.tf_flash_decode(*args))
-    ptr = w.alloc("fd.trace", 8 * 16 * 4096)[0]
-    t = w.get(ptr, (4096, 16), np.uint64).astype(np.int64)
+    ptr = w.alloc("fd.trace", 8 * 32 * 4096)[0]
+    t = w.get(ptr, (4096, 32), np.uint64).astype(np.int64)
     t = t[t[:, 0] > 0]
     t0 = t[:, 0].min()
     names = {0: "entry", 10: "first-stage", 1: "consumers-done", 2: "post-start", 13: "subitem-claimed",
-             9: "split-fold-start", 8: "split-folded", 15: "gtick-done", 7: "flags-released", 4: "fold-phase",
+             9: "split-fold-start", 16: "fold-max-done", 17: "fold-rows-done", 18: "fold-combined",
+             8: "split-folded", 15: "gtick-done", 7: "flags-released", 4: "fold-phase",
              6: "exit"}
     for i, n in names.items():
         col = t[:, i]
