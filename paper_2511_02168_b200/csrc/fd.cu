@@ -288,11 +288,11 @@ __device__ __forceinline__ uint32_t movtrans(uint32_t x) {
   return y;
 }
 
-__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+__device__ __forceinline__ uint4 ldg_stream(const void* p, uint64_t pol) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
+               : "l"(p), "l"(pol));
   return r;
 }
 
@@ -329,6 +329,8 @@ __device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
   int badl = 0;
   const uint4 z = make_uint4(0, 0, 0, 0);
+  uint64_t pol;  // K/V read once: L2 evict-first (see l2_evict_first_policy)
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   uint4 k_a[4], k_b[4], v_a[4], v_b[4];
   // Row a of each 16-key tile is key j0 + gq, row b is j0 + gq + 8: one
   // pointer per stream, lane slice folded in, tile/row/chunk offsets as
@@ -343,13 +345,13 @@ __device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
     const bool va = rem > 0, vb = rem > 8;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      k_a[i] = va ? ldg_stream(kp + 32 * i) : z;
-      k_b[i] = vb ? ldg_stream(kp + 8 * 128 + 32 * i) : z;
+      k_a[i] = va ? ldg_stream(kp + 32 * i, pol) : z;
+      k_b[i] = vb ? ldg_stream(kp + 8 * 128 + 32 * i, pol) : z;
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      v_a[i] = va ? ldg_stream(vp + 32 * i) : z;
-      v_b[i] = vb ? ldg_stream(vp + 8 * 128 + 32 * i) : z;
+      v_a[i] = va ? ldg_stream(vp + 32 * i, pol) : z;
+      v_b[i] = vb ? ldg_stream(vp + 8 * 128 + 32 * i, pol) : z;
     }
     // S^T = K . Q^T over 8 k-steps of 16 d.
     float s[4] = {0.f, 0.f, 0.f, 0.f};
@@ -1451,12 +1453,20 @@ struct StreamSmem {
   int npub, pub[kPubMax];  // merged split rows not yet counted in (lr << 24 | g)
 };
 
+// K/V are read once: stream them with an L2 evict-first policy, so the
+// half-gigabyte pass does not flush what the tail needs from L2 (the split
+// rows, the item table, the kernel's own code).
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                            int c2) {
+                                            int c2, uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-      "[%5];" ::"r"(sm100::smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(sm100::smem_u32(bar))
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3, %4}], [%5], %6;" ::"r"(sm100::smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(sm100::smem_u32(bar)), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -1490,6 +1500,7 @@ __device__ __forceinline__ uint4 stream_item(const FdParams& P, unsigned it) {
 __device__ void stream_producer(const FdParams& P, const FdMaps& M, StreamSmem& sm) {
   unsigned seq = 0, skewed = 0;
   const uint64_t t0 = globaltimer_ns();
+  const uint64_t pol = l2_evict_first_policy();
   // First item static (blockIdx.x); later ones claimed two items ahead so
   // that both the claim and the table-entry load of the next item have
   // long landed when the current item's last stage is issued.  Claims only
@@ -1524,8 +1535,8 @@ __device__ void stream_producer(const FdParams& P, const FdMaps& M, StreamSmem& 
       }
       const bool first = key == e.z;
       sm100::mbar_arrive_expect_tx(&sm.full[st], kStageKV + (first ? 2048u : 0u));
-      tma_load_3d(sm.kv[st], &M.k[lr], &sm.full[st], 0, int(row0 + key), 0);
-      tma_load_3d(sm.kv[st] + kStageKV / 2, &M.v[lr], &sm.full[st], 0, int(row0 + key), 0);
+      tma_load_3d(sm.kv[st], &M.k[lr], &sm.full[st], 0, int(row0 + key), 0, pol);
+      tma_load_3d(sm.kv[st] + kStageKV / 2, &M.v[lr], &sm.full[st], 0, int(row0 + key), 0, pol);
       if (first) {
         bulk_load(sm.q[st], static_cast<const __nv_bfloat16*>(P.r[lr].q) + (size_t(b) * P.Hq + kvh * 8) * 128, 2048,
                   &sm.full[st]);
