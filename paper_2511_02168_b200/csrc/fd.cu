@@ -1242,7 +1242,10 @@ __device__ __noinline__ void fd_post_phases(const FdParams& P, unsigned ranks_ma
           else __threadfence_system();
         }
         unsigned long long* gt = reinterpret_cast<unsigned long long*>(P.gtick + size_t(lr) * G + g);
-        s_last = (P.direct ? atomicAdd(gt, 1ull) : atom_add_acq_rel_gpu(gt, 1ull)) == uint64_t(nhc) - 1;
+        // direct (W = 1): the flag only records "the group landed" for the
+        // flag snapshot -- nobody waits on it -- so head block 0 raises it
+        // without a round trip on the ticket.
+        s_last = P.direct ? hb == 0 : atom_add_acq_rel_gpu(gt, 1ull) == uint64_t(nhc) - 1;
       }
       __syncthreads();
       stamp(15);
@@ -1707,13 +1710,21 @@ __device__ void stream_consumer(const FdParams& P, StreamSmem& sm) {
     const int n = nk - tl * 16;  // valid keys of this warp's tile
     if ((unsigned(sidx) % kSel) == sel && n > 0) {
       const uint32_t kb = sm100::smem_u32(sm.kv[st]), vb = kb + kStageKV / 2;
-      float s[4] = {0.f, 0.f, 0.f, 0.f};
+      // S^T over 8 k-steps of 16 d as four independent accumulator chains
+      // (k-steps c, c + 4), summed in a fixed order: half the dependent
+      // MMA latency per tile of one 8-step chain.
+      float sc[4][4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sc[c][0] = sc[c][1] = sc[c][2] = sc[c][3] = 0.f;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         uint32_t a0, a1, a2, a3;
         ldsm_x4(kb + (kk >> 2) * (kStageKeys * 128) + krow + ((((2 * kk + khi) & 7) ^ sw) << 4), a0, a1, a2, a3);
-        mma_bf16(s, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+        mma_bf16(sc[kk & 3], a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
       }
+      float s[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) s[r] = (sc[0][r] + sc[1][r]) + (sc[2][r] + sc[3][r]);
       const bool va = gq < n, vbk = gq + 8 < n;
       const float x0 = va ? s[0] * sl2 : -INFINITY, x1 = va ? s[1] * sl2 : -INFINITY;
       const float x2 = vbk ? s[2] * sl2 : -INFINITY, x3 = vbk ? s[3] * sl2 : -INFINITY;
