@@ -2076,8 +2076,25 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   // TMA-fed kernel (fd_stream_kernel) with a guided item table, else the
   // register-streaming kernel with S equal splits per group.
   const bool stream = fd_stream_ok(sh, w, q, k_shard, v_shard);
+  // The plan is a function of (G, len, grid, knobs): built and uploaded
+  // once per geometry; later calls only need its size and split count.
   FdPlan plan;
-  if (stream) plan = fd_plan(G, len, unsigned(w->sm_count));
+  size_t plan_items = 0;
+  std::string plan_key;
+  if (stream) {
+    plan_key = std::to_string(G) + "x" + std::to_string(len) + "@" + std::to_string(w->sm_count);
+    for (const char* k : {"TFB_FD_MINKEYS", "TFB_FD_CHUNKDIV", "TFB_FD_GROUP_MAJOR"})
+      if (const char* e = std::getenv(k)) plan_key += std::string(",") + k + "=" + e;
+    uint64_t& n = w->epochs["fd.plan.items:" + plan_key];
+    uint64_t& smax = w->epochs["fd.plan.smax:" + plan_key];
+    if (!n) {
+      plan = fd_plan(G, len, unsigned(w->sm_count));
+      n = plan.items.size();
+      smax = uint64_t(plan.S_max);
+    }
+    plan_items = size_t(n);
+    plan.S_max = int(smax);
+  }
   const int S = stream ? plan.S_max : choose_splits(sh, len, w->sm_count);
   const size_t split_len = (len + S - 1) / S;
   const int S_eff = stream ? plan.S_max : int((len + split_len - 1) / split_len);
@@ -2141,12 +2158,12 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
   // any launch uses it) and the per-(rank, group) fold claims.
   size_t items_off = 0, fstate_off = 0;
   if (stream) {
-    const std::string key = std::to_string(G) + "x" + std::to_string(len) + "@" + std::to_string(w->sm_count);
-    const size_t tbytes = plan.items.size() * sizeof(uint4) + size_t(G) * sizeof(int);
-    TFB_CHECK(heap_get(w, "fd.items[" + key + "]", tbytes, &items_off));
+    const size_t tbytes = plan_items * sizeof(uint4) + size_t(G) * sizeof(int);
+    TFB_CHECK(heap_get(w, "fd.items[" + plan_key + "]", tbytes, &items_off));
     TFB_CHECK(heap_get(w, "fd.fstate[" + std::to_string(G) + "]", sizeof(unsigned) * kMaxLocal * G, &fstate_off));
     uint64_t& up = w->epochs["fd.items.uploaded@" + std::to_string(items_off)];
     if (!up) {
+      if (plan.items.empty()) plan = fd_plan(G, len, unsigned(w->sm_count));  // heap was reset
       std::vector<uint8_t> host(tbytes);
       std::memcpy(host.data(), plan.items.data(), plan.items.size() * sizeof(uint4));
       std::memcpy(host.data() + plan.items.size() * sizeof(uint4), plan.gS.data(), size_t(G) * sizeof(int));
@@ -2270,8 +2287,8 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
         Q.owner = owner;
         if (stream) {
           Q.items = reinterpret_cast<const uint4*>(w->ptr(lead, items_off));
-          Q.gS = reinterpret_cast<const int*>(Q.items + plan.items.size());
-          Q.nitems = unsigned(plan.items.size()) * unsigned(Q.nlocal);
+          Q.gS = reinterpret_cast<const int*>(Q.items + plan_items);
+          Q.nitems = unsigned(plan_items) * unsigned(Q.nlocal);
         }
         cudaSetDevice(kv.first);
         // Every co-located rank's inputs may come from its own stream: the
