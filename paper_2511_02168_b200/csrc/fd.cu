@@ -2006,10 +2006,21 @@ static FdPlan fd_plan(int G, size_t len, unsigned grid) {
   return pl;
 }
 
+// Which tensor-core kernel runs a fast-path shape.  The TMA-fed stream
+// kernel balances the work dynamically and wins when there are many KV
+// streams (config 4: 256 groups, 630 vs 640 us); with few long streams
+// (config 3: 8 groups) the register-streaming kernel's static splits over
+// two CTAs per SM stream faster (100 vs 110 us) -- both measured in one
+// process (tools/fd_ab.py).  Shape-only, so every schedule and rank of a
+// problem runs the same kernel (bitwise-equal partials).
+// TFB_FD_STREAM=1/0 forces it (TFB_FD_LEGACY=1 is the old spelling of 0).
 static bool fd_stream_ok(const tf_fd_shape& s, World* w, const void* const* q, const void* const* k,
                          const void* const* v) {
-  if (std::getenv("TFB_FD_LEGACY")) return false;  // A/B: the register-streaming kernel
+  if (std::getenv("TFB_FD_LEGACY")) return false;
   if (!fast_ok(s)) return false;
+  const char* force = std::getenv("TFB_FD_STREAM");
+  if (force && std::atoi(force) == 0) return false;
+  if (!force && long(s.batch) * s.kv_heads < 64) return false;
   const size_t len = s.kv_len / size_t(w->W);
   if (size_t(s.batch) * s.kv_heads * len >= (size_t(1) << 31)) return false;
   for (int r = 0; r < w->W; ++r)
@@ -2304,7 +2315,12 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
         }
         // Tensor-core split with bf16 P for bf16 output, hi/lo P when the
         // caller asked for fp32 output; the generic split otherwise.
-        const bool hilo = sh.out_dtype == TF_F32 || std::getenv("TFB_FD_HILO");
+        // P reaches the PV product as a bf16 hi + lo pair for every output
+        // dtype: attention accurate to ~1e-5 whatever the output, so a bf16
+        // output's only error is its own rounding (<= 2^-8 of the head's
+        // max).  Measured cost < 1 % (HBM-bound).  TFB_FD_HILO=0: one bf16 P.
+        const char* hl = std::getenv("TFB_FD_HILO");
+        const bool hilo = sh.out_dtype == TF_F32 || !hl || std::atoi(hl) != 0;
         if (stream) {
           FdMaps maps{};
           for (int i = 0; i < Q.nlocal; ++i) {

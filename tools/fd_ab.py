@@ -12,9 +12,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2511_02168_b200 as tf  # noqa: E402
 from paper_2511_02168_b200 import _abi  # noqa: E402
 
-CFGS = {"c3": (1, 131072), "c4": (32, 32768)}
+CFGS = {"c3": (1, 131072), "c4": (32, 32768), "c3w8": (1, 16384), "c4w8": (32, 4096)}
 which = sys.argv[1:] or ["c3", "c4"]
-variants = [v for v in os.environ.get("FDAB", "stream,legacy,stream_hilo").split(",")]
+variants = [v for v in os.environ.get("FDAB", "stream,legacy").split(",")]
 
 
 def ref_attn(q, k, v, scale):
@@ -39,12 +39,8 @@ for name in which:
     ref = ref_attn(q[bs], k[bs], v[bs], d ** -0.5)
     with tf.World(1, [0], 256 << 20) as w:
         for var in variants:
-            os.environ.pop("TFB_FD_LEGACY", None)
-            os.environ.pop("TFB_FD_HILO", None)
-            if var.startswith("legacy"):
-                os.environ["TFB_FD_LEGACY"] = "1"
-            if var.endswith("hilo"):
-                os.environ["TFB_FD_HILO"] = "1"
+            os.environ["TFB_FD_STREAM"] = "0" if var.startswith("legacy") else "1"
+            os.environ["TFB_FD_HILO"] = "0" if var.endswith("bf16p") else "1"
             for odt in (_abi.TF_BF16, _abi.TF_F32):
                 out = torch.empty(Bt, Hq, d, device="cuda", dtype=torch.bfloat16 if odt == _abi.TF_BF16 else torch.float32)
                 shape = _abi.FdShape(Bt, Hq, Hkv, d, L, d ** -0.5, _abi.TF_BF16, odt)
@@ -55,7 +51,7 @@ for name in which:
                 for _ in range(5):
                     _abi.check(w.lib.tf_flash_decode_async(*args))
                 _abi.check(w.lib.tf_world_sync(w.handle))
-                n = 40 if name == "c3" else 10
+                n = 10 if name == "c4" else 40
                 evs = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
                 evs[0].record(st)
                 for i in range(n):
