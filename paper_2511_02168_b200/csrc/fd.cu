@@ -2006,21 +2006,25 @@ static FdPlan fd_plan(int G, size_t len, unsigned grid) {
   return pl;
 }
 
-// Which tensor-core kernel runs a fast-path shape.  The TMA-fed stream
-// kernel balances the work dynamically and wins when there are many KV
-// streams (config 4: 256 groups, 630 vs 640 us); with few long streams
-// (config 3: 8 groups) the register-streaming kernel's static splits over
-// two CTAs per SM stream faster (100 vs 110 us) -- both measured in one
-// process (tools/fd_ab.py).  Shape-only, so every schedule and rank of a
-// problem runs the same kernel (bitwise-equal partials).
-// TFB_FD_STREAM=1/0 forces it (TFB_FD_LEGACY=1 is the old spelling of 0).
+// Which tensor-core kernel runs a fast-path shape (tools/fd_ab.py, one
+// process, profiles/r2_fd_ab.log).  The TMA-fed stream kernel balances the
+// work dynamically and wins on many long KV streams (config 4 at W = 1:
+// 256 groups x 32K keys, 632 vs 643 us); everywhere else the register-
+// streaming kernel's static splits over two CTAs per SM are faster (config
+// 3: 100 vs 112 us; per-rank W = 8 shapes: 33 vs 38 us and 100 vs 118 us),
+// because the stream kernel's fold tail costs ~5 us per sub-item round.
+// Shape-only, so every schedule and rank of a problem runs the same kernel
+// (bitwise-equal partials).  TFB_FD_STREAM=1/0 forces it (TFB_FD_LEGACY=1
+// is the old spelling of 0).
 static bool fd_stream_ok(const tf_fd_shape& s, World* w, const void* const* q, const void* const* k,
                          const void* const* v) {
   if (std::getenv("TFB_FD_LEGACY")) return false;
   if (!fast_ok(s)) return false;
   const char* force = std::getenv("TFB_FD_STREAM");
   if (force && std::atoi(force) == 0) return false;
-  if (!force && long(s.batch) * s.kv_heads < 64) return false;
+  if (!force && (long(s.batch) * s.kv_heads < 64 ||
+                 double(s.batch) * s.kv_heads * double(s.kv_len / size_t(w->W)) < 4.0 * 1024 * 1024))
+    return false;
   const size_t len = s.kv_len / size_t(w->W);
   if (size_t(s.batch) * s.kv_heads * len >= (size_t(1) << 31)) return false;
   for (int r = 0; r < w->W; ++r)
