@@ -269,6 +269,27 @@ tf_status tf_flash_decode_async(tf_world* w, tf_fd_variant variant,
                                 const void* const* k_shard,
                                 const void* const* v_shard, void* const* out,
                                 void* const* inbox_opt, void* const* streams);
+/* The BSP schedule's two compute stages, for callers that bring their own
+ * collective (e.g. NCCL all_gather_into_tensor of the rows in between, the
+ * north_star's BSP baseline):
+ *   tf_fd_partial_async  attention_partial + serialize_partial for every
+ *                        (batch, q-head) of each local rank's shard
+ *                        (tilemath.hpp:145-181, 244-258;
+ *                        flash_decode.hpp:162-167): rows[r] receives the
+ *                        rank's wire rows [B][Hq][d+2] fp32 -- bitwise the
+ *                        rows every other schedule exchanges.
+ *   tf_fd_combine_async  fold_rows + finalize (flash_decode.hpp:171-180,
+ *                        tilemath.hpp:186-239): rows[r] holds W sources'
+ *                        rows [W][B][Hq][d+2]; folded in ascending source
+ *                        order into out[r] (out_dtype) -- bitwise every
+ *                        schedule's output.  TF_ERR_EMPTY_ATTENTION on an
+ *                        empty normalizer.
+ * Both only enqueue (streams as for tf_flash_decode). */
+tf_status tf_fd_partial_async(tf_world* w, const tf_fd_shape* shape, const void* const* q,
+                              const void* const* k_shard, const void* const* v_shard,
+                              void* const* rows, void* const* streams);
+tf_status tf_fd_combine_async(tf_world* w, const tf_fd_shape* shape, const void* const* rows,
+                              void* const* out, void* const* streams);
 /* fd flag row after the last push-style run (flash_decode.hpp:198-206):
  * per source, normalised so one completed run reads 1. */
 tf_status tf_fd_flag_counts(tf_world* w, int rank, uint64_t* out, size_t cap,

@@ -120,6 +120,8 @@ SIGNATURES = {
     "tf_flash_decode": (C.c_int, [_P, C.c_int, C.POINTER(FdShape), _PP, _PP, _PP, _PP, _PP, _PP]),
     "tf_flash_decode_async": (C.c_int, [_P, C.c_int, C.POINTER(FdShape), _PP, _PP, _PP, _PP,
                                         _PP, _PP]),
+    "tf_fd_partial_async": (C.c_int, [_P, C.POINTER(FdShape), _PP, _PP, _PP, _PP, _PP]),
+    "tf_fd_combine_async": (C.c_int, [_P, C.POINTER(FdShape), _PP, _PP, _PP]),
     "tf_fd_flag_counts": (C.c_int, [_P, C.c_int, C.POINTER(C.c_uint64), C.c_size_t,
                                     C.POINTER(C.c_size_t)]),
     "tf_memcpy": (C.c_int, [_P, _P, _P, C.c_size_t]),

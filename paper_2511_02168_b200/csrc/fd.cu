@@ -2070,14 +2070,15 @@ void fd_preload() {  // see ag_exact_preload
 
 using namespace tfb;
 
-extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
-                                           const tf_fd_shape* shape, const void* const* q,
-                                           const void* const* k_shard,
-                                           const void* const* v_shard, void* const* out,
-                                           void* const* inbox_opt, void* const* streams) {
+// Every Flash Decode entry point.  rows_out != NULL: the attention stage
+// only (the BSP schedule's first kernel), each local rank's partial wire
+// rows [B][Hq][d+2] landing in rows_out[r] instead of the heap.
+static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape* shape, const void* const* q,
+                          const void* const* k_shard, const void* const* v_shard, void* const* out,
+                          void* const* inbox_opt, void* const* streams, void* const* rows_out) {
   if (!tw) return set_error(TF_ERR_CONFIG, "tf_flash_decode: NULL world");
   World* w = &tw->impl;
-  TFB_CHECK(fd_validate(w, shape, q, k_shard, v_shard, out));
+  TFB_CHECK(fd_validate(w, shape, q, k_shard, v_shard, rows_out ? rows_out : out));
   if (variant < TF_FD_BSP || variant > TF_FD_FUSED_OWNER)
     return set_error(TF_ERR_CONFIG, "run_fd: unknown variant");
   const tf_fd_shape& sh = *shape;
@@ -2275,7 +2276,8 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
         for (int i = 0; i < Q.nlocal; ++i) {
           const int r = rs[c0 + i];
           Q.r[i] = FdRank{q[r], k_shard[r], v_shard[r], out[r],
-                          reinterpret_cast<float*>(w->ptr(r, pub_off)), inbox_of(r),
+                          rows_out ? static_cast<float*>(rows_out[r]) : reinterpret_cast<float*>(w->ptr(r, pub_off)),
+                          inbox_of(r),
                           reinterpret_cast<uint64_t*>(w->ptr(r, fb.offset)), r, w->skew_of(r)};
         }
         Q.err = w->err_of(lead);
@@ -2386,6 +2388,7 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
     return TF_OK;
   };
 
+  if (rows_out) return launch_attention(0, 0);  // attention stage only: rows to the caller
   // Every schedule lands W wire rows per rank in an inbox / stage
   // (flash_decode_test.cpp:167-196: W*W*wire*4 bytes world-wide).
   for (int r = 0; r < W; ++r)
@@ -2453,6 +2456,63 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
     fd_fold_kernel<<<sh.batch * sh.q_heads, 32, 0, st[r]>>>(
         inbox_of(r), out[r], with_err(r), r, reinterpret_cast<uint64_t*>(w->ptr(r, fb.offset)),
         wait_all ? 0 : 1);
+    TFB_CUDA(cudaGetLastError());
+    ++w->launches;
+  }
+  return TF_OK;
+}
+
+extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
+                                           const tf_fd_shape* shape, const void* const* q,
+                                           const void* const* k_shard,
+                                           const void* const* v_shard, void* const* out,
+                                           void* const* inbox_opt, void* const* streams) {
+  return fd_async(tw, variant, shape, q, k_shard, v_shard, out, inbox_opt, streams, nullptr);
+}
+
+// attention_partial + serialize_partial of every (b, q-head) for each local
+// rank (tilemath.hpp:145-181, 244-258; flash_decode.hpp:162-167): the
+// rank's wire rows [B][Hq][d+2] fp32 into rows[r] -- the BSP schedule's
+// attention kernel alone, so callers can exchange the rows with their own
+// collective (NCCL all-gather) and fold them with tf_fd_combine_async.
+extern "C" tf_status tf_fd_partial_async(tf_world* tw, const tf_fd_shape* shape, const void* const* q,
+                                         const void* const* k_shard, const void* const* v_shard,
+                                         void* const* rows, void* const* streams) {
+  if (!rows) return set_error(TF_ERR_CONFIG, "tf_fd_partial: NULL rows");
+  return fd_async(tw, TF_FD_BSP, shape, q, k_shard, v_shard, nullptr, nullptr, streams, rows);
+}
+
+// fold_rows + finalize (flash_decode.hpp:171-180, tilemath.hpp:186-239):
+// rows[r] holds W sources' wire rows [W][B][Hq][d+2] (an all-gather of
+// every rank's tf_fd_partial_async rows), folded in ascending source order
+// into out[r] -- the BSP schedule's fold kernel, bitwise every schedule's
+// output.
+extern "C" tf_status tf_fd_combine_async(tf_world* tw, const tf_fd_shape* shape, const void* const* rows,
+                                         void* const* out, void* const* streams) {
+  if (!tw || !shape || !rows || !out) return set_error(TF_ERR_CONFIG, "tf_fd_combine: NULL argument");
+  World* w = &tw->impl;
+  const tf_fd_shape& sh = *shape;
+  if (sh.head_dim < 1 || sh.head_dim > 256 || sh.batch < 1 || sh.q_heads < 1)
+    return set_error(TF_ERR_CONFIG, "fd_combine: bad shape");
+  auto st = resolve_streams(w, streams);
+  TFB_CHECK(refuse_multi_rank_capture(w, st, "tf_fd_combine"));
+  TFB_CHECK(order_after_legacy(w, streams));
+  FdParams P{};
+  P.W = w->W;
+  P.B = sh.batch;
+  P.Hq = sh.q_heads;
+  P.Hkv = sh.kv_heads;
+  P.gs = sh.kv_heads > 0 ? sh.q_heads / sh.kv_heads : 1;
+  P.d = sh.head_dim;
+  P.out_bf16 = sh.out_dtype == TF_BF16;
+  P.watchdog_ns = w->watchdog_ns;
+  for (int r = 0; r < w->W; ++r) {
+    if (!w->ranks[r].local) continue;
+    if (!rows[r] || !out[r]) return set_error(TF_ERR_CONFIG, "fd_combine: NULL buffer for rank " + std::to_string(r));
+    cudaSetDevice(w->ranks[r].device);
+    P.err = w->err_of(r);
+    fd_fold_kernel<<<sh.batch * sh.q_heads, 32, 0, st[r]>>>(static_cast<const float*>(rows[r]), out[r], P, r,
+                                                              nullptr, 0);
     TFB_CUDA(cudaGetLastError());
     ++w->launches;
   }
