@@ -2275,7 +2275,7 @@ static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape
         const int lead = rs[c0];
         for (int i = 0; i < Q.nlocal; ++i) {
           const int r = rs[c0 + i];
-          Q.r[i] = FdRank{q[r], k_shard[r], v_shard[r], out[r],
+          Q.r[i] = FdRank{q[r], k_shard[r], v_shard[r], out ? out[r] : nullptr,
                           rows_out ? static_cast<float*>(rows_out[r]) : reinterpret_cast<float*>(w->ptr(r, pub_off)),
                           inbox_of(r),
                           reinterpret_cast<uint64_t*>(w->ptr(r, fb.offset)), r, w->skew_of(r)};
