@@ -29,6 +29,12 @@ def test_bench_two_processes_shared_gpu():
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["config"]["world_size"] == 2
     assert line["e2e"]["matches_device_run"] is True
-    assert line["numerics"]["ag_sampled_rows_norm_err"] is None  # W > 1: no single-rank full operand
+    # W > 1: sampled rows of C against an fp32 product of the NCCL(gloo)-gathered operand
+    assert line["numerics"]["ag_sampled_rows_norm_err"] <= 4e-3
+    assert line["nvlink"]["bytes_per_rank"] > 0
     for k in ("fd_config3_b1_L128k", "fd_config4_b32_L32k"):
-        assert line["secondary"][k]["fused_us"] > 0
+        sec = line["secondary"][k]
+        assert sec["fused_us"] > 0 and sec["nccl_bsp_us"] > 0
+        assert sec["numerics"]["fused_equals_nccl_bsp_bitwise"] is True
+        assert sec["numerics"]["bf16"]["head_rel_err"] <= sec["numerics"]["bf16"]["tol"]
+        assert sec["numerics"]["f32"]["head_rel_err"] <= sec["numerics"]["f32"]["tol"]
