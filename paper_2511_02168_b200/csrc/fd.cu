@@ -112,6 +112,14 @@ struct FdParams {
   // table entry i / nlocal of local rank i % nlocal); per group split count;
   // per (lr, g) fold claim state (0 free, 1 folded inline by the last
   // split's CTA, 2 taken by the fold phase; reset by the last CTA).
+  // Device-resident epochs (fused schedules): when set, a launch reads its
+  // flag / claim epochs from these cells (+1) and its last CTA stores them
+  // back, so the launch is self-contained and a captured CUDA graph replays
+  // with fresh epochs.  [0] fused flag board, [1] owner flag board, [2]
+  // owner final-row flags, [3] fold claims.  inbox_all / outbox_all are then
+  // the parity-0 halves; the launch adds epoch parity x *_pstride.
+  uint64_t* depoch;
+  size_t inbox_pstride, outbox_pstride;
   const uint4* items;
   unsigned nitems;
   const int* gS;
@@ -122,6 +130,39 @@ struct FdParams {
 __device__ __forceinline__ int split_count(const FdParams& P, int lr, int g) {
   (void)lr;  // every rank cuts the same splits
   return P.gS ? P.gS[g] : P.S;
+}
+
+// This launch's epochs (fd_epochs_begin): the device cells' values + 1, or
+// the host's when the schedule is host-driven (P.depoch == nullptr).
+__shared__ uint64_t s_fe, s_oe, s_ce;
+
+__device__ __forceinline__ uint64_t fe(const FdParams& P) { return P.depoch ? s_fe : P.flag_epoch; }
+__device__ __forceinline__ uint64_t oe(const FdParams& P) { return P.depoch ? s_oe : P.oflag_epoch; }
+__device__ __forceinline__ uint64_t ce(const FdParams& P) { return P.depoch ? s_ce : P.epoch; }
+// Inboxes / outboxes of this epoch's parity (peers are at most one run ahead).
+__device__ __forceinline__ float* inbox_at(const FdParams& P, int dst) {
+  return P.inbox_all[dst] + (P.depoch ? size_t(s_fe & 1) * P.inbox_pstride : 0);
+}
+__device__ __forceinline__ const float* rank_inbox(const FdParams& P, int lr) {
+  return P.r[lr].inbox + (P.depoch ? size_t(s_fe & 1) * P.inbox_pstride : 0);
+}
+__device__ __forceinline__ float* outbox_at(const FdParams& P, int dst) {
+  return P.outbox_all[dst] + (P.depoch ? size_t(s_oe & 1) * P.outbox_pstride : 0);
+}
+// Thread 0 at launch start (a __syncthreads follows in every kernel).
+__device__ __forceinline__ void fd_epochs_begin(const FdParams& P) {
+  if (!P.depoch) return;
+  const volatile uint64_t* c = P.depoch;
+  s_fe = c[P.owner ? 1 : 0] + 1;
+  s_oe = c[2] + 1;
+  s_ce = c[3] + 1;
+}
+// The launch's last CTA, after every CTA has passed its start.
+__device__ __forceinline__ void fd_epochs_end(const FdParams& P) {
+  if (!P.depoch) return;
+  P.depoch[P.owner ? 1 : 0] = s_fe;
+  if (P.owner) P.depoch[2] = s_oe;
+  P.depoch[3] = s_ce;
 }
 
 __device__ __forceinline__ void consumer_bar() {  // the 8 consumer warps of fd_stream_kernel
@@ -575,7 +616,7 @@ __device__ __noinline__ bool fold_group_batched(const FdParams& P, int lr, int g
     if (threadIdx.x == 0) {
       int ok = 1;
       for (int i = 0; i < P.W && ok; ++i) {
-        ok = wait_geq(R.flags + size_t(i) * G + g, P.flag_epoch, P.watchdog_ns, P.err, kWaitSignal, R.rank,
+        ok = wait_geq(R.flags + size_t(i) * G + g, fe(P), P.watchdog_ns, P.err, kWaitSignal, R.rank,
                       P.board, i, g, 0);
         if (ok && P.events_all[R.rank])  // first (only) read of source i's rows of g
           P.events_all[R.rank][(size_t(i) * G + g) * 2 + 1] = globaltimer_ns();
@@ -589,7 +630,7 @@ __device__ __noinline__ bool fold_group_batched(const FdParams& P, int lr, int g
     const size_t src_stride = size_t(P.B) * P.Hq * row_len;
     for (int h = warp; h < P.gs; h += nw) {
       const int hq = kvh * P.gs + h;
-      const float* row0 = R.inbox + (size_t(b) * P.Hq + hq) * row_len;
+      const float* row0 = rank_inbox(P, lr) + (size_t(b) * P.Hq + hq) * row_len;
       float bm[8], bl[8], bo[8][EL];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -629,7 +670,7 @@ __device__ __noinline__ bool fold_group_batched(const FdParams& P, int lr, int g
           store_out(R.out, ooff + e, y, P.out_bf16);
           if (P.owner)
             for (int dst = 0; dst < P.W; ++dst)
-              if (dst != R.rank) P.outbox_all[dst][ooff + e] = y;
+              if (dst != R.rank) outbox_at(P, dst)[ooff + e] = y;
         }
       }
     }
@@ -675,7 +716,7 @@ __device__ __forceinline__ void emit_wire_row4(const FdParams& P, int lr, int g,
   if (P.push) {
     for (int dst = 0; dst < W; ++dst) {
       if (P.owner && dst != g % W) continue;  // owner-combine: the group's owner only
-      put(P.inbox_all[dst] + base_src + off);
+      put(inbox_at(P, dst) + base_src + off);
     }
   } else {
     put(P.r[lr].pub + off);
@@ -827,21 +868,21 @@ __device__ __noinline__ bool fold_group(const FdParams& P, int lr, int g, int& s
     if (threadIdx.x == 0) {
       int src = -1;
       if (!P.by_arrival) {
-        if (wait_geq(R.flags + size_t(i) * G + g, P.flag_epoch, P.watchdog_ns, P.err, kWaitSignal,
+        if (wait_geq(R.flags + size_t(i) * G + g, fe(P), P.watchdog_ns, P.err, kWaitSignal,
                      R.rank, P.board, i, g, 0))
           src = i;
       } else {
         const uint64_t t0 = globaltimer_ns();
         for (unsigned polls = 0; src < 0; ++polls) {
           for (int s = 0; s < P.W; ++s)
-            if (!((folded >> s) & 1ull) && ld_acquire_sys(R.flags + size_t(s) * G + g) >= P.flag_epoch) {
+            if (!((folded >> s) & 1ull) && ld_acquire_sys(R.flags + size_t(s) * G + g) >= fe(P)) {
               src = s;
               break;
             }
           if (src < 0 && (polls & 63u) == 63u) {
             if (err_raised(P.err)) break;
             if (globaltimer_ns() - t0 > P.watchdog_ns) {
-              raise_err(P.err, TF_ERR_DEADLOCK, kWaitSignal, R.rank, P.board, -1, g, P.flag_epoch, 0, 0);
+              raise_err(P.err, TF_ERR_DEADLOCK, kWaitSignal, R.rank, P.board, -1, g, fe(P), 0, 0);
               break;
             }
           }
@@ -855,7 +896,7 @@ __device__ __noinline__ bool fold_group(const FdParams& P, int lr, int g, int& s
     __syncthreads();
     if (src < 0) return false;
     folded |= 1ull << src;
-    const float* base = R.inbox + size_t(src) * P.B * P.Hq * row_len;
+    const float* base = rank_inbox(P, lr) + size_t(src) * P.B * P.Hq * row_len;
 #pragma unroll
     for (int j = 0; j < MAXH; ++j) {
       const int h = warp + j * nw;
@@ -881,7 +922,7 @@ __device__ __noinline__ bool fold_group(const FdParams& P, int lr, int g, int& s
         store_out(R.out, ooff + e, y, P.out_bf16);
         if (P.owner)  // owner-combine: the finalized row to every other rank
           for (int dst = 0; dst < P.W; ++dst)
-            if (dst != R.rank) P.outbox_all[dst][ooff + e] = y;
+            if (dst != R.rank) outbox_at(P, dst)[ooff + e] = y;
       }
     }
   }
@@ -908,14 +949,14 @@ __device__ __noinline__ bool take_group(const FdParams& P, int lr, int g) {
   const int b = g / P.Hkv, kvh = g % P.Hkv, d = P.d, owner = g % P.W;
   __shared__ int s_ok;
   if (threadIdx.x == 0)
-    s_ok = wait_geq(P.oflags_all[R.rank] + g, P.oflag_epoch, P.watchdog_ns, P.err, kWaitSignal, R.rank,
+    s_ok = wait_geq(P.oflags_all[R.rank] + g, oe(P), P.watchdog_ns, P.err, kWaitSignal, R.rank,
                     P.board, owner, g, 0);
   __syncthreads();
   const int ok = s_ok;
   __syncthreads();
   if (!ok) return false;
   const size_t base = (size_t(b) * P.Hq + kvh * P.gs) * d;
-  const float* src = P.outbox_all[R.rank] + base;
+  const float* src = outbox_at(P, R.rank) + base;
   for (int e = threadIdx.x; e < P.gs * d; e += blockDim.x) store_out(R.out, base + e, __ldcg(src + e), P.out_bf16);
   return true;
 }
@@ -953,7 +994,7 @@ __device__ __forceinline__ void emit_wire_row(const FdParams& P, int lr, int g, 
   if (P.push) {
     for (int dst = 0; dst < W; ++dst) {
       if (P.owner && dst != g % W) continue;  // owner-combine: the group's owner only
-      float* r = P.inbox_all[dst] + base_src + off;
+      float* r = inbox_at(P, dst) + base_src + off;
       if (lane == 0) {
         r[0] = M;
         r[1] = L;
@@ -1268,8 +1309,8 @@ __device__ __noinline__ void fd_post_phases(const FdParams& P, unsigned ranks_ma
         if (threadIdx.x == 0) s_src = 0;
         if (threadIdx.x == 0 && (!P.owner || g % P.W == R.rank)) {
           bool all = true;
-          for (int i = 0; i < P.W && all; ++i) all = ld_acquire_sys(R.flags + size_t(i) * G + g) >= P.flag_epoch;
-          s_src = all && atomicMax(&P.claim[size_t(lr) * G + g], (unsigned long long)P.epoch) < P.epoch;
+          for (int i = 0; i < P.W && all; ++i) all = ld_acquire_sys(R.flags + size_t(i) * G + g) >= fe(P);
+          s_src = all && atomicMax(&P.claim[size_t(lr) * G + g], (unsigned long long)ce(P)) < ce(P);
         }
         __syncthreads();
         const int mine = s_src;
@@ -1287,7 +1328,7 @@ __device__ __noinline__ void fd_post_phases(const FdParams& P, unsigned ranks_ma
       __syncthreads();
       if (threadIdx.x == 0) {
         s_item = atomicAdd(&P.ctr[1], 1u);
-        s_src = s_item < nfold && atomicMax(&P.claim[s_item], (unsigned long long)P.epoch) < P.epoch;
+        s_src = s_item < nfold && atomicMax(&P.claim[s_item], (unsigned long long)ce(P)) < ce(P);
       }
       __syncthreads();
       const unsigned item = s_item;
@@ -1341,6 +1382,7 @@ __device__ __noinline__ void fd_post_phases(const FdParams& P, unsigned ranks_ma
       P.ctr[2] = 0;
       P.ctr[3] = 0;
       for (int i = 0; i < P.nlocal; ++i) P.sfc[i] = 0;
+      fd_epochs_end(P);
     }
     __threadfence();
   }
@@ -1364,7 +1406,10 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
   stamp(0);
   unsigned ranks_mask = 0;  // local ranks this CTA computed for
   __shared__ unsigned long long s_t0;  // CTA entry time (straggler model)
-  if (threadIdx.x == 0) s_t0 = globaltimer_ns();
+  if (threadIdx.x == 0) {
+    s_t0 = globaltimer_ns();
+    fd_epochs_begin(P);
+  }
   if (tr && threadIdx.x == 0)
     for (int i = 1; i < kTraceSlots; ++i)
       if (i != 12 && i != 13) tr[i] = 0;
@@ -1809,6 +1854,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     sm.bad = 0;
     sm.ranks_mask = 0;
     sm.npub = 0;
+    fd_epochs_begin(P);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (threadIdx.x == 32 * kProducerWarp) {
@@ -2083,7 +2129,12 @@ static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape
     return set_error(TF_ERR_CONFIG, "run_fd: unknown variant");
   const tf_fd_shape& sh = *shape;
   auto st = resolve_streams(w, streams);
-  TFB_CHECK(refuse_multi_rank_capture(w, st, "tf_flash_decode"));
+  const bool fused_v = variant == TF_FD_FUSED || variant == TF_FD_FUSED_BY_ARRIVAL || variant == TF_FD_FUSED_OWNER;
+  // The fused schedules keep their epochs on the device (FdParams::depoch):
+  // one self-contained launch per device, capturable into a CUDA graph in
+  // any world.  The multi-kernel schedules' epochs are host state.
+  const bool dev_epochs = fused_v && !rows_out && !w->events;
+  if (!dev_epochs) TFB_CHECK(refuse_multi_rank_capture(w, st, "tf_flash_decode"));
   TFB_CHECK(order_after_legacy(w, streams));
   const int W = w->W, d = sh.head_dim, G = sh.batch * sh.kv_heads, gs = sh.q_heads / sh.kv_heads;
   const size_t len = sh.kv_len / W;
@@ -2157,8 +2208,19 @@ static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape
   // in the buffer a slow rank is still folding.
   size_t inbox_off = 0, pub_off = 0, ws_off = 0, tick_off = 0, ctr_off = 0;
   const std::string geo = "[" + std::to_string(row_floats) + "]";
-  TFB_CHECK(heap_get(w, (owner ? "fd.inbox.owner" : "fd.inbox") + geo, sizeof(float) * W * row_floats * 2,
-                     &inbox_off));
+  // The fused schedules own their inboxes (device-epoch parity); the others
+  // share one (host-counted parity).
+  TFB_CHECK(heap_get(w, (owner ? "fd.inbox.owner" : fused ? "fd.inbox.fused" : "fd.inbox") + geo,
+                     sizeof(float) * W * row_floats * 2, &inbox_off));
+  size_t depoch_off = 0;
+  if (dev_epochs) {
+    TFB_CHECK(heap_get(w, "fd.depoch", sizeof(uint64_t) * 4, &depoch_off));
+    if (!owner) {
+      w->fd_flags.dev = true;
+      w->fd_flags.dev_off = depoch_off;
+      w->fd_flags.dev_idx = 0;
+    }
+  }
   TFB_CHECK(heap_get(w, "fd.partials" + geo, sizeof(float) * row_floats, &pub_off));
   const int nlocal_max = std::min(w->n_local, kMaxLocal);
   const size_t ws_floats = size_t(nlocal_max) * G * S_eff * gs * ws_row(d);
@@ -2200,13 +2262,16 @@ static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape
   // call sequence, so every rank agrees on it; consecutive pushing runs
   // alternate buffers, and a peer is at most one run ahead.
   int parity = 0;
-  if (variant != TF_FD_BSP)
+  if (variant != TF_FD_BSP && !dev_epochs)
     parity = int(++w->epochs[std::string(owner ? "fd.inbox.owner" : "fd.inbox") + "@" + std::to_string(inbox_off)] & 1);
 
   auto inbox_of = [&](int r) -> float* {
     if (inbox_opt && inbox_opt[r]) return static_cast<float*>(inbox_opt[r]);
     return reinterpret_cast<float*>(w->ptr(r, inbox_off)) + size_t(parity) * W * row_floats;
   };
+  // Device-epoch launches add the parity themselves (a caller's inbox is a
+  // single buffer: no parity).
+  const bool caller_inbox = inbox_opt != nullptr;
 
   FdParams P{};
   P.W = W;
@@ -2255,7 +2320,7 @@ static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape
   if (owner) {
     P.oflag_epoch = ob.epoch;
     for (int r = 0; r < W; ++r) {
-      P.outbox_all[r] = reinterpret_cast<float*>(w->ptr(r, outbox_off)) + size_t(ob.epoch & 1) * out_floats;
+      P.outbox_all[r] = reinterpret_cast<float*>(w->ptr(r, outbox_off)) + (dev_epochs ? 0 : size_t(ob.epoch & 1) * out_floats);
       P.oflags_all[r] = reinterpret_cast<uint64_t*>(w->ptr(r, ob.offset));
     }
   }
@@ -2282,6 +2347,11 @@ static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape
         }
         Q.err = w->err_of(lead);
         Q.ws = reinterpret_cast<float*>(w->ptr(lead, ws_off));
+        if (dev_epochs && fold_inline) {
+          Q.depoch = reinterpret_cast<uint64_t*>(w->ptr(lead, depoch_off));
+          Q.inbox_pstride = caller_inbox ? 0 : size_t(W) * row_floats;
+          Q.outbox_pstride = out_floats;
+        }
         if (std::getenv("TFB_TRACE")) {
           size_t toff;
           TFB_CHECK(heap_get(w, "fd.trace", sizeof(unsigned long long) * kTraceSlots * 4096, &toff));
@@ -2541,11 +2611,23 @@ extern "C" tf_status tf_fd_flag_counts(tf_world* tw, int rank, uint64_t* out, si
   std::vector<uint64_t> v(f.cells);
   TFB_CUDA(cudaMemcpy(v.data(), w->ptr(rank, it->second.offset), sizeof(uint64_t) * f.cells,
                       cudaMemcpyDefault));
+  uint64_t epoch = f.epoch;
+  if (f.dev && w->ranks[rank].local) {
+    // The epoch the rank's launch left in its device's lead cell.
+    int lead = rank;
+    for (int r = 0; r < w->W; ++r)
+      if (w->ranks[r].local && w->ranks[r].device == w->ranks[rank].device) {
+        lead = r;
+        break;
+      }
+    TFB_CUDA(cudaMemcpy(&epoch, reinterpret_cast<uint64_t*>(w->ptr(lead, f.dev_off)) + f.dev_idx, sizeof(uint64_t),
+                        cudaMemcpyDefault));
+  }
   const size_t per = f.cells / size_t(w->W);
   for (int s = 0; s < w->W && size_t(s) < cap; ++s) {
     uint64_t mn = UINT64_MAX;
     for (size_t g = 0; g < per; ++g) mn = std::min(mn, v[size_t(s) * per + g]);
-    out[s] = mn - (f.epoch - 1);
+    out[s] = mn - (epoch - 1);
   }
   return TF_OK;
 }

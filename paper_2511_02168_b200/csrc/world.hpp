@@ -51,6 +51,12 @@ struct FlagSnapshot {
   std::string board;
   size_t cells = 0;     // per rank
   uint64_t epoch = 0;   // value a completed run leaves in every cell
+  // Device-epoch schedules: the epoch is read from the launch's cell
+  // (heap offset dev_off, index dev_idx of the rank's device lead) -- it
+  // advances in graph replays the host never sees.
+  bool dev = false;
+  size_t dev_off = 0;
+  int dev_idx = 0;
 };
 
 struct World {

@@ -1,9 +1,11 @@
-"""CUDA-graph capture of the single-rank fused paths: tf_flash_decode_async
-(fused) and tf_ag_gemm_async (pull, whole-K and split-K) captured once on a
-user stream and replayed give the eager call's bits -- every per-launch
-counter is reset by the launch's own last CTA, so a replay needs no host
-state.  Multi-rank schedules bake the host's flag epoch into the launch, so
-capturing one must fail loudly (TF_ERR_CONFIG), never replay stale waits."""
+"""CUDA-graph capture of the fused paths: tf_flash_decode_async (fused, every
+world size: its flag/claim epochs live on the device, read at launch start
+and written back by the launch's last CTA) and tf_ag_gemm_async (pull,
+single rank) captured once on a user stream and replayed give the eager
+call's bits -- every per-launch counter is reset by the launch's own last
+CTA, so a replay needs no host state.  Multi-rank schedules whose epochs
+are host state (AG, the multi-kernel FD schedules) must refuse capture
+loudly (TF_ERR_CONFIG), never replay stale waits."""
 import ctypes as C
 
 import pytest
@@ -101,3 +103,70 @@ def test_multi_rank_capture_is_refused():
         except RuntimeError:
             pass  # an empty capture may be rejected by torch itself; the status is what matters
         assert rc == [_abi.TF_ERR_CONFIG]
+
+
+@pytest.mark.parametrize("w,variant", [(2, _abi.TF_FD_FUSED), (4, _abi.TF_FD_FUSED),
+                                       (4, _abi.TF_FD_FUSED_OWNER)])
+def test_fd_fused_multi_rank_graph_replay(w, variant):
+    # A loopback world's fused decode (the push + flag-gated fold across W
+    # ranks in one launch) captured once and replayed with new inputs in
+    # the same buffers: every replay equals an eager call on those inputs
+    # bit for bit, and eager calls interleave with replays (the device
+    # epochs stay in step), every flag reading 1 after each.
+    import torch
+    B, Hq, Hkv, d, L = 1, 64, 8, 128, 4096 * w
+    gen = torch.Generator(device="cuda").manual_seed(w)
+    ln = L // w
+    q = torch.empty(B, Hq, d, device="cuda", dtype=torch.bfloat16)
+    ks = [torch.empty(B, Hkv, ln, d, device="cuda", dtype=torch.bfloat16) for _ in range(w)]
+    vs = [torch.empty_like(t) for t in ks]
+    outs = [torch.empty(B, Hq, d, device="cuda", dtype=torch.bfloat16) for _ in range(w)]
+
+    def fill(seed):
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        q.copy_((torch.rand(B, Hq, d, device="cuda", generator=g) * 2 - 1).bfloat16())
+        for t in ks + vs:
+            t.copy_((torch.rand(t.shape, device="cuda", generator=g) * 2 - 1).bfloat16())
+
+    with tf.World(w, [0] * w, 128 << 20) as wd:
+        cs = torch.cuda.Stream()
+        shape = _abi.FdShape(B, Hq, Hkv, d, L, d ** -0.5, _abi.TF_BF16, _abi.TF_BF16)
+        args = (wd.handle, variant, C.byref(shape), _abi.ptr_array([q.data_ptr()] * w),
+                _abi.ptr_array([t.data_ptr() for t in ks]), _abi.ptr_array([t.data_ptr() for t in vs]),
+                _abi.ptr_array([o.data_ptr() for o in outs]), None, _abi.ptr_array([cs.cuda_stream] * w))
+
+        def eager():
+            cs.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cs):
+                _abi.check(wd.lib.tf_flash_decode_async(*args))
+            cs.synchronize()
+            _abi.check(wd.lib.tf_world_sync(wd.handle))
+            return [o.clone() for o in outs]
+
+        def flags_all_one():
+            for r in range(w):
+                buf = (C.c_uint64 * w)()
+                cnt = C.c_size_t()
+                _abi.check(wd.lib.tf_fd_flag_counts(wd.handle, r, buf, w, C.byref(cnt)))
+                if variant == _abi.TF_FD_FUSED:
+                    assert list(buf[: cnt.value]) == [1] * w, list(buf[: cnt.value])
+
+        fill(100)
+        torch.cuda.synchronize()
+        first = eager()  # eager first: lazily allocated workspace exists before capture
+        for o in first[1:]:
+            assert torch.equal(o, first[0])
+        g = _capture(lambda: _abi.check(wd.lib.tf_flash_decode_async(*args)), cs)
+        for it in range(4):
+            fill(200 + it)
+            torch.cuda.synchronize()
+            for o in outs:
+                o.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            replayed = [o.clone() for o in outs]
+            flags_all_one()
+            want = eager()  # the same inputs through an eager call
+            flags_all_one()
+            for r in range(w):
+                assert torch.equal(replayed[r], want[r]), (it, r)
