@@ -1395,7 +1395,8 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
   __shared__ unsigned int s_item;
   __shared__ int s_last, s_src;
   __shared__ FastSmem fsm;
-  __shared__ float s_wm[8], s_fL[8], s_fO[8 * 256];
+  __shared__ float s_wm[8], s_fL[8];
+  __shared__ __align__(16) float s_fO[8 * 256];  // float4 rows (fold_heads128)
   const int G = P.B * P.Hkv;
   const unsigned total = unsigned(P.nlocal) * G * P.S;
   const int d = P.d, row_len = d + 2, wrl = ws_row(d);
@@ -1839,7 +1840,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   StreamSmem& sm = *reinterpret_cast<StreamSmem*>((reinterpret_cast<uintptr_t>(fd_smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ unsigned int s_item;
   __shared__ int s_last, s_src;
-  __shared__ float s_wm[8], s_fL[8], s_fO[8 * 256];
+  __shared__ float s_wm[8], s_fL[8];
+  __shared__ __align__(16) float s_fO[8 * 256];  // float4 rows (fold_heads128)
   unsigned long long* tr = P.trace ? P.trace + size_t(blockIdx.x) * kTraceSlots : nullptr;
   if (tr && threadIdx.x == 0) {
     tr[0] = globaltimer_ns();
