@@ -46,3 +46,53 @@ with tf.World(1, [0], M * K * 2 + (64 << 20)) as w:
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     print(f"AG M=128 host per call {(t1-t0)/200*1e6:.1f} us, wall per call incl. GPU {(t2-t0)/200*1e6:.1f} us")
+# The fused Flash Decode of a W=2 loopback world (push + flag-gated fold in
+# one launch) as an async C-ABI call vs replayed from a captured CUDA graph:
+# the device-resident epochs make the launch replayable, which removes the
+# per-call host cost (the paper's launch tax).
+W = 2
+with tf.World(W, [0] * W, 512 << 20) as w:
+    ln = L // W
+    q = (torch.rand(Bt, Hq, d, device="cuda") * 2 - 1).bfloat16()
+    ks = [(torch.rand(Bt, Hkv, ln, d, device="cuda") * 2 - 1).bfloat16() for _ in range(W)]
+    vs = [(torch.rand(Bt, Hkv, ln, d, device="cuda") * 2 - 1).bfloat16() for _ in range(W)]
+    outs = [torch.empty(Bt, Hq, d, device="cuda", dtype=torch.bfloat16) for _ in range(W)]
+    cs = torch.cuda.Stream()
+    shape = _abi.FdShape(Bt, Hq, Hkv, d, L, d ** -0.5, 1, 1)
+    args = (w.handle, 3, C.byref(shape), _abi.ptr_array([q.data_ptr()] * W), _abi.ptr_array([t.data_ptr() for t in ks]),
+            _abi.ptr_array([t.data_ptr() for t in vs]), _abi.ptr_array([o.data_ptr() for o in outs]), None,
+            _abi.ptr_array([cs.cuda_stream] * W))
+    with torch.cuda.stream(cs):
+        _abi.check(w.lib.tf_flash_decode_async(*args))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(200):
+        w.lib.tf_flash_decode_async(*args)
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    print(f"FD W=2 async call: host {(t1-t0)/200*1e6:.1f} us, wall per call incl. GPU {(t2-t0)/200*1e6:.1f} us")
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=cs):
+        _abi.check(w.lib.tf_flash_decode_async(*args))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(200):
+        g.replay()
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    print(f"FD W=2 graph replay: host {(t1-t0)/200*1e6:.1f} us, wall per call incl. GPU {(t2-t0)/200*1e6:.1f} us")
+    # 16 calls per graph: the host cost of one replay spread over 16 decodes.
+    g16 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g16, stream=cs):
+        for _ in range(16):
+            _abi.check(w.lib.tf_flash_decode_async(*args))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(20):
+        g16.replay()
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    print(f"FD W=2 graph of 16 calls: host {(t1-t0)/320*1e6:.2f} us per call, wall {(t2-t0)/320*1e6:.1f} us per call")
