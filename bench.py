@@ -498,6 +498,24 @@ def bench_fd(ctx, cfg, steps, warmup, pk, cooldown=lambda: None):
                 launches = (w.launches() - l0) // (steps + warmup) * steps
         _abi.check(w.lib.tf_world_sync(w.handle))
         torch.cuda.synchronize()
+        # End to end through the C ABI: the KV cache is resident in HBM (it
+        # is a cache); every decode step brings its new query from pinned
+        # host memory and returns the output to the host, both inside the
+        # timed region, on the world stream with the fused launch.
+        hq = q.cpu().pin_memory()
+        hout = torch.empty(outs["bf16"].shape, dtype=torch.bfloat16).pin_memory()
+        fused_bf16 = fd_step(_abi.TF_FD_FUSED, "bf16")
+
+        def e2e_step():
+            with torch.cuda.stream(sws):
+                q.copy_(hq, non_blocking=True)
+            fused_bf16()
+            with torch.cuda.stream(sws):
+                hout.copy_(outs["bf16"], non_blocking=True)
+
+        cooldown()
+        res["e2e"] = time_steps(ctx, stw, e2e_step, steps, warmup)
+        e2e_ok = ctx.all_true(bool(torch.equal(hout, outs["bf16"].cpu())))
         # The library's BSP schedule replayed from a CUDA graph (W = 1): the
         # host launch cost removed, its device-side stages kept.
         if W == 1:
@@ -542,7 +560,8 @@ def bench_fd(ctx, cfg, steps, warmup, pk, cooldown=lambda: None):
                 e["max_abs"] = max(e["max_abs"], ctx.max(float(diff.max())))
         num["batches_checked"] = sorted({0, B - 1})
         kv_bytes = 2 * B * Hkv * ln * d * 2
-        return dict(res=res, clocks=clocks, kv_bytes=kv_bytes, num=num, launches=launches, row_bytes=row * 4)
+        return dict(res=res, clocks=clocks, kv_bytes=kv_bytes, num=num, launches=launches, row_bytes=row * 4,
+                    e2e=dict(h2d=hq.numel() * 2, d2h=hout.numel() * 2, matches_device_run=e2e_ok))
     finally:
         w.close()
 
@@ -739,6 +758,10 @@ def fd_secondary(name, cfg, r, pk, W, cpu):
                         "frac": gbs / pk["hbm"], "algorithmic_bytes_per_launch": r["kv_bytes"],
                         "peak_source": pk["src"] + " copy bandwidth (MEASURED_PEAKS.json)"},
            "numerics": r["num"], "config": cfg, "clocks": r["clocks"]["fused"], "gpu_launches_fused": r["launches"]}
+    sec["e2e"] = {"value": res["e2e"]["ms"] * 1e3, "unit": "us", "h2d_bytes_per_step": r["e2e"]["h2d"],
+                  "d2h_bytes_per_step": r["e2e"]["d2h"], "matches_device_run": r["e2e"]["matches_device_run"],
+                  "what": "tf_flash_decode_async (fused) with the query H2D from pinned memory and the output D2H "
+                          "every step; the KV cache resident in HBM"}
     if "owner" in res:
         sec["owner_combine_us"] = res["owner"]["ms"] * 1e3
     if "bsp_graph" in res:
