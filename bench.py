@@ -516,6 +516,12 @@ def bench_fd(ctx, cfg, steps, warmup, pk, cooldown=lambda: None):
         cooldown()
         res["e2e"] = time_steps(ctx, stw, e2e_step, steps, warmup)
         e2e_ok = ctx.all_true(bool(torch.equal(hout, outs["bf16"].cpu())))
+        e2e_bytes = dict(h2d=hq.numel() * 2, d2h=hout.numel() * 2, matches_device_run=e2e_ok)
+        # Torch's pinned-host allocator recorded the world stream on these
+        # blocks; free them while that stream still exists (w.close()
+        # destroys it, and a later free would touch a dead stream).
+        torch.cuda.synchronize()
+        del hq, hout, e2e_step
         # The library's BSP schedule replayed from a CUDA graph (W = 1): the
         # host launch cost removed, its device-side stages kept.
         if W == 1:
@@ -527,6 +533,8 @@ def bench_fd(ctx, cfg, steps, warmup, pk, cooldown=lambda: None):
                 with torch.cuda.graph(gr, stream=cs):
                     _abi.check(w.lib.tf_flash_decode_async(*bargs))
                 res["bsp_graph"] = time_steps(ctx, torch.cuda.current_stream(), gr.replay, steps, warmup)
+                torch.cuda.synchronize()
+                del gr  # holds nodes on the world's resources: gone before w.close()
             except Exception as e:  # noqa: BLE001 -- reported, not fatal
                 res["bsp_graph_error"] = repr(e)[:200]
         # Numerics (the last timed runs' outputs): batch 0 (and the last
@@ -561,7 +569,7 @@ def bench_fd(ctx, cfg, steps, warmup, pk, cooldown=lambda: None):
         num["batches_checked"] = sorted({0, B - 1})
         kv_bytes = 2 * B * Hkv * ln * d * 2
         return dict(res=res, clocks=clocks, kv_bytes=kv_bytes, num=num, launches=launches, row_bytes=row * 4,
-                    e2e=dict(h2d=hq.numel() * 2, d2h=hout.numel() * 2, matches_device_run=e2e_ok))
+                    e2e=e2e_bytes)
     finally:
         w.close()
 
