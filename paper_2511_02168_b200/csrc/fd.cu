@@ -1193,11 +1193,11 @@ struct PostShared {
   int* src;
   float *wm, *fL, *fO;
 };
-// TAG: one instance per calling kernel, so each is register-allocated
-// under its own caller's budget.
-template <int TAG>
-__device__ __noinline__ void fd_post_phases(const FdParams& P, unsigned ranks_mask, unsigned long long* tr,
-                                            PostShared sh) {
+// Inlined into both kernels: as a separate (noinline) function it spilled
+// (432 B of spill loads) on the latency-critical fold chain -- ~3 us per
+// launch at config 3 (A/B against the round-1 build), ~2 us at config 4.
+__device__ __forceinline__ void fd_post_phases_body(const FdParams& P, unsigned ranks_mask,
+                                                    unsigned long long* tr, PostShared sh) {
   unsigned& s_item = *sh.item;
   int& s_last = *sh.last;
   int& s_src = *sh.src;
@@ -1407,9 +1407,18 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
   stamp(0);
   unsigned ranks_mask = 0;  // local ranks this CTA computed for
   __shared__ unsigned long long s_t0;  // CTA entry time (straggler model)
+  // Device epochs: loads issued now, consumed only by the post phases, so
+  // their L2 round trip overlaps the first item's claim and stream instead
+  // of delaying both (measured: ~1 us per launch at config 3).
+  uint64_t ep[3] = {0, 0, 0};
   if (threadIdx.x == 0) {
     s_t0 = globaltimer_ns();
-    fd_epochs_begin(P);
+    if (P.depoch) {
+      const volatile uint64_t* c = P.depoch;
+      ep[0] = c[P.owner ? 1 : 0];
+      ep[1] = c[2];
+      ep[2] = c[3];
+    }
   }
   if (tr && threadIdx.x == 0)
     for (int i = 1; i < kTraceSlots; ++i)
@@ -1450,7 +1459,15 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
     }
   }
   stamp(2);
-  fd_post_phases<0>(P, ranks_mask, tr, PostShared{&s_item, &s_last, &s_src, s_wm, s_fL, s_fO});
+  if (P.depoch) {
+    if (threadIdx.x == 0) {
+      s_fe = ep[0] + 1;
+      s_oe = ep[1] + 1;
+      s_ce = ep[2] + 1;
+    }
+    __syncthreads();
+  }
+  fd_post_phases_body(P, ranks_mask, tr, PostShared{&s_item, &s_last, &s_src, s_wm, s_fL, s_fO});
 }
 
 // ---- TMA-fed split partials (bf16 K/V, d = 128, 8 q-heads per KV head) ----
@@ -1879,7 +1896,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     tr[14] = smid;
     tr[2] = globaltimer_ns();
   }
-  fd_post_phases<1>(P, sm.ranks_mask, tr, PostShared{&s_item, &s_last, &s_src, s_wm, s_fL, s_fO});
+  fd_post_phases_body(P, sm.ranks_mask, tr, PostShared{&s_item, &s_last, &s_src, s_wm, s_fL, s_fO});
 }
 
 // Push this rank's published rows into every inbox slot `self` and signal
