@@ -2044,10 +2044,11 @@ static FdPlan fd_plan(int G, size_t len, unsigned grid) {
   size_t min_keys = 256;
   if (const char* e = std::getenv("TFB_FD_MINKEYS")) min_keys = std::max<size_t>(64, std::strtoull(e, nullptr, 10));
   const bool group_major = std::getenv("TFB_FD_GROUP_MAJOR") != nullptr;
-  // Items are remaining / (div * grid): a quarter of a CTA's fair share at
-  // most, so a CTA streaming ~15 % slower than the rest (measured spread)
-  // is still rebalanced by the items after its first.
-  int div = 4;
+  // Items are remaining / (div * grid): half a CTA's fair share at most, so
+  // a CTA streaming ~15 % slower than the rest (measured spread) is still
+  // rebalanced by the items after its first.  Config 4: div 1/2/3/4/6 ->
+  // 677/620/622/628/640 us (each item pays ~1.5 us of merge and refill).
+  int div = 2;
   if (const char* e = std::getenv("TFB_FD_CHUNKDIV")) div = std::max(1, std::atoi(e));
   const size_t ng = size_t(nlocal) * G;
   pl.gS.assign(ng, 0);
