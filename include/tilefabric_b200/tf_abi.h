@@ -269,6 +269,36 @@ tf_status tf_flash_decode_async(tf_world* w, tf_fd_variant variant,
                                 const void* const* k_shard,
                                 const void* const* v_shard, void* const* out,
                                 void* const* inbox_opt, void* const* streams);
+/* Paged KV cache (an extension: the reference lists paged KV as a non-goal,
+ * SPEC.md:327).  Rank r's K and V are page pools k_pool[r], v_pool[r]
+ * (kv_dtype), TF_PAGED_NHD [num_pages][page_size][kv_heads][head_dim] or
+ * TF_PAGED_HND [num_pages][kv_heads][page_size][head_dim] (one head's keys
+ * of a page contiguous: the faster layout for decode streaming),
+ * and block_tables[r]: int32 [batch][pages_per_seq] (device memory) maps
+ * the rank's local position x of sequence b (x < kv_len / W, the same
+ * position split as tf_flash_decode) to row x % page_size of page
+ * block_tables[r][b][x / page_size].  page_size is a power of two;
+ * pages_per_seq * page_size >= kv_len / W.  Every schedule, the wire rows
+ * and the output are bitwise those of tf_flash_decode over the same logical
+ * KV.  A table entry outside [0, num_pages) fails the call with
+ * TF_ERR_SHAPE (the device reads page 0 instead of faulting). */
+typedef enum { TF_PAGED_NHD = 0, TF_PAGED_HND = 1 } tf_paged_layout;
+typedef struct {
+  int page_size, pages_per_seq, num_pages;
+  tf_paged_layout layout;
+} tf_fd_paged;
+
+tf_status tf_flash_decode_paged(tf_world* w, tf_fd_variant variant, const tf_fd_shape* shape,
+                                const tf_fd_paged* paged, const void* const* q,
+                                const void* const* k_pool, const void* const* v_pool,
+                                const void* const* block_tables, void* const* out,
+                                void* const* inbox_opt, void* const* streams);
+tf_status tf_flash_decode_paged_async(tf_world* w, tf_fd_variant variant,
+                                      const tf_fd_shape* shape, const tf_fd_paged* paged,
+                                      const void* const* q, const void* const* k_pool,
+                                      const void* const* v_pool,
+                                      const void* const* block_tables, void* const* out,
+                                      void* const* inbox_opt, void* const* streams);
 /* The BSP schedule's two compute stages, for callers that bring their own
  * collective (e.g. NCCL all_gather_into_tensor of the rows in between, the
  * north_star's BSP baseline):

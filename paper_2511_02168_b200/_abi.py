@@ -60,6 +60,7 @@ TF_AG_BASELINE, TF_AG_PULL, TF_AG_PUSH = 0, 1, 2
 TF_FD_BSP, TF_FD_INDEPENDENT_AG, TF_FD_FINE_WAITS, TF_FD_FUSED, TF_FD_FUSED_BY_ARRIVAL = 0, 1, 2, 3, 4
 TF_FD_FUSED_OWNER = 5
 TF_F32, TF_BF16 = 0, 1
+TF_PAGED_NHD, TF_PAGED_HND = 0, 1
 TF_OK, TF_ERR_CONFIG, TF_ERR_BOUNDS, TF_ERR_SHAPE, TF_ERR_DEADLOCK, TF_ERR_WORLD = 0, 1, 2, 3, 4, 5
 TF_ERR_EMPTY_ATTENTION, TF_ERR_NUMERIC, TF_ERR_CUDA = 6, 7, 8
 IPC_HANDLE_BYTES = 64
@@ -83,6 +84,12 @@ class Taxes(C.Structure):
 
     def as_dict(self):
         return {f: int(getattr(self, f)) for f, _ in self._fields_}
+
+
+class FdPaged(C.Structure):
+    """tf_fd_paged: page pools NHD [num_pages][page_size][kv_heads][d] (layout 0) or
+    HND [num_pages][kv_heads][page_size][d] (layout 1) + block tables."""
+    _fields_ = [("page_size", C.c_int), ("pages_per_seq", C.c_int), ("num_pages", C.c_int), ("layout", C.c_int)]
 
 
 # name -> (restype, argtypes); every symbol tf_abi.h declares.
@@ -120,6 +127,10 @@ SIGNATURES = {
     "tf_flash_decode": (C.c_int, [_P, C.c_int, C.POINTER(FdShape), _PP, _PP, _PP, _PP, _PP, _PP]),
     "tf_flash_decode_async": (C.c_int, [_P, C.c_int, C.POINTER(FdShape), _PP, _PP, _PP, _PP,
                                         _PP, _PP]),
+    "tf_flash_decode_paged": (C.c_int, [_P, C.c_int, C.POINTER(FdShape), C.POINTER(FdPaged), _PP, _PP, _PP, _PP,
+                                        _PP, _PP, _PP]),
+    "tf_flash_decode_paged_async": (C.c_int, [_P, C.c_int, C.POINTER(FdShape), C.POINTER(FdPaged), _PP, _PP, _PP,
+                                              _PP, _PP, _PP, _PP]),
     "tf_fd_partial_async": (C.c_int, [_P, C.POINTER(FdShape), _PP, _PP, _PP, _PP, _PP]),
     "tf_fd_combine_async": (C.c_int, [_P, C.POINTER(FdShape), _PP, _PP, _PP]),
     "tf_fd_flag_counts": (C.c_int, [_P, C.c_int, C.POINTER(C.c_uint64), C.c_size_t,

@@ -32,7 +32,7 @@ struct DevErr {
   unsigned long long rank_waits[64], rank_wait_ns[64], rank_barriers[64], rank_barrier_ns[64];
 };
 
-enum : int { kWaitSignal = 0, kWaitBarrier = 1, kNumeric = 2, kEmpty = 3 };
+enum : int { kWaitSignal = 0, kWaitBarrier = 1, kNumeric = 2, kEmpty = 3, kPage = 4 };
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;

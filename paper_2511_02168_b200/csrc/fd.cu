@@ -71,6 +71,7 @@ struct FdRank {
   uint64_t* flags;   // [W][G] local flag board
   int rank;          // global rank id
   uint64_t skew_ns;  // straggler delay before this rank's compute (fabric.hpp:59-62)
+  const int* pages;  // paged KV: block table [B][pps] into this rank's pool (else null)
 };
 
 struct FdParams {
@@ -124,8 +125,30 @@ struct FdParams {
   unsigned nitems;
   const int* gS;
   unsigned* fstate;
+  // Paged KV (tf_flash_decode_paged): k / v of each rank are page pools,
+  // NHD [num_pages][1 << page_shift][Hkv][d] or (hnd) HND
+  // [num_pages][Hkv][1 << page_shift][d]; key x of batch b sits in row
+  // x & (page - 1) of page pages[b * pps + (x >> page_shift)].
+  int paged, page_shift, pps, num_pages, hnd;
   FdRank r[kMaxLocal];
 };
+
+// Paged KV: the pool row (in units of d elements) of key x of batch b, KV
+// head kvh.  An entry outside the pool raises TF_ERR_SHAPE (kPage) and reads
+// page 0, so a bad table never faults the device.
+__device__ __forceinline__ size_t paged_row_of(const FdParams& P, int pg, size_t x, int kvh, int b, int rank) {
+  const size_t slot = x >> P.page_shift;
+  if (unsigned(pg) >= unsigned(P.num_pages)) {
+    raise_err(P.err, TF_ERR_SHAPE, kPage, rank, -1, b, int(slot), uint64_t(P.num_pages), uint64_t(unsigned(pg)), 0);
+    pg = 0;
+  }
+  const size_t in_page = x & ((size_t(1) << P.page_shift) - 1);
+  return P.hnd ? ((size_t(pg) * P.Hkv + kvh) << P.page_shift) + in_page
+               : ((size_t(pg) << P.page_shift) + in_page) * size_t(P.Hkv) + kvh;
+}
+__device__ __forceinline__ size_t paged_row(const FdParams& P, const int* tbl, size_t x, int kvh, int b, int rank) {
+  return paged_row_of(P, __ldg(tbl + (x >> P.page_shift)), x, kvh, b, rank);
+}
 
 __device__ __forceinline__ int split_count(const FdParams& P, int lr, int g) {
   (void)lr;  // every rank cuts the same splits
@@ -261,6 +284,7 @@ __device__ void generic_split(const FdParams& P, int lr, int g, int sp, float* w
   const size_t k1 = min(P.len, k0 + P.split_len);
   const int d = P.d;
   const size_t kvbase = (size_t(b) * P.Hkv + kvh) * P.len * d;
+  const int* tbl = P.paged ? R.pages + size_t(b) * P.pps : nullptr;
   for (int h = warp; h < P.gs; h += blockDim.x >> 5) {
     const int hq = kvh * P.gs + h;
     const size_t qbase = (size_t(b) * P.Hq + hq) * d;
@@ -274,10 +298,11 @@ __device__ void generic_split(const FdParams& P, int lr, int g, int sp, float* w
     float m = -INFINITY, l = 0.0f;
     for (size_t j = k0; j < k1; ++j) {
       float part = 0.0f;
+      const size_t kvj = tbl ? paged_row(P, tbl, j, kvh, b, R.rank) * d : kvbase + j * d;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int e = lane + 32 * i;
-        if (e < d) part = __fadd_rn(part, __fmul_rn(q[i], load_kv(R.k, kvbase + j * d + e, P.kv_bf16)));
+        if (e < d) part = __fadd_rn(part, __fmul_rn(q[i], load_kv(R.k, kvj + e, P.kv_bf16)));
       }
 #pragma unroll
       for (int off = 16; off; off >>= 1) part = __fadd_rn(part, __shfl_xor_sync(0xffffffffu, part, off));
@@ -296,7 +321,7 @@ __device__ void generic_split(const FdParams& P, int lr, int g, int sp, float* w
       for (int i = 0; i < 8; ++i) {
         const int e = lane + 32 * i;
         if (e < d)
-          o[i] = __fadd_rn(__fmul_rn(o[i], alpha), __fmul_rn(w, load_kv(R.v, kvbase + j * d + e, P.kv_bf16)));
+          o[i] = __fadd_rn(__fmul_rn(o[i], alpha), __fmul_rn(w, load_kv(R.v, kvj + e, P.kv_bf16)));
       }
       m = mn;
     }
@@ -353,10 +378,15 @@ __device__ __forceinline__ int fast_d(int i, int j, int r) {
 
 // One warp: keys [kb, ke) of the group's stream; leaves its log2-domain
 // partial for the 8 heads in smem (m2[8], l[8], o[8][128]).
-template <bool HILO>
+// PAGED: K / V are the rank's page pools and every 16-key tile looks its
+// two rows up in the batch's block table `tbl` (L1-resident; the rows of a
+// tile may sit in two pages) -- the same keys in the same order, so a paged
+// run is bitwise the contiguous run of the same logical KV.
+template <bool HILO, bool PAGED>
 __device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
                                 const __nv_bfloat16* V, const __nv_bfloat16* Q, size_t kb,
-                                size_t ke, int stride, float* sm_m, float* sm_l, float* sm_o, int* bad) {
+                                size_t ke, int stride, float* sm_m, float* sm_l, float* sm_o, int* bad,
+                                const int* tbl = nullptr, int kvh = 0, int b = 0, int rank = 0) {
   const int lane = threadIdx.x & 31;
   const int gq = lane >> 2, t = lane & 3;
   const float sl2 = P.scale * kLog2e;
@@ -382,17 +412,38 @@ __device__ void fast_warp_range(const FdParams& P, const __nv_bfloat16* K,
   //  128-register budget 16 warps/SM need and lost 10 %; the loads are issued
   //  at the top of each tile instead and the 16 resident warps overlap them.)
   // 16-key tiles kb, kb + stride, ... below ke.
+  // PAGED: the block-table entries of the next tile's two rows are loaded
+  // one tile ahead, so a tile's K/V loads never wait on a table lookup.
+  int pg_a = 0, pg_b = 0;
+  if (PAGED) {
+    const int rem0 = int(ke - kb) - gq;
+    if (rem0 > 0) pg_a = __ldg(tbl + ((ke - size_t(rem0)) >> P.page_shift));
+    if (rem0 > 8) pg_b = __ldg(tbl + ((ke - size_t(rem0) + 8) >> P.page_shift));
+  }
   for (int rem = int(ke - kb) - gq; rem > -gq; rem -= stride, kp += size_t(stride) * 128, vp += size_t(stride) * 128) {
     const bool va = rem > 0, vb = rem > 8;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      k_a[i] = va ? ldg_stream(kp + 32 * i, pol) : z;
-      k_b[i] = vb ? ldg_stream(kp + 8 * 128 + 32 * i, pol) : z;
+    const __nv_bfloat16 *ka_p = kp, *kb_p = kp + 8 * 128, *va_p = vp, *vb_p = vp + 8 * 128;
+    if (PAGED) {
+      const size_t x = ke - size_t(rem);  // row a's key (row b: x + 8)
+      const size_t oa = va ? paged_row_of(P, pg_a, x, kvh, b, rank) * 128 + 8 * t : 0;
+      const size_t ob = vb ? paged_row_of(P, pg_b, x + 8, kvh, b, rank) * 128 + 8 * t : 0;
+      const int rn = rem - stride;
+      pg_a = rn > 0 ? __ldg(tbl + ((x + stride) >> P.page_shift)) : 0;
+      pg_b = rn > 8 ? __ldg(tbl + ((x + stride + 8) >> P.page_shift)) : 0;
+      ka_p = K + oa;
+      kb_p = K + ob;
+      va_p = V + oa;
+      vb_p = V + ob;
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      v_a[i] = va ? ldg_stream(vp + 32 * i, pol) : z;
-      v_b[i] = vb ? ldg_stream(vp + 8 * 128 + 32 * i, pol) : z;
+      k_a[i] = va ? ldg_stream(ka_p + 32 * i, pol) : z;
+      k_b[i] = vb ? ldg_stream(kb_p + 32 * i, pol) : z;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v_a[i] = va ? ldg_stream(va_p + 32 * i, pol) : z;
+      v_b[i] = vb ? ldg_stream(vb_p + 32 * i, pol) : z;
     }
     // S^T = K . Q^T over 8 k-steps of 16 d.
     float s[4] = {0.f, 0.f, 0.f, 0.f};
@@ -505,7 +556,7 @@ struct FastSmem {
   unsigned long long wend[kFastWarps];  // TFB_TRACE: per-warp finish times
 };
 
-template <bool HILO>
+template <bool HILO, bool PAGED>
 __device__ void fast_split(const FdParams& P, int lr, int g, int sp, float* wsrow,
                            FastSmem& sm) {
   const FdRank& R = P.r[lr];
@@ -537,8 +588,13 @@ __device__ void fast_split(const FdParams& P, int lr, int g, int sp, float* wsro
   for (int i = threadIdx.x; i < 8 * 16; i += blockDim.x) sm.q[i] = reinterpret_cast<const uint4*>(Q)[i];
   __syncthreads();
   trace_at(P, 12);
-  fast_warp_range<HILO>(P, K, V, reinterpret_cast<const __nv_bfloat16*>(sm.q), wb, we, stride, sm.m[warp], sm.l[warp],
-                  sm.o[warp], &sm.bad);
+  if (PAGED)
+    fast_warp_range<HILO, true>(P, static_cast<const __nv_bfloat16*>(R.k), static_cast<const __nv_bfloat16*>(R.v),
+                                reinterpret_cast<const __nv_bfloat16*>(sm.q), wb, we, stride, sm.m[warp], sm.l[warp],
+                                sm.o[warp], &sm.bad, R.pages + size_t(b) * P.pps, kvh, b, R.rank);
+  else
+    fast_warp_range<HILO, false>(P, K, V, reinterpret_cast<const __nv_bfloat16*>(sm.q), wb, we, stride, sm.m[warp],
+                                 sm.l[warp], sm.o[warp], &sm.bad);
   if (P.trace && (threadIdx.x & 31) == 0) sm.wend[warp] = globaltimer_ns();
   __syncthreads();
   trace_at(P, 13);
@@ -1389,7 +1445,9 @@ __device__ __forceinline__ void fd_post_phases_body(const FdParams& P, unsigned 
 }
 
 // ---- the persistent kernel ------------------------------------------------
-// MODE: 0 generic split, 1 fast split with bf16 P, 2 fast split with hi/lo P.
+// MODE: 0 generic split, 1 fast split with bf16 P, 2 fast split with hi/lo P,
+// 3 / 4 the same over a paged KV cache (own instances: the contiguous
+// kernels keep their register allocation).
 template <int MODE>
 __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __grid_constant__ FdParams P) {
   __shared__ unsigned int s_item;
@@ -1440,8 +1498,10 @@ __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __g
     }
     float* grp = P.ws + ((size_t(lr) * G + g) * P.S) * P.gs * wrl;
     float* wsrow = grp + size_t(sp) * P.gs * wrl;
-    if (MODE == 2) fast_split<true>(P, lr, g, sp, wsrow, fsm);
-    else if (MODE == 1) fast_split<false>(P, lr, g, sp, wsrow, fsm);
+    if (MODE == 2) fast_split<true, false>(P, lr, g, sp, wsrow, fsm);
+    else if (MODE == 1) fast_split<false, false>(P, lr, g, sp, wsrow, fsm);
+    else if (MODE == 4) fast_split<true, true>(P, lr, g, sp, wsrow, fsm);
+    else if (MODE == 3) fast_split<false, true>(P, lr, g, sp, wsrow, fsm);
     else generic_split(P, lr, g, sp, wsrow);
     stamp(1);
     if (tr && threadIdx.x == 0) {
@@ -2125,6 +2185,8 @@ void fd_preload() {  // see ag_exact_preload
   cudaFuncGetAttributes(&a, fd_attention_kernel<0>);
   cudaFuncGetAttributes(&a, fd_attention_kernel<1>);
   cudaFuncGetAttributes(&a, fd_attention_kernel<2>);
+  cudaFuncGetAttributes(&a, fd_attention_kernel<3>);
+  cudaFuncGetAttributes(&a, fd_attention_kernel<4>);
   cudaFuncGetAttributes(&a, fd_stream_kernel<false>);
   cudaFuncGetAttributes(&a, fd_stream_kernel<true>);
   cudaFuncGetAttributes(&a, fd_push_kernel);
@@ -2141,10 +2203,31 @@ using namespace tfb;
 // rows [B][Hq][d+2] landing in rows_out[r] instead of the heap.
 static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape* shape, const void* const* q,
                           const void* const* k_shard, const void* const* v_shard, void* const* out,
-                          void* const* inbox_opt, void* const* streams, void* const* rows_out) {
+                          void* const* inbox_opt, void* const* streams, void* const* rows_out,
+                          const tf_fd_paged* paged = nullptr, const void* const* tables = nullptr) {
   if (!tw) return set_error(TF_ERR_CONFIG, "tf_flash_decode: NULL world");
   World* w = &tw->impl;
   TFB_CHECK(fd_validate(w, shape, q, k_shard, v_shard, rows_out ? rows_out : out));
+  int page_shift = 0;
+  if (paged) {
+    const size_t len_r = shape->kv_len / size_t(w->W);
+    const int ps = paged->page_size;
+    if (ps < 1 || ps > (1 << 20) || (ps & (ps - 1)))
+      return set_error(TF_ERR_CONFIG, "flash_decode_paged: page_size must be a power of two in [1, 2^20]");
+    while ((1 << page_shift) < ps) ++page_shift;
+    if (paged->layout != TF_PAGED_NHD && paged->layout != TF_PAGED_HND)
+      return set_error(TF_ERR_CONFIG, "flash_decode_paged: layout must be TF_PAGED_NHD or TF_PAGED_HND");
+    if (paged->num_pages < 1)
+      return set_error(TF_ERR_CONFIG, "flash_decode_paged: num_pages must be >= 1");
+    if (size_t(paged->pages_per_seq) * size_t(ps) < len_r)
+      return set_error(TF_ERR_SHAPE, "flash_decode_paged: pages_per_seq * page_size = " +
+                                         std::to_string(size_t(paged->pages_per_seq) * size_t(ps)) +
+                                         " < kv_len / world_size = " + std::to_string(len_r));
+    if (!tables) return set_error(TF_ERR_CONFIG, "flash_decode_paged: NULL block tables");
+    for (int r = 0; r < w->W; ++r)
+      if (w->ranks[r].local && !tables[r])
+        return set_error(TF_ERR_CONFIG, "flash_decode_paged: NULL block table for rank " + std::to_string(r));
+  }
   if (variant < TF_FD_BSP || variant > TF_FD_FUSED_OWNER)
     return set_error(TF_ERR_CONFIG, "run_fd: unknown variant");
   const tf_fd_shape& sh = *shape;
@@ -2162,7 +2245,7 @@ static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape
   const bool fast = fast_ok(sh);
   // TMA-fed kernel (fd_stream_kernel) with a guided item table, else the
   // register-streaming kernel with S equal splits per group.
-  const bool stream = fd_stream_ok(sh, w, q, k_shard, v_shard);
+  const bool stream = !paged && fd_stream_ok(sh, w, q, k_shard, v_shard);  // paged: register kernel
   // The plan is a function of (G, len, grid, knobs): built and uploaded
   // once per geometry; later calls only need its size and split count.
   FdPlan plan;
@@ -2299,6 +2382,13 @@ static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape
   P.Hq = sh.q_heads;
   P.Hkv = sh.kv_heads;
   P.gs = gs;
+  if (paged) {
+    P.paged = 1;
+    P.page_shift = page_shift;
+    P.pps = paged->pages_per_seq;
+    P.num_pages = paged->num_pages;
+    P.hnd = paged->layout == TF_PAGED_HND;
+  }
   P.d = d;
   P.len = len;
   P.S = S_eff;
@@ -2363,7 +2453,8 @@ static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape
           Q.r[i] = FdRank{q[r], k_shard[r], v_shard[r], out ? out[r] : nullptr,
                           rows_out ? static_cast<float*>(rows_out[r]) : reinterpret_cast<float*>(w->ptr(r, pub_off)),
                           inbox_of(r),
-                          reinterpret_cast<uint64_t*>(w->ptr(r, fb.offset)), r, w->skew_of(r)};
+                          reinterpret_cast<uint64_t*>(w->ptr(r, fb.offset)), r, w->skew_of(r),
+                          paged ? static_cast<const int*>(tables[r]) : nullptr};
         }
         Q.err = w->err_of(lead);
         Q.ws = reinterpret_cast<float*>(w->ptr(lead, ws_off));
@@ -2450,17 +2541,21 @@ static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape
           continue;
         }
         const unsigned items = unsigned(Q.nlocal) * G * S_eff;
-        const int mode = !fast ? 0 : (hilo ? 2 : 1);
+        const int mode = !fast ? 0 : (hilo ? 2 : 1) + (paged ? 2 : 0);
         const void* kfn = mode == 0 ? reinterpret_cast<const void*>(fd_attention_kernel<0>)
                         : mode == 1 ? reinterpret_cast<const void*>(fd_attention_kernel<1>)
-                                    : reinterpret_cast<const void*>(fd_attention_kernel<2>);
+                        : mode == 2 ? reinterpret_cast<const void*>(fd_attention_kernel<2>)
+                        : mode == 3 ? reinterpret_cast<const void*>(fd_attention_kernel<3>)
+                                    : reinterpret_cast<const void*>(fd_attention_kernel<4>);
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kFastThreads, 0);
         const unsigned grid =
             std::max(1u, std::min(items, unsigned(std::max(per_sm, 1) * w->sm_count)));
         if (mode == 0) fd_attention_kernel<0><<<grid, kFastThreads, 0, st[lead]>>>(Q);
         else if (mode == 1) fd_attention_kernel<1><<<grid, kFastThreads, 0, st[lead]>>>(Q);
-        else fd_attention_kernel<2><<<grid, kFastThreads, 0, st[lead]>>>(Q);
+        else if (mode == 2) fd_attention_kernel<2><<<grid, kFastThreads, 0, st[lead]>>>(Q);
+        else if (mode == 3) fd_attention_kernel<3><<<grid, kFastThreads, 0, st[lead]>>>(Q);
+        else fd_attention_kernel<4><<<grid, kFastThreads, 0, st[lead]>>>(Q);
         TFB_CUDA(cudaGetLastError());
         ++w->launches;
         // Ranks sharing the launch are complete when it is: order their streams.
@@ -2558,6 +2653,28 @@ extern "C" tf_status tf_flash_decode_async(tf_world* tw, tf_fd_variant variant,
                                            const void* const* v_shard, void* const* out,
                                            void* const* inbox_opt, void* const* streams) {
   return fd_async(tw, variant, shape, q, k_shard, v_shard, out, inbox_opt, streams, nullptr);
+}
+
+// Paged KV cache (an extension beyond the reference API: its SPEC lists
+// paged KV as a non-goal).  Same schedules, wire format and
+// fold as tf_flash_decode; the K/V of each rank are page pools addressed
+// through per-rank block tables.
+extern "C" tf_status tf_flash_decode_paged_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape* shape,
+                                                 const tf_fd_paged* paged, const void* const* q,
+                                                 const void* const* k_pool, const void* const* v_pool,
+                                                 const void* const* block_tables, void* const* out,
+                                                 void* const* inbox_opt, void* const* streams) {
+  if (!paged) return set_error(TF_ERR_CONFIG, "flash_decode_paged: NULL paged layout");
+  return fd_async(tw, variant, shape, q, k_pool, v_pool, out, inbox_opt, streams, nullptr, paged, block_tables);
+}
+
+extern "C" tf_status tf_flash_decode_paged(tf_world* tw, tf_fd_variant variant, const tf_fd_shape* shape,
+                                           const tf_fd_paged* paged, const void* const* q, const void* const* k_pool,
+                                           const void* const* v_pool, const void* const* block_tables,
+                                           void* const* out, void* const* inbox_opt, void* const* streams) {
+  TFB_CHECK(tf_flash_decode_paged_async(tw, variant, shape, paged, q, k_pool, v_pool, block_tables, out, inbox_opt,
+                                        streams));
+  return sync_and_check(&tw->impl, resolve_streams(&tw->impl, streams));
 }
 
 // attention_partial + serialize_partial of every (b, q-head) for each local

@@ -200,6 +200,11 @@ tf_status check_record(World* w) {
       msg = rank + "attention_partial: non-finite score at head " +
             std::to_string(e->aux >> 32) + ", position " + std::to_string(e->aux & 0xffffffffu);
       break;
+    case kPage:
+      msg = rank + "flash_decode (paged KV): block table entry " + std::to_string(e->observed) +
+            " at batch " + std::to_string(e->row) + ", page slot " + std::to_string(e->slot) +
+            " is outside the pool of " + std::to_string(e->expected) + " pages";
+      break;
     case kEmpty:
       msg = rank + "finalize: head " + std::to_string(e->aux) +
             " has an empty normalizer (no keys folded)";

@@ -346,6 +346,18 @@ class fd:  # namespace tilefabric::fd
         owner_combine: bool = False  # extension: TF_FD_FUSED_OWNER
 
     @dataclass
+    class PagedLayout:
+        """Paged KV cache (an extension: SPEC.md:327 lists paged KV as a
+        non-goal of the reference).  Each rank's positions of every sequence
+        are cut into pages of `page_size` keys, scattered over a pool of
+        B * pages_per_seq + spare_pages pages by a seeded permutation
+        (tf_fd_paged; pool [num_pages][page_size][kv_heads][d])."""
+        page_size: int = 16
+        spare_pages: int = 3
+        seed: int = 0
+        hnd: bool = False  # pool layout: NHD [pages][ps][Hkv][d], HND [pages][Hkv][ps][d]
+
+    @dataclass
     class FdRun:
         """flash_decode.hpp:116-123 (+ each rank's inbox and the launch count)."""
         out: List[np.ndarray]
@@ -367,8 +379,11 @@ class fd:  # namespace tilefabric::fd
 
     @staticmethod
     def run_fd(p: "fd.DecodeProblem", variant, cfg: WorldConfig, opts: Optional["fd.FdOptions"] = None,
-               dtype: int = _abi.TF_F32, out_dtype: Optional[int] = None):
-        """flash_decode.hpp:425-438"""
+               dtype: int = _abi.TF_F32, out_dtype: Optional[int] = None,
+               paged: Optional["fd.PagedLayout"] = None, bad_page: bool = False):
+        """flash_decode.hpp:425-438.  paged: the same problem through
+        tf_flash_decode_paged (K/V scattered into page pools); bad_page:
+        corrupt one block-table entry (error-path test)."""
         if opts is not None and opts.owner_combine:
             if int(variant) != _abi.TF_FD_FUSED or opts.fold_by_arrival:
                 raise ConfigError("owner_combine applies to the fused schedule (ascending fold) only")
@@ -395,21 +410,56 @@ class fd:  # namespace tilefabric::fd
             q = torch.from_numpy(np.ascontiguousarray(p.q, np.float32)).reshape(B, H, d).to(tdt)
             k = torch.from_numpy(np.ascontiguousarray(p.k, np.float32)).reshape(B, Hkv, L, d).to(tdt)
             v = torch.from_numpy(np.ascontiguousarray(p.v, np.float32)).reshape(B, Hkv, L, d).to(tdt)
-            qs, ks, vs, outs = [], [], [], []
+            qs, ks, vs, outs, tables = [], [], [], [], []
+            pl = None
+            if paged is not None:
+                ps = paged.page_size
+                pps = -(-ln // ps)
+                pl = _abi.FdPaged(ps, pps, B * pps + paged.spare_pages,
+                                  _abi.TF_PAGED_HND if paged.hnd else _abi.TF_PAGED_NHD)
             for r in range(W):
                 dev = torch.device("cuda", w.devices[r])
                 qs.append(q.to(dev))
-                ks.append(k[:, :, r * ln:(r + 1) * ln].contiguous().to(dev))  # slice_shard :140-160
-                vs.append(v[:, :, r * ln:(r + 1) * ln].contiguous().to(dev))
+                kr = k[:, :, r * ln:(r + 1) * ln].contiguous()  # slice_shard :140-160
+                vr = v[:, :, r * ln:(r + 1) * ln].contiguous()
+                if pl is not None:
+                    # [B][Hkv][ln][d] -> pages [B*pps][ps][Hkv][d] at permuted pool slots
+                    perm = np.random.default_rng(paged.seed + r).permutation(pl.num_pages)[: B * pps]
+                    tbl = torch.from_numpy(perm.astype(np.int32)).reshape(B, pps)
+                    if bad_page:
+                        tbl[B - 1, pps - 1] = pl.num_pages + 5
+                    pools = []
+                    for t in (kr, vr):
+                        pad = torch.zeros(B, Hkv, pps * ps, d, dtype=t.dtype)
+                        pad[:, :, :ln] = t
+                        if paged.hnd:
+                            pages = pad.reshape(B, Hkv, pps, ps, d).permute(0, 2, 1, 3, 4).reshape(B * pps, Hkv, ps, d)
+                        else:
+                            pages = pad.reshape(B, Hkv, pps, ps, d).permute(0, 2, 3, 1, 4).reshape(B * pps, ps, Hkv, d)
+                        pool = torch.full((pl.num_pages,) + tuple(pages.shape[1:]), float("nan"), dtype=t.dtype)
+                        pool[torch.from_numpy(perm)] = pages
+                        pools.append(pool.to(dev))
+                    ks.append(pools[0])
+                    vs.append(pools[1])
+                    tables.append(tbl.to(dev))
+                else:
+                    ks.append(kr.to(dev))
+                    vs.append(vr.to(dev))
                 outs.append(torch.empty((B, H, d), dtype=tod, device=dev))
             torch.cuda.synchronize()
             shape = _abi.FdShape(B, H, Hkv, d, L, p.scale, dtype, odt)
             before = w.launches()
-            _abi.check(w.lib.tf_flash_decode(
-                w.handle, int(variant), C.byref(shape),
-                _abi.ptr_array([t.data_ptr() for t in qs]), _abi.ptr_array([t.data_ptr() for t in ks]),
-                _abi.ptr_array([t.data_ptr() for t in vs]), _abi.ptr_array([t.data_ptr() for t in outs]),
-                _abi.ptr_array(inbox), None))
+            ptrs = (_abi.ptr_array([t.data_ptr() for t in qs]), _abi.ptr_array([t.data_ptr() for t in ks]),
+                    _abi.ptr_array([t.data_ptr() for t in vs]))
+            if pl is not None:
+                _abi.check(w.lib.tf_flash_decode_paged(
+                    w.handle, int(variant), C.byref(shape), C.byref(pl), *ptrs,
+                    _abi.ptr_array([t.data_ptr() for t in tables]),
+                    _abi.ptr_array([t.data_ptr() for t in outs]), _abi.ptr_array(inbox), None))
+            else:
+                _abi.check(w.lib.tf_flash_decode(
+                    w.handle, int(variant), C.byref(shape), *ptrs,
+                    _abi.ptr_array([t.data_ptr() for t in outs]), _abi.ptr_array(inbox), None))
             launches = w.launches() - before
             taxes = [w.taxes(r) for r in range(W)]
             out = [o.float().cpu().numpy().reshape(B * H, d) if B > 1 else
