@@ -178,10 +178,19 @@ tf_status tf_signal_soak(tf_world* w, uint64_t seed, int rounds,
  * multi-rank schedule returns TF_ERR_CONFIG.  Arrays are indexed by global rank;
  * entries for ranks not local to this process are ignored except a_shard,
  * whose peer entries must be the heap mappings tf_heap_alloc returned. */
+/* How A is sharded before the all-gather.  TF_SHARD_K (0, the reference,
+ * ag_gemm.hpp:100-107): rank r holds columns [r*k/W, (r+1)*k/W), an m x k/W
+ * shard.  TF_SHARD_M (1, an extension: the alternative sharding the paper
+ * lists and the reference leaves out): rank r holds rows
+ * [r*m/W, (r+1)*m/W), an (m/W) x k shard; bf16 only, m/W a multiple of
+ * 128; the gathered operand and C are the same m x k / m x n. */
+typedef enum { TF_SHARD_K = 0, TF_SHARD_M = 1 } tf_ag_shard;
+
 typedef struct {
   size_t m, n, k;
   size_t bm, bn, bk; /* TileSpec; 0 -> 16 (tilemath.hpp:79-81) */
   tf_dtype dtype;
+  tf_ag_shard shard; /* zero-initialised = TF_SHARD_K, the reference's layout */
 } tf_ag_shape;
 
 tf_status tf_ag_gemm(tf_world* w, tf_ag_variant variant, const tf_ag_shape* shape,

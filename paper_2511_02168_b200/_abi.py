@@ -61,6 +61,7 @@ TF_FD_BSP, TF_FD_INDEPENDENT_AG, TF_FD_FINE_WAITS, TF_FD_FUSED, TF_FD_FUSED_BY_A
 TF_FD_FUSED_OWNER = 5
 TF_F32, TF_BF16 = 0, 1
 TF_PAGED_NHD, TF_PAGED_HND = 0, 1
+TF_SHARD_K, TF_SHARD_M = 0, 1
 TF_OK, TF_ERR_CONFIG, TF_ERR_BOUNDS, TF_ERR_SHAPE, TF_ERR_DEADLOCK, TF_ERR_WORLD = 0, 1, 2, 3, 4, 5
 TF_ERR_EMPTY_ATTENTION, TF_ERR_NUMERIC, TF_ERR_CUDA = 6, 7, 8
 IPC_HANDLE_BYTES = 64
@@ -68,7 +69,8 @@ IPC_HANDLE_BYTES = 64
 
 class AgShape(C.Structure):
     _fields_ = [("m", C.c_size_t), ("n", C.c_size_t), ("k", C.c_size_t),
-                ("bm", C.c_size_t), ("bn", C.c_size_t), ("bk", C.c_size_t), ("dtype", C.c_int)]
+                ("bm", C.c_size_t), ("bn", C.c_size_t), ("bk", C.c_size_t), ("dtype", C.c_int),
+                ("shard", C.c_int)]  # tf_ag_shard: 0 K (the reference), 1 M
 
 
 class FdShape(C.Structure):

@@ -19,14 +19,23 @@ static tf_status ag_validate(World* w, const tf_ag_shape* sh, void* const* a_sha
                                         std::to_string(w->W));
   if (sh->dtype != TF_F32 && sh->dtype != TF_BF16)
     return set_error(TF_ERR_CONFIG, "ag_gemm: unknown dtype");
+  if (sh->shard != TF_SHARD_K && sh->shard != TF_SHARD_M)
+    return set_error(TF_ERR_CONFIG, "ag_gemm: unknown shard layout");
+  const bool msh = sh->shard == TF_SHARD_M;
+  if (msh && sh->dtype != TF_BF16)
+    return set_error(TF_ERR_CONFIG, "ag_gemm: M-sharded A is supported on the bf16 tensor-core path");
+  if (msh && sh->m % (size_t(w->W) * 128) != 0)
+    return set_error(TF_ERR_SHAPE, "ag_gemm (M-sharded): m = " + std::to_string(sh->m) +
+                                       " must be a multiple of 128 * world_size");
   const size_t esz = sh->dtype == TF_F32 ? 4 : 2;
   const size_t kw = sh->k / size_t(w->W);
+  const size_t shard_elems = msh ? sh->m / size_t(w->W) * sh->k : sh->m * kw;
   for (int r = 0; r < w->W; ++r) {
     if (!a_shard[r])
       return set_error(TF_ERR_CONFIG, "ag_gemm: a_shard[" + std::to_string(r) + "] is NULL");
-    if (!in_heap(w, r, a_shard[r], esz * sh->m * kw))
-      return set_error(TF_ERR_BOUNDS, "ag_gemm: a_shard[" + std::to_string(r) +
-                                          "] is not an m x k/W region of rank " +
+    if (!in_heap(w, r, a_shard[r], esz * shard_elems))
+      return set_error(TF_ERR_BOUNDS, "ag_gemm: a_shard[" + std::to_string(r) + "] is not an " +
+                                          (msh ? "m/W x k" : "m x k/W") + " region of rank " +
                                           std::to_string(r) + "'s symmetric heap");
     if (w->ranks[r].local && (!b[r] || !c[r]))
       return set_error(TF_ERR_CONFIG, "ag_gemm: b/c for local rank " + std::to_string(r) +
@@ -113,8 +122,12 @@ extern "C" tf_status tf_ag_gathered(tf_world* tw, int rank, void* dst, size_t by
   TFB_CHECK(sync_and_check(w, resolve_streams(w, nullptr)));
   for (int s = 0; s < w->W; ++s) {
     const World::AgBlock& b = w->ag_src[rank][s];
-    TFB_CUDA(cudaMemcpy2D(static_cast<char*>(dst) + size_t(s) * kw * esz, k * esz,
-                          static_cast<const char*>(b.p), b.pitch * esz, kw * esz, m, cudaMemcpyDefault));
+    if (w->ag_msharded)  // block s: rows [s*m/W, (s+1)*m/W), every column
+      TFB_CUDA(cudaMemcpy2D(static_cast<char*>(dst) + size_t(s) * (m / w->W) * k * esz, k * esz,
+                            static_cast<const char*>(b.p), b.pitch * esz, k * esz, m / w->W, cudaMemcpyDefault));
+    else
+      TFB_CUDA(cudaMemcpy2D(static_cast<char*>(dst) + size_t(s) * kw * esz, k * esz,
+                            static_cast<const char*>(b.p), b.pitch * esz, kw * esz, m, cudaMemcpyDefault));
   }
   return TF_OK;
 }

@@ -137,6 +137,9 @@ extern "C" tf_status tf_ag_gemm_host_async(tf_world* tw, tf_ag_variant variant, 
     return set_error(TF_ERR_CONFIG, "ag_gemm: k = " + std::to_string(sh.k) +
                                         " must be divisible by world_size = " + std::to_string(w->W));
   if (sh.dtype != TF_F32 && sh.dtype != TF_BF16) return set_error(TF_ERR_CONFIG, "ag_gemm: unknown dtype");
+  if (sh.shard != TF_SHARD_K)
+    return set_error(TF_ERR_CONFIG, "tf_ag_gemm_host: M-sharded A is supported by the device-resident entry points "
+                                    "(tf_ag_gemm[_async]) only");
   if (sh.bm == 0) sh.bm = 16;
   if (sh.bn == 0) sh.bn = 16;
   if (sh.bk == 0) sh.bk = 16;

@@ -102,6 +102,10 @@ struct AgTcParams {
   int ldc;     // row pitch of C (elements)
   int b4;      // whole tiles load B with ONE 4-D box per stage (tmB4) instead of NH * CPH 2-D boxes
   uint8_t* ws;  // split-K exchange through L2: [grid CTAs][NH][128 rows x 1 KB]; nullptr: through DSMEM
+  // M-sharded A (TF_SHARD_M): rank s owns m-blocks [s*mpr, (s+1)*mpr) (all
+  // of K); k runs ascending and the tile rows rotate by mt_rot so a rank's
+  // own rows come first (they never wait on the network).
+  int msharded, mpr, mt_rot;
   const __nv_bfloat16* peer_shard[64];
 };
 
@@ -267,9 +271,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // [ks*kb/S, (ks+1)*kb/S) of the rank's rotated k order (never empty:
   // the host keeps kb_total >= 4 * ksplit).
   const int num_tiles = p.total_items;
+  auto tcoords = [&](int t, int& mt, int& nb) {
+    tile_coords(num_mt, p.num_n, t, mt, nb);
+    if (p.mt_rot) mt = (mt + p.mt_rot) % num_mt;
+  };
   auto item_coords = [&](int t, int& mt, int& nb, int& i0, int& i1) {
     const int ks = t % p.ksplit;
-    tile_coords(num_mt, p.num_n, t / p.ksplit, mt, nb);
+    tcoords(t / p.ksplit, mt, nb);
     i0 = ks * p.kb_total / p.ksplit;
     i1 = (ks + 1) * p.kb_total / p.ksplit;
   };
@@ -285,7 +293,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       w = K_::BN_TILE;
     } else {
       const int j = t - p.full_items;
-      tile_coords(num_mt, p.num_n, p.full_items + j / p.q_tail, mt, nb);
+      tcoords(p.full_items + j / p.q_tail, mt, nb);
       w = K_::BN_TILE / p.q_tail;
       col0 = nb * K_::BN_TILE + (j % p.q_tail) * w;
       i0 = 0;
@@ -334,8 +342,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t tx = uint32_t(CG) * uint32_t(A_BYTES + nhalf * cpc * BK * 128);
         uint64_t ready_mask = 0;
         for (int i = i0; i < i1; ++i) {
-          const int kb = p.own >= 0 ? (i + p.own * p.kbw) % p.kb_total : i;
-          const int src = kb / p.kbw;
+          const int kb = p.msharded ? i : p.own >= 0 ? (i + p.own * p.kbw) % p.kb_total : i;
+          // Owner of this k-block of this m-block: by column band (K-sharded)
+          // or row band (M-sharded; rows past M read the zero-filled edge).
+          const int src = !p.msharded ? kb / p.kbw : mb < p.num_m ? mb / p.mpr : -1;
           mbar_wait(&empty[stage], phase ^ 1);
           const bool from_own = src == p.own;
           if (!from_own && p.ready && mb < p.num_m && !((ready_mask >> src) & 1ull)) {
@@ -350,7 +360,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (leader) mbar_arrive_expect_tx(&full[stage], tx);
           else mbar_arrive_cluster(bar);
           uint8_t* a_dst = smA + stage * A_BYTES;
-          if (from_own) tma_load<CG>(a_dst, &tmA_own, bar, kb * BK - p.own * p.kw, m0);
+          if (from_own && p.msharded) tma_load<CG>(a_dst, &tmA_own, bar, kb * BK, m0 - p.own * p.mpr * BM);
+          else if (from_own) tma_load<CG>(a_dst, &tmA_own, bar, kb * BK - p.own * p.kw, m0);
           else tma_load<CG>(a_dst, &tmA_inbox, bar, kb * BK, m0);
           uint8_t* b_dst = smB + stage * K_::B_BYTES;
           if (wcol == K_::BN_TILE && p.b4) {
@@ -567,18 +578,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // wasted m x kw read + write per call.  A caller-supplied gathered
     // buffer (placement check) gets the own shard too, last.
     const int nsrc = p.W - 1 + p.gather_own;
-    const unsigned total = unsigned(p.num_m) * unsigned(nsrc);
-    const int vec_per_row = p.kw / 8;  // 16-byte vectors per shard row
+    // M-sharded: one chunk per m-block this rank does not own (plus its own,
+    // last, into a caller's buffer), starting after its own rows -- the
+    // order its rotated tile rows consume them.  Rows are contiguous in the
+    // owner's shard and in the inbox, so a chunk is one flat copy.
+    const unsigned total = p.msharded ? unsigned(p.num_m - (p.gather_own ? 0 : p.mpr))
+                                      : unsigned(p.num_m) * unsigned(nsrc);
+    const int vec_per_row = (p.msharded ? p.K : p.kw) / 8;  // 16-byte vectors per copied row
     for (;;) {
       if (gt == 0) s_chunk = atomicAdd(&p.ctr[0], 1u);
       named_bar(1, GATHER_T);
       const unsigned c = s_chunk;
       named_bar(1, GATHER_T);
       if (c >= total) break;
-      const int mb = int(c / nsrc);
-      const int src = (p.own + 1 + int(c % nsrc)) % p.W;
+      const int mb = p.msharded ? int((unsigned(p.own + 1) * p.mpr + c) % unsigned(p.num_m)) : int(c / nsrc);
+      const int src = p.msharded ? mb / p.mpr : (p.own + 1 + int(c % nsrc)) % p.W;
       const int r0 = mb * BM, rows = min(BM, p.M - r0);
-      const uint4* s = reinterpret_cast<const uint4*>(p.peer_shard[src] + size_t(r0) * p.kw);
+      const uint4* s = reinterpret_cast<const uint4*>(
+          p.msharded ? p.peer_shard[src] + size_t(r0 - src * p.mpr * BM) * p.K : p.peer_shard[src] + size_t(r0) * p.kw);
       const int nvec = rows * vec_per_row;
       constexpr int U = 8;
       for (int base = 0; base < nvec; base += GATHER_T * U) {
@@ -593,7 +610,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int e = base + u * GATHER_T + gt;
           if (e < nvec) {
             const int rr = e / vec_per_row, cv = e % vec_per_row;
-            *reinterpret_cast<uint4*>(p.inbox + size_t(r0 + rr) * p.K + size_t(src) * p.kw + 8 * cv) = v[u];
+            *reinterpret_cast<uint4*>(p.inbox + size_t(r0 + rr) * p.K + (p.msharded ? 0 : size_t(src) * p.kw) + 8 * cv) =
+                v[u];
           }
         }
       }
@@ -762,13 +780,14 @@ struct PushParams {
   uint64_t* ready[64];
   unsigned long long* events[64];  // every rank's event log (or null)
   int M, K, kw, W, self, num_m;
+  int msharded, mpr;  // M-sharded A: push this rank's own row band
   unsigned int* ctr;  // [0] chunk counter, [1] done
 };
 
 __global__ void __launch_bounds__(512) ag_push_kernel(const PushParams p) {
   __shared__ unsigned int s_chunk;
-  const unsigned total = unsigned(p.num_m) * p.W;
-  const int vec_per_row = p.kw / 8;
+  const unsigned total = p.msharded ? unsigned(p.mpr) * p.W : unsigned(p.num_m) * p.W;
+  const int vec_per_row = (p.msharded ? p.K : p.kw) / 8;
   for (;;) {
     if (threadIdx.x == 0) s_chunk = atomicAdd(&p.ctr[0], 1u);
     __syncthreads();
@@ -777,10 +796,11 @@ __global__ void __launch_bounds__(512) ag_push_kernel(const PushParams p) {
     if (c >= total) break;
     // m-block major so every consumer's first tiles are fed first; peers
     // before self (the consumer reads its own shard directly).
-    const int mb = int(c / p.W);
+    const int mb = p.msharded ? p.self * p.mpr + int(c / p.W) : int(c / p.W);
     const int dst = (p.self + 1 + int(c % p.W)) % p.W;
     const int r0 = mb * BM, rows = min(BM, p.M - r0);
-    const uint4* s = reinterpret_cast<const uint4*>(p.shard + size_t(r0) * p.kw);
+    const uint4* s = reinterpret_cast<const uint4*>(p.msharded ? p.shard + size_t(r0 - p.self * p.mpr * BM) * p.K
+                                                               : p.shard + size_t(r0) * p.kw);
     __nv_bfloat16* ib = p.inbox[dst];
     const int nvec = rows * vec_per_row;
     constexpr int U = 8;  // 64 KB of loads in flight per CTA feeding peer stores
@@ -796,7 +816,8 @@ __global__ void __launch_bounds__(512) ag_push_kernel(const PushParams p) {
         const int e = base + u * 512 + threadIdx.x;
         if (e < nvec) {
           const int rr = e / vec_per_row, cv = e % vec_per_row;
-          *reinterpret_cast<uint4*>(ib + size_t(r0 + rr) * p.K + size_t(p.self) * p.kw + 8 * cv) = v[u];
+          *reinterpret_cast<uint4*>(ib + size_t(r0 + rr) * p.K + (p.msharded ? 0 : size_t(p.self) * p.kw) + 8 * cv) =
+              v[u];
         }
       }
     }
@@ -881,7 +902,8 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   CUtensorMap mOwn{}, mInbox{}, mB{}, mC{};
   // C: 64-column x 32-row boxes, one per epilogue warp per store.
   TFB_CHECK(make_map(&mC, c, sh.n, sh.m, ldc, 64, 32));
-  if (shard) TFB_CHECK(make_map(&mOwn, shard, kw, sh.m, kw, BK, BM));
+  if (shard && proto.msharded) TFB_CHECK(make_map(&mOwn, shard, sh.k, sh.m / W, sh.k, BK, BM));
+  else if (shard) TFB_CHECK(make_map(&mOwn, shard, kw, sh.m, kw, BK, BM));
   if (inbox) TFB_CHECK(make_map(&mInbox, inbox, sh.k, sh.m, sh.k, BK, BM));
   if (!shard) mOwn = mInbox;
   if (!inbox) mInbox = mOwn;
@@ -990,6 +1012,7 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   }
   const int CG = shp->CG;
   p.num_n = num_n;
+  p.mt_rot = (p.msharded && own >= 0) ? (own * p.mpr / CG) % ((p.num_m + CG - 1) / CG) : 0;
   p.num_tiles = tiles;
   p.ksplit = ks;
   p.full_items = tiles * ks;
@@ -1089,16 +1112,20 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
                       const std::vector<cudaStream_t>& streams, const AgLayout& lay) {
   const int W = w->W;
   const size_t m = sh.m, n = sh.n, k = sh.k, kw = k / W;
-  if (kw % BK != 0)
-    return set_error(TF_ERR_SHAPE, "ag_gemm(bf16): k / world_size = " + std::to_string(kw) +
-                                       " must be a multiple of 64");
+  const bool msh = sh.shard == TF_SHARD_M && W > 1;  // W = 1: both layouts are the whole A
+  const size_t mr = m / size_t(W);                    // M-sharded: rows per rank
+  if (msh ? k % BK != 0 : kw % BK != 0)
+    return set_error(TF_ERR_SHAPE, msh ? "ag_gemm(bf16, M-sharded): k = " + std::to_string(k) +
+                                             " must be a multiple of 64"
+                                       : "ag_gemm(bf16): k / world_size = " + std::to_string(kw) +
+                                             " must be a multiple of 64");
   if (n % 8 != 0) return set_error(TF_ERR_SHAPE, "ag_gemm(bf16): n must be a multiple of 8");
   if (m > (size_t(1) << 31) || n > (size_t(1) << 31) || k > (size_t(1) << 31))
     return set_error(TF_ERR_SHAPE, "ag_gemm(bf16): dimensions must fit in int32");
   const int num_m = int((m + BM - 1) / BM);
   const unsigned sms = unsigned(w->sm_count);
 
-  if (!lay.inbox_complete) w->record_ag(m, kw, 2);
+  if (!lay.inbox_complete) w->record_ag(m, kw, 2, msh);
   if (W == 1) {
     // No exchange: the fused kernel degenerates to the GEMM over the shard.
     if (!w->ranks[0].local) return TF_OK;
@@ -1137,8 +1164,8 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
     for (int r = 0; r < W; ++r)
       for (int s = 0; s < W; ++s)
         w->ag_src[r][s] = (variant == TF_AG_PULL && s == r && !(gathered && gathered[r]))
-                              ? World::AgBlock{a_shard[r], kw}  // read in place by the TMA producer
-                              : World::AgBlock{inbox_of(r) + size_t(s) * kw, k};
+                              ? World::AgBlock{a_shard[r], msh ? k : kw}  // read in place by the TMA producer
+                              : World::AgBlock{inbox_of(r) + (msh ? size_t(s) * mr * k : size_t(s) * kw), k};
   auto ready_of = [&](int r) { return reinterpret_cast<uint64_t*>(w->ptr(r, rb.offset)); };
   auto ctr_of = [&](int r, int slot) { return reinterpret_cast<unsigned int*>(w->ptr(r, ctr_off)) + slot * 4; };
   // Event log (tf_world_set_events; debug, untimed): per (m-block, source)
@@ -1187,9 +1214,14 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
     for (int r = 0; r < W; ++r) {
       if (!w->ranks[r].local) continue;
       cudaSetDevice(w->ranks[r].device);
-      for (int s = 0; s < W; ++s)
-        TFB_CUDA(cudaMemcpy2DAsync(inbox_of(r) + size_t(s) * kw, k * 2, a_shard[s], kw * 2, kw * 2, m,
-                                   cudaMemcpyDefault, streams[r]));
+      for (int s = 0; s < W; ++s) {
+        if (msh)  // row band s: one contiguous copy
+          TFB_CUDA(cudaMemcpyAsync(inbox_of(r) + size_t(s) * mr * k, a_shard[s], mr * k * 2, cudaMemcpyDefault,
+                                   streams[r]));
+        else
+          TFB_CUDA(cudaMemcpy2DAsync(inbox_of(r) + size_t(s) * kw, k * 2, a_shard[s], kw * 2, kw * 2, m,
+                                     cudaMemcpyDefault, streams[r]));
+      }
     }
     TFB_CHECK(world_barrier(w, streams));
     for (int r = 0; r < W; ++r) {
@@ -1209,6 +1241,8 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
       for (int s = 0; s < W; ++s) proto.peer_shard[s] = static_cast<const __nv_bfloat16*>(a_shard[s]);
       proto.inbox = inbox_of(r);
       proto.gather_own = (gathered && gathered[r]) ? 1 : 0;
+      proto.msharded = msh;
+      proto.mpr = int(mr / BM);
       proto.ready_w = ready_of(r);
       proto.ctr = ctr_of(r, 0);
       proto.events = events_of(r);
@@ -1255,6 +1289,8 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
     pp.W = W;
     pp.self = r;
     pp.num_m = num_m;
+    pp.msharded = msh;
+    pp.mpr = int(mr / BM);
     pp.ctr = ctr_of(r, 1);
     for (int d = 0; d < W; ++d) pp.events[d] = events_of(d);
     ag_push_kernel<<<push_ctas_of(r), 512, 0, w->ranks[r].side>>>(pp);
@@ -1265,6 +1301,8 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
     if (!w->ranks[r].local) continue;
     AgTcParams proto{};
     proto.events = events_of(r);
+    proto.msharded = msh;
+    proto.mpr = int(mr / BM);
     TFB_CHECK(launch_skew(w, r, streams[r]));
     TFB_CHECK(launch_gemm(w, r, sh, a_shard[r], inbox_of(r), b[r], c[r], ready_of(r), rb.epoch, r, 0,
                           proto, streams[r], rb.id, push_cap(sms, push_ctas_of(r), per_dev[w->ranks[r].device]), lay));

@@ -102,10 +102,12 @@ struct World {
   };
   std::vector<std::vector<AgBlock>> ag_src;
   size_t ag_m = 0, ag_kw = 0, ag_esz = 0;
-  void record_ag(size_t m, size_t kw, size_t esz) {
+  bool ag_msharded = false;  // blocks are row bands (TF_SHARD_M), else column bands
+  void record_ag(size_t m, size_t kw, size_t esz, bool msharded = false) {
     ag_m = m;
     ag_kw = kw;
     ag_esz = esz;
+    ag_msharded = msharded;
     ag_src.assign(W, std::vector<AgBlock>(W));
   }
   // Event log (tf_world_set_events): the last pull/push run's per-chunk

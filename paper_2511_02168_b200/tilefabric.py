@@ -234,22 +234,30 @@ class ag:  # namespace tilefabric::ag
                                 v[m * k:].reshape(k, n).copy())
 
     @staticmethod
-    def _run(variant: int, p: "ag.AgGemmProblem", cfg: WorldConfig, dtype: int = _abi.TF_F32):
+    def _run(variant: int, p: "ag.AgGemmProblem", cfg: WorldConfig, dtype: int = _abi.TF_F32,
+             shard_m: bool = False):
+        """shard_m: A sharded by rows (TF_SHARD_M, an extension: the sharding
+        the paper lists and the reference leaves out) instead of
+        by columns (fill_shard, ag_gemm.hpp:103-112)."""
         cfg.validate()
         p.validate(cfg.world_size)
         torch = _torch()
         W = cfg.world_size
         kw = p.k // W
+        mr = p.m // W
         esz = 4 if dtype == _abi.TF_F32 else 2
         tdt = torch.float32 if dtype == _abi.TF_F32 else torch.bfloat16
         heap = esz * p.m * kw + 2 * esz * p.m * p.k + (8 << 20)
         with World.from_config(cfg, heap) as w:
-            shards = w.alloc("ag.a", esz * p.m * kw)
+            shards = w.alloc("ag.a", esz * (mr * p.k if shard_m else p.m * kw))
             A = torch.from_numpy(np.ascontiguousarray(p.a, np.float32))
             bufs_b, bufs_c = [], []
             for r in range(W):
                 dev = torch.device("cuda", w.devices[r])
-                shard = A[:, r * kw:(r + 1) * kw].contiguous().to(tdt)  # fill_shard :103-112
+                if shard_m:
+                    shard = A[r * mr:(r + 1) * mr, :].contiguous().to(tdt)
+                else:
+                    shard = A[:, r * kw:(r + 1) * kw].contiguous().to(tdt)  # fill_shard :103-112
                 shard_d = shard.to(dev)
                 w.memcpy(shards[r], shard_d.data_ptr(), shard_d.numel() * esz)
                 bufs_b.append(torch.from_numpy(np.ascontiguousarray(p.b, np.float32)).to(tdt).to(dev))
@@ -257,7 +265,8 @@ class ag:  # namespace tilefabric::ag
             torch.cuda.synchronize()
             w.barrier()  # setup_fence (ag_gemm.hpp:189-191): every shard placed before any rank reads it
             w.tax_reset()  # untimed, like the reference's: the tax meter starts after it
-            shape = _abi.AgShape(p.m, p.n, p.k, p.tiles.bm, p.tiles.bn, p.tiles.bk, dtype)
+            shape = _abi.AgShape(p.m, p.n, p.k, p.tiles.bm, p.tiles.bn, p.tiles.bk, dtype,
+                                 _abi.TF_SHARD_M if shard_m else _abi.TF_SHARD_K)
             before = w.launches()
             _abi.check(w.lib.tf_ag_gemm(
                 w.handle, variant, C.byref(shape), _abi.ptr_array(shards),
@@ -284,19 +293,19 @@ class ag:  # namespace tilefabric::ag
             return ag.AgGemmRun(cs, flags, gath, launches, taxes)
 
     @staticmethod
-    def run_baseline(p, cfg, dtype=_abi.TF_F32):
+    def run_baseline(p, cfg, dtype=_abi.TF_F32, shard_m=False):
         """ag_gemm.hpp:134-180"""
-        return ag._run(_abi.TF_AG_BASELINE, p, cfg, dtype)
+        return ag._run(_abi.TF_AG_BASELINE, p, cfg, dtype, shard_m)
 
     @staticmethod
-    def run_pull(p, cfg, dtype=_abi.TF_F32):
+    def run_pull(p, cfg, dtype=_abi.TF_F32, shard_m=False):
         """ag_gemm.hpp:185-222"""
-        return ag._run(_abi.TF_AG_PULL, p, cfg, dtype)
+        return ag._run(_abi.TF_AG_PULL, p, cfg, dtype, shard_m)
 
     @staticmethod
-    def run_push(p, cfg, dtype=_abi.TF_F32):
+    def run_push(p, cfg, dtype=_abi.TF_F32, shard_m=False):
         """ag_gemm.hpp:228-305"""
-        return ag._run(_abi.TF_AG_PUSH, p, cfg, dtype)
+        return ag._run(_abi.TF_AG_PUSH, p, cfg, dtype, shard_m)
 
 
 # ---- flash_decode.hpp -------------------------------------------------------------

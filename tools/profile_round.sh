@@ -8,7 +8,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   --log-file gpurun_out/${R}_launches_bench.csv python bench.py --steps 2 --warmup 1 --no-cpu \
   > gpurun_out/${R}_bench_under_ncu.log 2>&1
 for x in ag fd3 fd4 agM128 agM256; do
-  k=ag_gemm_sm100; case $x in fd*) k=fd_attention;; esac
+  k=ag_gemm_sm100; case $x in fd*) k="fd_(attention|stream)";; esac
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
     -o gpurun_out/${R}_$x -f python tools/profile_kernels.py $x > gpurun_out/${R}_$x.log 2>&1
 done
