@@ -106,6 +106,7 @@ struct AgTcParams {
   // of K); k runs ascending and the tile rows rotate by mt_rot so a rank's
   // own rows come first (they never wait on the network).
   int msharded, mpr, mt_rot;
+  int l2hint;  // TMA L2 policies: 1 A evict_last, 2 B evict_first (TFB_L2HINT)
   const __nv_bfloat16* peer_shard[64];
 };
 
@@ -151,7 +152,22 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
 
 template <int CG>
 __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
-                                         int c1) {
+                                         int c1, uint64_t pol = 0) {
+  if (pol) {  // with an L2 cache policy (createpolicy)
+    if (CG == 2)
+      asm volatile(
+          "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+          "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+          "l"(map), "r"(c0), "r"(c1), "r"(bar_cluster), "l"(pol)
+          : "memory");
+    else
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+          "{%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+          "l"(map), "r"(c0), "r"(c1), "r"(bar_cluster), "l"(pol)
+          : "memory");
+    return;
+  }
   if (CG == 2)
     asm volatile(
         "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
@@ -173,7 +189,22 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint
 // boxes is what raises the L2->SM rate.
 template <int CG>
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c1,
-                                            int c2, int c3) {
+                                            int c2, int c3, uint64_t pol = 0) {
+  if (pol) {
+    if (CG == 2)
+      asm volatile(
+          "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+          "[%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
+          "l"(map), "r"(0), "r"(c1), "r"(c2), "r"(c3), "r"(bar_cluster), "l"(pol)
+          : "memory");
+    else
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+          "{%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
+          "l"(map), "r"(0), "r"(c1), "r"(c2), "r"(c3), "r"(bar_cluster), "l"(pol)
+          : "memory");
+    return;
+  }
   if (CG == 2)
     asm volatile(
         "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
@@ -330,6 +361,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      // L2 policies (p.l2hint): A rows are re-read by every tile column of
+      // their raster group, B panels only by the tiles running at the same
+      // time -- keep A, stream B.
+      uint64_t pol_a = 0, pol_b = 0;
+      if (p.l2hint & 1) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_a));
+      if (p.l2hint & 2) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_b));
       for (int t = cid; t < num_tiles; t += ncl) {
         int mt, n0, wcol, i0, i1;
         item_geom(t, mt, n0, wcol, i0, i1);
@@ -360,12 +397,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (leader) mbar_arrive_expect_tx(&full[stage], tx);
           else mbar_arrive_cluster(bar);
           uint8_t* a_dst = smA + stage * A_BYTES;
-          if (from_own && p.msharded) tma_load<CG>(a_dst, &tmA_own, bar, kb * BK, m0 - p.own * p.mpr * BM);
-          else if (from_own) tma_load<CG>(a_dst, &tmA_own, bar, kb * BK - p.own * p.kw, m0);
-          else tma_load<CG>(a_dst, &tmA_inbox, bar, kb * BK, m0);
+          if (from_own && p.msharded) tma_load<CG>(a_dst, &tmA_own, bar, kb * BK, m0 - p.own * p.mpr * BM, pol_a);
+          else if (from_own) tma_load<CG>(a_dst, &tmA_own, bar, kb * BK - p.own * p.kw, m0, pol_a);
+          else tma_load<CG>(a_dst, &tmA_inbox, bar, kb * BK, m0, pol_a);
           uint8_t* b_dst = smB + stage * K_::B_BYTES;
           if (wcol == K_::BN_TILE && p.b4) {
-            tma_load_4d<CG>(b_dst, &tmB4, bar, kb * BK, int(prank) * CPH, n0 / 256);
+            tma_load_4d<CG>(b_dst, &tmB4, bar, kb * BK, int(prank) * CPH, n0 / 256, pol_b);
           } else if (wcol == K_::BN_TILE) {
 #pragma unroll
             for (int h = 0; h < NH; ++h)
@@ -926,6 +963,7 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   p.err = w->err_of(r);
   p.board = board;
   if (const char* e = std::getenv("TFB_DEBUG")) p.dbg = std::atoi(e);
+  if (const char* e = std::getenv("TFB_L2HINT")) p.l2hint = std::atoi(e);
   const int dev = w->ranks[r].device;
   cudaSetDevice(dev);
   // Kernel shapes: CTA pairs (cta_group::2) with 256 x 512 tiles whenever
