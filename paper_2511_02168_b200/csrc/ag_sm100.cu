@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                          const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC,
                          const __grid_constant__ CUtensorMap tmB4, const AgTcParams p) {
+  pdl_begin();
   using K_ = Cfg<CG, NH_>;
   constexpr int STAGES = K_::STAGES, NH = K_::NH, CPH = K_::CPH;
   extern __shared__ uint8_t smem_raw[];
@@ -1103,13 +1104,13 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   cfg.blockDim = dim3(NUM_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG * p.ksplit;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 1 + unsigned(pdl_attrs(&attr[1]));
   {
     // TFB_GROUP_M (profiling knob) lives in a __constant__ per device.
     static std::atomic<int> last_gm[64];

@@ -159,6 +159,16 @@ static __device__ __noinline__ bool wait_geq(const uint64_t* cell, uint64_t expe
   return ok;
 }
 
+// Programmatic dependent launch (the hot kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a kernel lets the
+// next launch on its stream start being scheduled at once (the ~3 us
+// launch gap overlaps its tail) and waits for its own predecessor's memory
+// before touching any global data -- stream order is unchanged.
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);

@@ -1450,6 +1450,7 @@ __device__ __forceinline__ void fd_post_phases_body(const FdParams& P, unsigned 
 // kernels keep their register allocation).
 template <int MODE>
 __global__ void __launch_bounds__(kFastThreads, 2) fd_attention_kernel(const __grid_constant__ FdParams P) {
+  pdl_begin();
   __shared__ unsigned int s_item;
   __shared__ int s_last, s_src;
   __shared__ FastSmem fsm;
@@ -1913,6 +1914,7 @@ __device__ void stream_consumer(const FdParams& P, StreamSmem& sm) {
 template <bool HILO>
 __global__ void __launch_bounds__(kStreamThreads, 1)
     fd_stream_kernel(const __grid_constant__ FdParams P, const __grid_constant__ FdMaps M) {
+  pdl_begin();
   extern __shared__ uint8_t fd_smem_raw[];
   StreamSmem& sm = *reinterpret_cast<StreamSmem*>((reinterpret_cast<uintptr_t>(fd_smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ unsigned int s_item;
@@ -2525,8 +2527,16 @@ static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape
             attr[hilo][kv.first & 63].store(true);
           }
           const unsigned grid = std::max(1u, std::min(Q.nitems, unsigned(w->sm_count)));
-          if (hilo) fd_stream_kernel<true><<<grid, kStreamThreads, smem, st[lead]>>>(Q, maps);
-          else fd_stream_kernel<false><<<grid, kStreamThreads, smem, st[lead]>>>(Q, maps);
+          cudaLaunchConfig_t lc{};
+          cudaLaunchAttribute la[1];
+          lc.gridDim = dim3(grid);
+          lc.blockDim = dim3(kStreamThreads);
+          lc.dynamicSmemBytes = smem;
+          lc.stream = st[lead];
+          lc.attrs = la;
+          lc.numAttrs = unsigned(pdl_attrs(la));
+          if (hilo) TFB_CUDA(cudaLaunchKernelEx(&lc, fd_stream_kernel<true>, Q, maps));
+          else TFB_CUDA(cudaLaunchKernelEx(&lc, fd_stream_kernel<false>, Q, maps));
           TFB_CUDA(cudaGetLastError());
           ++w->launches;
           for (int i = 1; i < Q.nlocal; ++i) {
@@ -2551,11 +2561,18 @@ static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kFastThreads, 0);
         const unsigned grid =
             std::max(1u, std::min(items, unsigned(std::max(per_sm, 1) * w->sm_count)));
-        if (mode == 0) fd_attention_kernel<0><<<grid, kFastThreads, 0, st[lead]>>>(Q);
-        else if (mode == 1) fd_attention_kernel<1><<<grid, kFastThreads, 0, st[lead]>>>(Q);
-        else if (mode == 2) fd_attention_kernel<2><<<grid, kFastThreads, 0, st[lead]>>>(Q);
-        else if (mode == 3) fd_attention_kernel<3><<<grid, kFastThreads, 0, st[lead]>>>(Q);
-        else fd_attention_kernel<4><<<grid, kFastThreads, 0, st[lead]>>>(Q);
+        cudaLaunchConfig_t lc{};
+        cudaLaunchAttribute la[1];
+        lc.gridDim = dim3(grid);
+        lc.blockDim = dim3(kFastThreads);
+        lc.stream = st[lead];
+        lc.attrs = la;
+        lc.numAttrs = unsigned(pdl_attrs(la));
+        if (mode == 0) TFB_CUDA(cudaLaunchKernelEx(&lc, fd_attention_kernel<0>, Q));
+        else if (mode == 1) TFB_CUDA(cudaLaunchKernelEx(&lc, fd_attention_kernel<1>, Q));
+        else if (mode == 2) TFB_CUDA(cudaLaunchKernelEx(&lc, fd_attention_kernel<2>, Q));
+        else if (mode == 3) TFB_CUDA(cudaLaunchKernelEx(&lc, fd_attention_kernel<3>, Q));
+        else TFB_CUDA(cudaLaunchKernelEx(&lc, fd_attention_kernel<4>, Q));
         TFB_CUDA(cudaGetLastError());
         ++w->launches;
         // Ranks sharing the launch are complete when it is: order their streams.

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <vector>
@@ -179,6 +180,15 @@ tf_status order_after_legacy(World* w, void* const* streams);
 // their launches, so a captured graph would replay stale waits: refuse
 // (TF_ERR_CONFIG) when W > 1 and any rank's stream is capturing.
 tf_status refuse_multi_rank_capture(World* w, const std::vector<cudaStream_t>& s, const char* what);
+// Launch attributes for the hot kernels: programmatic dependent launch
+// unless TFB_NO_PDL is set (A/B).  Returns the number of attributes filled.
+inline int pdl_attrs(cudaLaunchAttribute* a) {
+  if (std::getenv("TFB_NO_PDL")) return 0;
+  a->id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a->val.programmaticStreamSerializationAllowed = 1;
+  return 1;
+}
+
 // Grow-only device scratch of rank r (slot < 3); first use allocates.
 tf_status ensure_scratch(World* w, int r, int slot, size_t bytes, void** out);
 // Wait for local streams and turn the device error record into a status.
