@@ -94,7 +94,7 @@ struct AgTcParams {
   DevErr* err;
   int board;
   int dbg;  // TFB_DEBUG knobs: 1 skip C stores, 2 skip MMAs, 8 force CG=1, 16 skip the split-K reduce,
-           // 32 poll-wait the epilogue, 64 skip the epilogue (profiling aids)
+           // 32 poll-wait the epilogue, 64 skip the epilogue, 4096 print CTA 0's phase stamps (profiling aids)
   int ksplit;  // > 1: skinny-M split-K across a cluster of ksplit CTAs (pairs), reduced through DSMEM
   int full_items;   // items [0, full_items) are whole tiles (x k-splits)
   int q_tail;       // > 1: the tiles after them run as q_tail column slices each (last-wave balance)
@@ -356,6 +356,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Profiling (TFB_DEBUG & 4096): %globaltimer phase stamps of CTA 0, printed at exit.
+  __shared__ unsigned long long s_ts[12];
+  const bool tsd = (p.dbg & 4096) && blockIdx.x == 0;
+  if (tsd && threadIdx.x == 0)
+    for (int i = 0; i < 12; ++i) s_ts[i] = i == 0 ? globaltimer_ns() : 0;
 
   if (warp == 0) {
     // ===== TMA producer (both CTAs of a pair) =====
@@ -507,11 +512,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         for (; i < i1; ++i) {
           mbar_wait(&full[stage], phase);
+          if (tsd && !s_ts[1]) s_ts[1] = globaltimer_ns();
           tc_fence_after();
           mma_kblock(stage, 0, NH, i == i0, whole, nhalf, idesc);
           mma_commit_all<CG>(&empty[stage], pair_mask);
           advance(stage, phase);
         }
+        if (tsd) s_ts[2] = globaltimer_ns();
         mma_commit_all<CG>(&tfull[acc], pair_mask);
         if (++acc == K_::ACC_BUFS) {
           acc = 0;
@@ -607,6 +614,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
     if (lane == 0) bulk_wait_all();  // C stores complete before the CTA retires
+    if (tsd && warp == 2 && lane == 0) s_ts[7] = globaltimer_ns();
   } else if (p.gather) {
     // ===== gather (PULL): peer shard chunks -> local inbox + ready flags =====
     const int gt = threadIdx.x - 6 * 32;  // 0..GATHER_T-1
@@ -683,6 +691,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (warp >= 2 && warp < 6) {
       mbar_wait(&tfull[0], 0);
       tc_fence_after();
+      if (tsd && warp == 2 && lane == 0) s_ts[3] = globaltimer_ns();
     }
 #pragma unroll 1
     for (int h = 0; h < NH; ++h) {
@@ -745,6 +754,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       } else {
         cluster_sync();
       }
+      if (tsd && threadIdx.x == 0 && h == 0) s_ts[4] = globaltimer_ns();  // partials exchanged
       uint32_t src[8];
 #pragma unroll
       for (int s2 = 0; s2 < 8; ++s2)
@@ -787,6 +797,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           *reinterpret_cast<uint4*>(p.C + size_t(grow) * p.ldc + gcol) = o;
         }
       }
+      if (tsd && threadIdx.x == 0) s_ts[5 + h] = globaltimer_ns();  // half h summed + stored
       if (p.ws) named_bar(2, NUM_THREADS);  // R fully read before the next half's dump
       else cluster_sync();  // siblings done reading R before it is rewritten / released
     }
@@ -795,6 +806,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_before();
   if (CG == 2 || p.ksplit > 1) cluster_sync();
   else __syncthreads();
+  if (tsd && threadIdx.x == 0) {
+    auto rel = [&](int i) { return s_ts[i] ? (long long)(s_ts[i] - s_ts[0]) : -1ll; };
+    printf("[ag cta0 CG=%d NH=%d S=%d] first-stage %lld last-commit %lld tfull %lld exchanged %lld "
+           "sum0 %lld sum1 %lld epilogue %lld exit %lld ns\n", CG, NH, p.ksplit, rel(1), rel(2), rel(3), rel(4),
+           rel(5), rel(6), rel(7), (long long)(globaltimer_ns() - s_ts[0]));
+  }
   if (warp == 1) {
     __syncwarp();
     tmem_dealloc_cg<CG>(tmem_base);
@@ -1078,7 +1095,7 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   // measured 35.7 vs 37.7 us at M = 128 (tools/ab_gemm.py, TFB_SPLITK_DSMEM
   // A/B); two-half tiles pay the copy-then-barrier latency chain twice and
   // lose ~2 us at M = 512, so they keep the DSMEM path.
-  if (p.ksplit > 1 && shp->NH == 1 && !std::getenv("TFB_SPLITK_DSMEM")) {
+  if (p.ksplit > 1 && (shp->NH == 1 || std::getenv("TFB_SPLITK_L2")) && !std::getenv("TFB_SPLITK_DSMEM")) {
     void* ws = nullptr;
     TFB_CHECK(ensure_scratch(w, r, 2, size_t(grid) * shp->NH * BM * 1024, &ws));
     p.ws = static_cast<uint8_t*>(ws);

@@ -9,7 +9,7 @@ import sys
 
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("TFB_PKG_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2511_02168_b200 as tf  # noqa: E402
 from paper_2511_02168_b200 import _abi  # noqa: E402
 
