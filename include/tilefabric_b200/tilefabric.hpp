@@ -171,12 +171,18 @@ enum class Dtype { kF32 = TF_F32, kBF16 = TF_BF16 };
 // ============================ ag_gemm.hpp =====================================
 namespace ag {
 
+// How A is sharded before the all-gather: by columns (the reference,
+// fill_shard, ag_gemm.hpp:103-112) or by rows (extension, TF_SHARD_M: the
+// sharding SPEC.md:265 leaves out; bf16, m a multiple of 128 * world_size).
+enum class Shard { kK = TF_SHARD_K, kM = TF_SHARD_M };
+
 struct AgGemmProblem {  // ag_gemm.hpp:47-66
   std::size_t m = 0, n = 0, k = 0;
   TileSpec tiles;
   std::vector<float> a;  // m x k
   std::vector<float> b;  // k x n
   Dtype dtype = Dtype::kF32;
+  Shard shard = Shard::kK;
   void validate(int world_size) const {
     if (m < 1 || n < 1 || k < 1) throw ConfigError("ag_gemm: m, n, k must be >= 1");
     if (k % std::size_t(world_size) != 0)
@@ -215,12 +221,14 @@ inline AgGemmRun run(tf_ag_variant variant, const AgGemmProblem& p, const WorldC
   const int W = cfg.world_size;
   const std::size_t kw = p.k / std::size_t(W);
   const bool bf = p.dtype == Dtype::kBF16;
+  const bool msh = p.shard == Shard::kM;
+  const std::size_t mr = p.m / std::size_t(W);
   const std::size_t esz = bf ? 2 : 4;
   const std::size_t heap = cfg.heap_bytes ? cfg.heap_bytes
                                           : esz * (p.m * kw + 5 * p.m * p.k) + (16u << 20);
   b200::World w(W, cfg.device_list(), heap, cfg.watchdog_secs);
   w.apply(cfg);
-  auto shards = w.heap("ag.a", esz * p.m * kw);
+  auto shards = w.heap("ag.a", esz * (msh ? mr * p.k : p.m * kw));
   std::vector<void*> B(W), C(W);
   auto pack = [&](const float* src, std::size_t n) {
     std::vector<uint8_t> out(n * esz);
@@ -232,10 +240,17 @@ inline AgGemmRun run(tf_ag_variant variant, const AgGemmProblem& p, const WorldC
   };
   const auto hb = pack(p.b.data(), p.b.size());
   for (int r = 0; r < W; ++r) {
-    // fill_shard (ag_gemm.hpp:103-112): columns [r*kw, (r+1)*kw) of A.
-    std::vector<float> shard(p.m * kw);
-    for (std::size_t i = 0; i < p.m; ++i)
-      std::memcpy(&shard[i * kw], &p.a[i * p.k + std::size_t(r) * kw], kw * 4);
+    // fill_shard (ag_gemm.hpp:103-112): columns [r*kw, (r+1)*kw) of A, or
+    // (Shard::kM) rows [r*m/W, (r+1)*m/W).
+    std::vector<float> shard;
+    if (msh) {
+      shard.assign(p.a.begin() + std::ptrdiff_t(std::size_t(r) * mr * p.k),
+                   p.a.begin() + std::ptrdiff_t(std::size_t(r + 1) * mr * p.k));
+    } else {
+      shard.resize(p.m * kw);
+      for (std::size_t i = 0; i < p.m; ++i)
+        std::memcpy(&shard[i * kw], &p.a[i * p.k + std::size_t(r) * kw], kw * 4);
+    }
     const auto hs = pack(shard.data(), shard.size());
     w.put(shards[r], hs.data(), hs.size());
     B[r] = w.device(r, hb.size());
@@ -247,7 +262,8 @@ inline AgGemmRun run(tf_ag_variant variant, const AgGemmProblem& p, const WorldC
   // tax meter starts after it.
   b200::check(tf_world_barrier(w.w, -1));
   b200::check(tf_tax_reset(w.w));
-  tf_ag_shape sh{p.m, p.n, p.k, p.tiles.bm, p.tiles.bn, p.tiles.bk, bf ? TF_BF16 : TF_F32};
+  tf_ag_shape sh{p.m, p.n, p.k, p.tiles.bm, p.tiles.bn, p.tiles.bk, bf ? TF_BF16 : TF_F32,
+                 static_cast<tf_ag_shard>(p.shard)};
   const std::uint64_t l0 = tf_launch_count(w.w);
   b200::check(tf_ag_gemm(w.w, variant, &sh, shards.data(), const_cast<const void* const*>(B.data()),
                          C.data(), nullptr, nullptr));
@@ -359,6 +375,10 @@ inline DecodeProblem make_problem(std::uint64_t seed, int heads, int head_dim, s
 struct FdOptions {  // :108-114
   bool fold_by_arrival = false;  // fused only: fold in arrival order (not bitwise reproducible)
   bool owner_combine = false;    // extension: fused with per-group owners (TF_FD_FUSED_OWNER)
+  // Extension (SPEC.md:327 lists paged KV as a non-goal): > 0 runs the problem
+  // through tf_flash_decode_paged with pages of this many keys (a power of
+  // two), scattered in reverse order over each rank's pool (HND layout).
+  int page_size = 0;
 };
 
 struct FdRun {  // :116-123
@@ -401,7 +421,10 @@ inline FdRun run_fd(const DecodeProblem& p, Variant variant, const WorldConfig& 
       std::memcpy(out.data(), src, n * 4);
     return out;
   };
-  std::vector<void*> Q(W), K(W), V(W), O(W);
+  std::vector<void*> Q(W), K(W), V(W), O(W), T(W);
+  const int ps = opts.page_size;
+  const std::size_t pps = ps > 0 ? (ln + std::size_t(ps) - 1) / std::size_t(ps) : 0;
+  const std::size_t npages = std::size_t(B) * pps;
   const auto hq = pack(p.q.data(), p.q.size());
   for (int r = 0; r < W; ++r) {
     // slice_shard (flash_decode.hpp:140-160): positions [r*ln, (r+1)*ln) of every head.
@@ -409,6 +432,29 @@ inline FdRun run_fd(const DecodeProblem& p, Variant variant, const WorldConfig& 
     for (std::size_t bh = 0; bh < std::size_t(B) * Hkv; ++bh) {
       std::memcpy(&ks[bh * ln * d], &p.k[(bh * L + std::size_t(r) * ln) * d], ln * d * 4);
       std::memcpy(&vs[bh * ln * d], &p.v[(bh * L + std::size_t(r) * ln) * d], ln * d * 4);
+    }
+    if (ps > 0) {
+      // HND page pools [npages][Hkv][ps][d]; sequence b's page j lives in
+      // pool slot npages - 1 - (b * pps + j) (reverse order); unused tail
+      // keys of the last page are zero.
+      std::vector<float> pk(npages * Hkv * std::size_t(ps) * d, 0.f), pv(pk.size(), 0.f);
+      std::vector<int> tbl(npages);
+      for (int b = 0; b < B; ++b)
+        for (std::size_t j = 0; j < pps; ++j) {
+          const std::size_t slot = npages - 1 - (std::size_t(b) * pps + j);
+          tbl[std::size_t(b) * pps + j] = int(slot);
+          for (int h = 0; h < Hkv; ++h)
+            for (std::size_t x = j * ps; x < std::min(ln, (j + 1) * std::size_t(ps)); ++x) {
+              const std::size_t src = ((std::size_t(b) * Hkv + h) * ln + x) * d;
+              const std::size_t dst = ((slot * Hkv + h) * ps + (x - j * ps)) * d;
+              std::memcpy(&pk[dst], &ks[src], d * 4);
+              std::memcpy(&pv[dst], &vs[src], d * 4);
+            }
+        }
+      ks.swap(pk);
+      vs.swap(pv);
+      T[r] = w.device(r, tbl.size() * sizeof(int));
+      w.put(T[r], tbl.data(), tbl.size() * sizeof(int));
     }
     const auto hk = pack(ks.data(), ks.size()), hv = pack(vs.data(), vs.size());
     Q[r] = w.device(r, hq.size());
@@ -421,9 +467,18 @@ inline FdRun run_fd(const DecodeProblem& p, Variant variant, const WorldConfig& 
   }
   tf_fd_shape sh{B, H, Hkv, d, L, p.scale, bf ? TF_BF16 : TF_F32, bf ? TF_BF16 : TF_F32};
   const std::uint64_t l0 = tf_launch_count(w.w);
-  b200::check(tf_flash_decode(w.w, static_cast<tf_fd_variant>(variant), &sh,
-                              const_cast<const void* const*>(Q.data()), const_cast<const void* const*>(K.data()),
-                              const_cast<const void* const*>(V.data()), O.data(), inbox.data(), nullptr));
+  if (ps > 0) {
+    const tf_fd_paged pl{ps, int(pps), int(npages), TF_PAGED_HND};
+    b200::check(tf_flash_decode_paged(w.w, static_cast<tf_fd_variant>(variant), &sh, &pl,
+                                      const_cast<const void* const*>(Q.data()),
+                                      const_cast<const void* const*>(K.data()),
+                                      const_cast<const void* const*>(V.data()),
+                                      const_cast<const void* const*>(T.data()), O.data(), inbox.data(), nullptr));
+  } else {
+    b200::check(tf_flash_decode(w.w, static_cast<tf_fd_variant>(variant), &sh,
+                                const_cast<const void* const*>(Q.data()), const_cast<const void* const*>(K.data()),
+                                const_cast<const void* const*>(V.data()), O.data(), inbox.data(), nullptr));
+  }
   FdRun out;
   out.launches = tf_launch_count(w.w) - l0;
   out.taxes = w.taxes();

@@ -166,6 +166,37 @@ int main() {
             for (const auto& c : run.c) EXPECT_TRUE(bitwise(c, oracle));
           }
   });
+  // Extension (SPEC.md:265 leaves row sharding out): A sharded by rows gives the
+  // K-sharded baseline's C and gathered operand bit for bit (bf16 path).
+  run_test("Extension.AgRowShardedMatchesColumnShardedBaseline", [] {
+    auto p = ag::make_problem(21, 256, 64, 128);
+    p.dtype = Dtype::kBF16;
+    const auto base = ag::run_baseline(p, quick_config(2));
+    p.shard = ag::Shard::kM;
+    for (auto* fn : {&ag::run_pull, &ag::run_baseline}) {
+      const auto run = (*fn)(p, quick_config(2));
+      for (int r = 0; r < 2; ++r) {
+        EXPECT_TRUE(bitwise(run.c[r], base.c[r]));
+        EXPECT_TRUE(bitwise(run.gathered[r], base.gathered[r]));
+      }
+    }
+    auto q = ag::make_problem(21, 64, 64, 128);  // m not a multiple of 128 * W
+    q.dtype = Dtype::kBF16;
+    q.shard = ag::Shard::kM;
+    EXPECT_THROW(ag::run_pull(q, quick_config(2)), ShapeError);
+  });
+  // Extension (SPEC.md:327 lists paged KV as a non-goal): a paged run is the
+  // contiguous run of the same logical KV, bit for bit, every schedule.
+  run_test("Extension.FdPagedEqualsContiguous", [] {
+    const auto p = fd::make_problem(8, 2, 16, 200);
+    for (const int w : {1, 2})
+      for (auto v : {fd::Variant::kBsp, fd::Variant::kFineWaits, fd::Variant::kFused}) {
+        fd::FdOptions paged;
+        paged.page_size = 16;
+        const auto base = fd::run_fd(p, v, quick_config(w)), pg = fd::run_fd(p, v, quick_config(w), paged);
+        for (int r = 0; r < w; ++r) EXPECT_TRUE(bitwise(pg.out[r], base.out[r]));
+      }
+  });
   // flash_decode_test.cpp:45-56
   run_test("FdProblem.ValidatesShardabilityAndScale", [] {
     auto p = fd::make_problem(1, 2, 4, 64);
