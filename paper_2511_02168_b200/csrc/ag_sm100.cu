@@ -688,17 +688,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     item_coords(cid, mt, nb, i0_, i1_);
     float* R = reinterpret_cast<float*>(smem);  // [128][256] fp32, 16-byte chunks swizzled by row & 7
     const int row_base = (mt * CG + int(prank)) * BM;
-    if (warp >= 2 && warp < 6) {
+    // The dump runs on warps 2-9 (the gather warps are done by now): two
+    // warps per TMEM lane quarter, each 128 of the half's 256 columns.
+    if (warp >= 2 && warp < 10) {
       mbar_wait(&tfull[0], 0);
       tc_fence_after();
       if (tsd && warp == 2 && lane == 0) s_ts[3] = globaltimer_ns();
     }
 #pragma unroll 1
     for (int h = 0; h < NH; ++h) {
-      if (warp >= 2 && warp < 6) {
+      if (warp >= 2 && warp < 10) {
         const int row = 32 * (warp & 3) + lane;
+        const int cc0 = warp < 6 ? 0 : 4;
 #pragma unroll 1
-        for (int cc = 0; cc < 8; ++cc) {
+        for (int cc = cc0; cc < cc0 + 4; ++cc) {
           uint32_t r0[32];
           tmem_ld_32x32b_x32(tmem_base + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(h * 256 + 32 * cc), r0);
           tmem_ld_wait();
@@ -773,6 +776,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint8_t* b = reinterpret_cast<const uint8_t*>(R) + (s2 - ks) * rows_per * 1024;
             x[s2] = *reinterpret_cast<const float4*>(b + off0);
             y[s2] = *reinterpret_cast<const float4*>(b + off1);
+          } else if (s2 == ks) {  // this CTA's own copy: a local smem load
+            x[s2] = *reinterpret_cast<const float4*>(reinterpret_cast<const uint8_t*>(R) + off0);
+            y[s2] = *reinterpret_cast<const float4*>(reinterpret_cast<const uint8_t*>(R) + off1);
           } else if (s2 < S) {
             asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
                          : "=f"(x[s2].x), "=f"(x[s2].y), "=f"(x[s2].z), "=f"(x[s2].w) : "r"(src[s2] + off0));
