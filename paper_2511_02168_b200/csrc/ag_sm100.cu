@@ -68,7 +68,8 @@ struct Cfg {
   static constexpr int NH = NH_;                        // 256-column MMA halves per tile
   static constexpr int BN_TILE = 256 * NH;              // tile width
   static constexpr int ACC_BUFS = NH == 2 ? 1 : 2;      // accumulators in 512 TMEM columns
-  static constexpr int STAGES = 4;
+  // Narrow pair tiles (32 KB stages) fit six in flight: the skinny main loop is load-latency bound.
+  static constexpr int STAGES = (CG == 2 && NH_ == 1) ? 6 : 4;
   static constexpr int CPH = 4 / CG;                    // 64-column B chunks per half per CTA
   static constexpr int B_BYTES = NH * CPH * BK * 128;   // 32 KB
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES; // 48 KB
@@ -94,7 +95,8 @@ struct AgTcParams {
   DevErr* err;
   int board;
   int dbg;  // TFB_DEBUG knobs: 1 skip C stores, 2 skip MMAs, 8 force CG=1, 16 skip the split-K reduce,
-           // 32 poll-wait the epilogue, 64 skip the epilogue, 4096 print CTA 0's phase stamps (profiling aids)
+           // 32 poll-wait the epilogue, 64 skip the epilogue, 256 skip A loads, 512 skip B loads,
+           // 4096 print CTA 0's phase stamps (profiling aids)
   int ksplit;  // > 1: skinny-M split-K across a cluster of ksplit CTAs (pairs), reduced through DSMEM
   int full_items;   // items [0, full_items) are whole tiles (x k-splits)
   int q_tail;       // > 1: the tiles after them run as q_tail column slices each (last-wave balance)
@@ -107,6 +109,7 @@ struct AgTcParams {
   // own rows come first (they never wait on the network).
   int msharded, mpr, mt_rot;
   int l2hint;  // TMA L2 policies: 1 A evict_last, 2 B evict_first (TFB_L2HINT)
+  int one_producer;  // TFB_ONE_PRODUCER: warp 0 issues A and B boxes (no B producer warp)
   const __nv_bfloat16* peer_shard[64];
 };
 
@@ -297,6 +300,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t lead = crank - prank;                  // the pair leader's cluster rank
   const uint16_t pair_mask = uint16_t(3u << lead);
   const bool leader = prank == 0;
+  const bool two_prod = NH == 1 && !p.gather && !p.one_producer;  // B boxes from warp 6 (see the producer)
   const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
   const int num_mt = (p.num_m + CG - 1) / CG;  // tile rows (BM * CG each)
   // Work items: (tile, k-split).  Split ks covers k-block slots
@@ -340,7 +344,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tma_prefetch(&tmC);
     if (p.b4) tma_prefetch(&tmB4);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], CG);  // one arrive per CTA of the pair (the leader's copy is used)
+      mbar_init(&full[s], CG * (two_prod ? 2 : 1));  // one arrive per producer thread per CTA (leader's copy used)
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -358,12 +362,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
   // Profiling (TFB_DEBUG & 4096): %globaltimer phase stamps of CTA 0, printed at exit.
   __shared__ unsigned long long s_ts[12];
+  __shared__ unsigned long long s_kp[24], s_km[24];  // TFB_DEBUG 8192: producer / MMA per-k-block stamps
   const bool tsd = (p.dbg & 4096) && blockIdx.x == 0;
   if (tsd && threadIdx.x == 0)
     for (int i = 0; i < 12; ++i) s_ts[i] = i == 0 ? globaltimer_ns() : 0;
 
-  if (warp == 0) {
+  if (warp == 0 || (two_prod && warp == 6)) {
     // ===== TMA producer (both CTAs of a pair) =====
+    // With NH = 1 and no gather work, warp 6 (otherwise idle) issues the B
+    // boxes and warp 0 the A boxes: the producer's per-k-block chain is the
+    // skinny-M bound (TFB_DEBUG 8192 cadence), and the TMA issue is most of it.
+    const bool do_a = warp == 0, do_b = warp == 6 || !two_prod;
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
@@ -373,6 +382,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint64_t pol_a = 0, pol_b = 0;
       if (p.l2hint & 1) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_a));
       if (p.l2hint & 2) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_b));
+      // Launch constants hoisted into registers: the k-block loop below is
+      // one thread's dependent instruction chain that no other warp hides,
+      // so it carries no divisions and no parameter reloads (TFB_DEBUG 8192
+      // cadence with loads and MMAs off: ~790 cycles per k-block with the
+      // per-iteration `%` / `/` and constant-bank reloads).
+      const int own = p.own, kbw = p.kbw, kbt = p.kb_total, nm = p.num_m;
+      const bool msh = p.msharded != 0, b4 = p.b4 != 0;
+      const bool skip_a = (p.dbg & 256) != 0 || !do_a, skip_b = (p.dbg & 512) != 0 || !do_b;
+      const bool kstamp = (p.dbg & 8192) != 0 && do_a;
+      const uint64_t* const ready = p.ready;
+      const uint32_t full_bar0 = CG == 2 ? mapa(&full[0], lead) : smem_u32(&full[0]);
+      const int a_col_own = msh ? 0 : own * p.kw;       // own-shard map: column offset (K-sharded)
+      const int a_row_own = msh ? own * p.mpr * BM : 0;  // own-shard map: row offset (M-sharded)
       for (int t = cid; t < num_tiles; t += ncl) {
         int mt, n0, wcol, i0, i1;
         item_geom(t, mt, n0, wcol, i0, i1);
@@ -382,34 +404,41 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // every 256-column MMA (CG = 2: 128 columns), or of one 128-wide one.
         const int nhalf = wcol >= 256 ? wcol / 256 : 1;
         const int cpc = wcol >= 256 ? CPH : 2 / CG;  // chunks per MMA per CTA
-        const uint32_t tx = uint32_t(CG) * uint32_t(A_BYTES + nhalf * cpc * BK * 128);
+        const uint32_t tx = uint32_t(CG) * uint32_t((skip_a ? 0 : A_BYTES) + (skip_b ? 0 : nhalf * cpc * BK * 128));
+        const bool whole = wcol == K_::BN_TILE;
         uint64_t ready_mask = 0;
+        // k-block of slot i0 in the rank's rotated order, its owner (column
+        // band; M-sharded: row band, rows past M reading the zero-filled
+        // edge) and its position inside the owner's band -- then stepped.
+        int kb = msh ? i0 : own >= 0 ? (i0 + own * kbw) % kbt : i0;
+        int src = !msh ? kb / kbw : mb < nm ? mb / p.mpr : -1;
+        int kin = msh ? 0 : kb - src * kbw;
+        const bool gated = do_a && ready != nullptr && mb < nm;
         for (int i = i0; i < i1; ++i) {
-          const int kb = p.msharded ? i : p.own >= 0 ? (i + p.own * p.kbw) % p.kb_total : i;
-          // Owner of this k-block of this m-block: by column band (K-sharded)
-          // or row band (M-sharded; rows past M read the zero-filled edge).
-          const int src = !p.msharded ? kb / p.kbw : mb < p.num_m ? mb / p.mpr : -1;
           mbar_wait(&empty[stage], phase ^ 1);
-          const bool from_own = src == p.own;
-          if (!from_own && p.ready && mb < p.num_m && !((ready_mask >> src) & 1ull)) {
-            wait_geq(p.ready + size_t(mb) * p.W + src, p.epoch, p.watchdog_ns, p.err, kWaitSignal,
-                     p.own, p.board, src, mb, 0);
+          if (kstamp && blockIdx.x == 0 && t == cid && i - i0 < 24) s_kp[i - i0] = clock64();
+          const bool from_own = src == own;
+          if (gated && !from_own && !((ready_mask >> src) & 1ull)) {
+            wait_geq(ready + size_t(mb) * p.W + src, p.epoch, p.watchdog_ns, p.err, kWaitSignal, own, p.board,
+                     src, mb, 0);
             fence_proxy_async_global();
             ready_mask |= 1ull << src;
             if (p.events)  // first consumer load of this (m-block, source) chunk
               atomicMin(p.events + (size_t(mb) * p.W + src) * 2 + 1, (unsigned long long)globaltimer_ns());
           }
-          const uint32_t bar = CG == 2 ? mapa(&full[stage], lead) : smem_u32(&full[stage]);
+          const uint32_t bar = full_bar0 + uint32_t(stage) * 8u;
           if (leader) mbar_arrive_expect_tx(&full[stage], tx);
           else mbar_arrive_cluster(bar);
-          uint8_t* a_dst = smA + stage * A_BYTES;
-          if (from_own && p.msharded) tma_load<CG>(a_dst, &tmA_own, bar, kb * BK, m0 - p.own * p.mpr * BM, pol_a);
-          else if (from_own) tma_load<CG>(a_dst, &tmA_own, bar, kb * BK - p.own * p.kw, m0, pol_a);
-          else tma_load<CG>(a_dst, &tmA_inbox, bar, kb * BK, m0, pol_a);
+          if (!skip_a) {
+            uint8_t* a_dst = smA + stage * A_BYTES;
+            if (from_own) tma_load<CG>(a_dst, &tmA_own, bar, kb * BK - a_col_own, m0 - a_row_own, pol_a);
+            else tma_load<CG>(a_dst, &tmA_inbox, bar, kb * BK, m0, pol_a);
+          }
           uint8_t* b_dst = smB + stage * K_::B_BYTES;
-          if (wcol == K_::BN_TILE && p.b4) {
+          if (skip_b) {
+          } else if (whole && b4) {
             tma_load_4d<CG>(b_dst, &tmB4, bar, kb * BK, int(prank) * CPH, n0 / 256, pol_b);
-          } else if (wcol == K_::BN_TILE) {
+          } else if (whole) {
 #pragma unroll
             for (int h = 0; h < NH; ++h)
 #pragma unroll
@@ -426,6 +455,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             stage = 0;
             phase ^= 1;
           }
+          if (msh) {
+            ++kb;
+          } else {
+            if (++kb == kbt) kb = 0;
+            if (++kin == kbw) {  // next owner's band (rare: W times per tile)
+              kin = 0;
+              src = kb / kbw;
+            }
+          }
         }
       }
     }
@@ -441,14 +479,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t aphase = 0;
+      // Shared-memory descriptors as base + offset: the start-address field
+      // is the low 14 bits of (address >> 4) and never carries (smem < 256
+      // KB), so stage / k / half steps are plain adds -- the MMA thread's
+      // per-k-block chain stays short (it paced the skinny main loops).
+      const uint64_t adesc0 = smem_desc_sw128(smem_u32(smA), 16, 1024);
+      const uint64_t bdesc0 = smem_desc_sw128(smem_u32(smB), BK * 128, 1024);
+      const bool no_mma = (p.dbg & 2) != 0;
       auto mma_kblock = [&](int stg, int h0, int h1, bool first_kb, bool whole, int nhalf, uint32_t idesc) {
-        const uint32_t a_addr = smem_u32(smA + stg * A_BYTES);
-        const uint32_t b_addr = smem_u32(smB + stg * K_::B_BYTES);
-        if (p.dbg & 2) return;
+        if (no_mma) return;
+        const uint64_t a_st = adesc0 + uint64_t(uint32_t(stg * A_BYTES) >> 4);
+        const uint64_t b_st = bdesc0 + uint64_t(uint32_t(stg * K_::B_BYTES) >> 4);
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k) {
           // A: K-major SW128, 8-row groups 1024 B apart; +32 B per K=16.
-          const uint64_t ad = smem_desc_sw128(a_addr + k * 32, 16, 1024);
+          const uint64_t ad = a_st + uint64_t((k * 32) >> 4);
           // B: MN-major SW128, 64-column chunks 8 KB apart (LBO), 8-row K
           // groups 1 KB apart (SBO); +16 rows (2 KB) per K=16.  Whole tiles
           // take the unrolled constant-descriptor path: the single issuing
@@ -458,12 +503,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int h = 0; h < NH; ++h) {
               if (h < h0 || h >= h1) continue;
-              const uint64_t bd = smem_desc_sw128(b_addr + h * CPH * (BK * 128) + k * 2048, BK * 128, 1024);
+              const uint64_t bd = b_st + uint64_t((h * CPH * (BK * 128) + k * 2048) >> 4);
               mma_issue<CG>(tmem_base + uint32_t((acc * NH + h) * 256), ad, bd, K_::IDESC, !first_kb || k != 0);
             }
           } else {
             for (int h = 0; h < nhalf; ++h) {
-              const uint64_t bd = smem_desc_sw128(b_addr + h * CPH * (BK * 128) + k * 2048, BK * 128, 1024);
+              const uint64_t bd = b_st + uint64_t(uint32_t(h * CPH * (BK * 128) + k * 2048) >> 4);
               mma_issue<CG>(tmem_base + uint32_t((acc * NH + h) * 256), ad, bd, idesc, !first_kb || k != 0);
             }
           }
@@ -512,6 +557,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         for (; i < i1; ++i) {
           mbar_wait(&full[stage], phase);
+          if ((p.dbg & 8192) && blockIdx.x == 0 && t == cid && i - i0 < 24) s_km[i - i0] = clock64();
           if (tsd && !s_ts[1]) s_ts[1] = globaltimer_ns();
           tc_fence_after();
           mma_kblock(stage, 0, NH, i == i0, whole, nhalf, idesc);
@@ -812,6 +858,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_before();
   if (CG == 2 || p.ksplit > 1) cluster_sync();
   else __syncthreads();
+  if ((p.dbg & 8192) && blockIdx.x == 0 && threadIdx.x == 0) {
+    printf("[ag cta0 k-block cadence, cycles] producer-empty:");
+    for (int i = 1; i < 24; ++i) printf(" %lld", (long long)(s_kp[i] - s_kp[i - 1]));
+    printf("\n[ag cta0 k-block cadence, cycles] mma-full:      ");
+    for (int i = 1; i < 24; ++i) printf(" %lld", (long long)(s_km[i] - s_km[i - 1]));
+    printf("\n[ag cta0] mma-full[i] - producer-empty[i]:");
+    for (int i = 0; i < 24; ++i) printf(" %lld", (long long)(s_km[i] - s_kp[i]));
+    printf("\n");
+  }
   if (tsd && threadIdx.x == 0) {
     auto rel = [&](int i) { return s_ts[i] ? (long long)(s_ts[i] - s_ts[0]) : -1ll; };
     printf("[ag cta0 CG=%d NH=%d S=%d] first-stage %lld last-commit %lld tfull %lld exchanged %lld "
@@ -988,6 +1043,7 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   p.board = board;
   if (const char* e = std::getenv("TFB_DEBUG")) p.dbg = std::atoi(e);
   if (const char* e = std::getenv("TFB_L2HINT")) p.l2hint = std::atoi(e);
+  p.one_producer = std::getenv("TFB_ONE_PRODUCER") ? 1 : 0;
   const int dev = w->ranks[r].device;
   cudaSetDevice(dev);
   // Kernel shapes: CTA pairs (cta_group::2) with 256 x 512 tiles whenever
