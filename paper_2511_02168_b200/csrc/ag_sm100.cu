@@ -486,6 +486,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint64_t adesc0 = smem_desc_sw128(smem_u32(smA), 16, 1024);
       const uint64_t bdesc0 = smem_desc_sw128(smem_u32(smB), BK * 128, 1024);
       const bool no_mma = (p.dbg & 2) != 0;
+      const bool mstamp = (p.dbg & 8192) != 0 && blockIdx.x == 0;
       auto mma_kblock = [&](int stg, int h0, int h1, bool first_kb, bool whole, int nhalf, uint32_t idesc) {
         if (no_mma) return;
         const uint64_t a_st = adesc0 + uint64_t(uint32_t(stg * A_BYTES) >> 4);
@@ -557,7 +558,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         for (; i < i1; ++i) {
           mbar_wait(&full[stage], phase);
-          if ((p.dbg & 8192) && blockIdx.x == 0 && t == cid && i - i0 < 24) s_km[i - i0] = clock64();
+          if (mstamp && t == cid && i - i0 < 24) s_km[i - i0] = clock64();
           if (tsd && !s_ts[1]) s_ts[1] = globaltimer_ns();
           tc_fence_after();
           mma_kblock(stage, 0, NH, i == i0, whole, nhalf, idesc);
