@@ -30,6 +30,15 @@ for name in sys.argv[1:] or ["c3", "c4"]:
         for _ in range(5):
             _abi.check(w.lib.tf_flash_decode_async(*args))
         _abi.check(w.lib.tf_world_sync(w.handle))
+        # back-to-back mean (no event between launches), then per-launch events
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for i in range(n):
+            _abi.check(w.lib.tf_flash_decode_async(*args))
+        e1.record(st)
+        _abi.check(w.lib.tf_world_sync(w.handle))
+        torch.cuda.synchronize()
+        mean = e0.elapsed_time(e1) * 1e3 / n
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
         evs[0].record(st)
         for i in range(n):
@@ -39,5 +48,5 @@ for name in sys.argv[1:] or ["c3", "c4"]:
         torch.cuda.synchronize()
         ts = sorted(evs[i].elapsed_time(evs[i + 1]) * 1e3 for i in range(n))
         kv = 2 * Bt * Hkv * L * d * 2
-        print(f"{tag:8s} {name:5s} p10 {ts[n // 10]:7.1f} p50 {ts[n // 2]:7.1f} min {ts[0]:7.1f} us  "
-              f"{kv / ts[n // 2] / 1e3:6.0f} GB/s", flush=True)
+        print(f"{tag:8s} {name:5s} mean {mean:7.1f} us ({kv / mean / 1e3:5.0f} GB/s)  per-launch-events p50 "
+              f"{ts[n // 2]:7.1f} min {ts[0]:7.1f} us", flush=True)
