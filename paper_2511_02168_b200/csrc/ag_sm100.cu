@@ -487,6 +487,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint64_t bdesc0 = smem_desc_sw128(smem_u32(smB), BK * 128, 1024);
       const bool no_mma = (p.dbg & 2) != 0;
       const bool mstamp = (p.dbg & 8192) != 0 && blockIdx.x == 0;
+      const bool kfence = (p.dbg & 32768) == 0;  // TFB_DEBUG 32768: no tcgen05 fence after each full wait (A/B)
       auto mma_kblock = [&](int stg, int h0, int h1, bool first_kb, bool whole, int nhalf, uint32_t idesc) {
         if (no_mma) return;
         const uint64_t a_st = adesc0 + uint64_t(uint32_t(stg * A_BYTES) >> 4);
@@ -536,7 +537,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint32_t p2 = phase;
           for (int j = 0; j < pre; ++j) {
             mbar_wait(&full[s2], p2);
-            tc_fence_after();
+            if (kfence) tc_fence_after();
             mma_kblock(s2, 0, 1, j == 0, true, 2, idesc);
             advance(s2, p2);
           }
@@ -560,7 +561,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_wait(&full[stage], phase);
           if (mstamp && t == cid && i - i0 < 24) s_km[i - i0] = clock64();
           if (tsd && !s_ts[1]) s_ts[1] = globaltimer_ns();
-          tc_fence_after();
+          if (kfence) tc_fence_after();
           mma_kblock(stage, 0, NH, i == i0, whole, nhalf, idesc);
           mma_commit_all<CG>(&empty[stage], pair_mask);
           advance(stage, phase);
