@@ -175,9 +175,15 @@ tf_status tf_signal_soak(tf_world* w, uint64_t seed, int rounds,
  * capture: a single-rank world's *_async calls may be captured on an
  * explicit stream and replayed (per-launch counters reset on the device;
  * after one eager call, so lazily allocated workspace exists); capturing a
- * multi-rank schedule returns TF_ERR_CONFIG.  Arrays are indexed by global rank;
- * entries for ranks not local to this process are ignored except a_shard,
- * whose peer entries must be the heap mappings tf_heap_alloc returned. */
+ * multi-rank schedule returns TF_ERR_CONFIG.  The tensor-core GEMM and the
+ * Flash Decode kernels are launched with programmatic dependent launch
+ * (cudaLaunchAttributeProgrammaticStreamSerialization): each waits for its
+ * stream predecessor's memory (griddepcontrol.wait) before touching any
+ * global data, so stream order is unchanged -- only the launch latency
+ * overlaps the predecessor's tail (TFB_NO_PDL=1 turns it off).  Arrays are
+ * indexed by global rank; entries for ranks not local to this process are
+ * ignored except a_shard, whose peer entries must be the heap mappings
+ * tf_heap_alloc returned. */
 /* How A is sharded before the all-gather.  TF_SHARD_K (0, the reference,
  * ag_gemm.hpp:100-107): rank r holds columns [r*k/W, (r+1)*k/W), an m x k/W
  * shard.  TF_SHARD_M (1, an extension: the alternative sharding the paper
