@@ -156,21 +156,44 @@ extern "C" tf_status tf_ag_gemm_host_async(tf_world* tw, tf_ag_variant variant, 
   g_trace.start(s[w->first_local]);
   const int tr = w->first_local;
 
+  // Buffer sets: a one-rank world alternates two (shard region, device B,
+  // device C), so back-to-back calls on different streams overlap -- call
+  // i+1's H2D streams in while call i's last slabs compute and read back.
+  // Every call orders its copies after the caller's prior work on its own
+  // stream, its H2D after the last GEMM that read the same set and its
+  // GEMMs after the last read-back of the same C (events per set).  With
+  // W > 1 (peers read the shard region) there is one set, so calls on
+  // different streams still serialise through those events.
+  const bool dual = W == 1;
+  int par = 0;
+  if (dual) {
+    par = w->ranks[w->first_local].host_par;
+    w->ranks[w->first_local].host_par ^= 1;
+  }
   // Shards live in the symmetric heap (peers pull them / push from them).
   size_t shard_off = 0;
-  TFB_CHECK(heap_get(w, "ag.host.a[" + std::to_string(m * kw * esz) + "]", m * kw * esz, &shard_off));
+  TFB_CHECK(heap_get(w, "ag.host.a" + std::string(par ? "1" : "") + "[" + std::to_string(m * kw * esz) + "]",
+                     m * kw * esz, &shard_off));
   std::vector<void*> shard(W), bdev(W, nullptr), cdev(W, nullptr);
   for (int r = 0; r < W; ++r) shard[r] = w->ptr(r, shard_off);
   for (int r = 0; r < W; ++r) {
     if (!w->ranks[r].local) continue;
     TFB_CHECK(ensure_copy_streams(w, r));
-    TFB_CHECK(ensure_scratch(w, r, 0, k * n * esz, &bdev[r]));
-    TFB_CHECK(ensure_scratch(w, r, 1, m * n * esz, &cdev[r]));
+    TFB_CHECK(ensure_scratch(w, r, par ? 3 : 0, k * n * esz, &bdev[r]));
+    TFB_CHECK(ensure_scratch(w, r, par ? 4 : 1, m * n * esz, &cdev[r]));
     RankRes& rr = w->ranks[r];
     cudaSetDevice(rr.device);
-    // Copies start after the caller's prior work on its stream (buffer reuse).
+    for (int i = 0; i < 2; ++i) {
+      if (!rr.host_reads_done[i]) TFB_CUDA(cudaEventCreateWithFlags(&rr.host_reads_done[i], cudaEventDisableTiming));
+      if (!rr.host_d2h_done[i]) TFB_CUDA(cudaEventCreateWithFlags(&rr.host_d2h_done[i], cudaEventDisableTiming));
+    }
+    // Copies start after the caller's prior work on its stream, the H2D
+    // after the set's previous readers, the GEMMs after the set's previous
+    // C read-back.
     TFB_CHECK(join(rr.h2d, s[r]));
     TFB_CHECK(join(rr.d2h, s[r]));
+    TFB_CUDA(cudaStreamWaitEvent(rr.h2d, rr.host_reads_done[par], 0));
+    TFB_CUDA(cudaStreamWaitEvent(s[r], rr.host_d2h_done[par], 0));
     TFB_CUDA(cudaMemcpyAsync(shard[r], a_host[r], m * kw * esz, cudaMemcpyDefault, rr.h2d));
     if (r == tr) g_trace.mark("h2d shard", rr.h2d);
   }
@@ -228,9 +251,16 @@ extern "C" tf_status tf_ag_gemm_host_async(tf_world* tw, tf_ag_variant variant, 
     }
     off += ns;
   }
-  // The call completes on the caller's streams.
+  // The set's readers and read-back are done at these events; the call
+  // completes on the caller's streams.
   for (int r = 0; r < W; ++r)
-    if (w->ranks[r].local) TFB_CHECK(join(s[r], w->ranks[r].d2h));
+    if (w->ranks[r].local) {
+      RankRes& rr = w->ranks[r];
+      cudaSetDevice(rr.device);
+      TFB_CUDA(cudaEventRecord(rr.host_reads_done[par], s[r]));
+      TFB_CUDA(cudaEventRecord(rr.host_d2h_done[par], rr.d2h));
+      TFB_CHECK(join(s[r], rr.d2h));
+    }
   return TF_OK;
 }
 

@@ -576,6 +576,10 @@ tf_status tf_world_destroy(tf_world* tw) {
     if (rr.d2h) cudaStreamSynchronize(rr.d2h), cudaStreamDestroy(rr.d2h);
     for (void* p : rr.scratch)
       if (p) cudaFree(p);
+    for (int i = 0; i < 2; ++i) {
+      if (rr.host_reads_done[i]) cudaEventDestroy(rr.host_reads_done[i]);
+      if (rr.host_d2h_done[i]) cudaEventDestroy(rr.host_d2h_done[i]);
+    }
   }
   for (int r = 0; r < (int)w->ranks.size(); ++r) {
     RankRes& rr = w->ranks[r];

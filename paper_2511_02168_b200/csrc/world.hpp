@@ -29,9 +29,16 @@ struct RankRes {
   // buffers, created on first use, grow-only.
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t legacy_ev = nullptr;  // order_after_legacy
-  // [0] B / [1] C device operands of host-buffer runs, [2] split-K workspace
-  void* scratch[3] = {nullptr, nullptr, nullptr};
-  size_t scratch_bytes[3] = {0, 0, 0};
+  // [0] B / [1] C device operands of host-buffer runs, [2] split-K
+  // workspace, [3] B / [4] C of the second host-run buffer set (W = 1)
+  void* scratch[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  size_t scratch_bytes[5] = {0, 0, 0, 0, 0};
+  // Host-buffer runs of a one-rank world alternate two buffer sets so that
+  // back-to-back calls on different streams overlap (ag_host.cu): per set,
+  // the event after its last GEMM (B / shard free) and after its last C
+  // read-back (C free).
+  int host_par = 0;
+  cudaEvent_t host_reads_done[2] = {nullptr, nullptr}, host_d2h_done[2] = {nullptr, nullptr};
 };
 
 struct HeapEntry {
@@ -189,7 +196,7 @@ inline int pdl_attrs(cudaLaunchAttribute* a) {
   return 1;
 }
 
-// Grow-only device scratch of rank r (slot < 3); first use allocates.
+// Grow-only device scratch of rank r (slot < 5); first use allocates.
 tf_status ensure_scratch(World* w, int r, int slot, size_t bytes, void** out);
 // Wait for local streams and turn the device error record into a status.
 tf_status sync_and_check(World* w, const std::vector<cudaStream_t>& streams);
