@@ -105,3 +105,41 @@ def test_host_bad_args():
         assert w.lib.tf_ag_gemm_host(w.handle, _abi.TF_AG_PULL, C.byref(bad), z, z, z, None) == _abi.TF_ERR_CONFIG
     finally:
         w.close()
+
+
+@pytest.mark.parametrize("W", [1, 2])
+def test_host_calls_overlap_on_two_streams(oracle, W):
+    """Back-to-back async calls with DIFFERENT inputs on two streams: a
+    one-rank world alternates two buffer sets (the second call's H2D runs
+    while the first still computes / reads back), a multi-rank world
+    serialises through the set events -- either way every call's C is its
+    own inputs' product, bitwise the single-call result."""
+    import torch
+    m, n, k = 512, 4616, 256 * W
+    kw = k // W
+    ins = [_bf16_inputs(oracle, 40 + i, m, n, k) for i in range(4)]
+    with tf.World(W, [0] * W, 64 << 20) as w:
+        want = [_host_run(w, _abi.TF_AG_PULL, m, n, k, a, b, _abi.TF_BF16, True) for a, b in ins]
+        streams = [[torch.cuda.Stream() for _ in range(W)] for _ in range(2)]  # per call parity, per rank
+        bufs = []
+        for i, (a, b) in enumerate(ins):
+            A = torch.from_numpy(a).bfloat16()
+            B = torch.from_numpy(b).bfloat16()
+            shards = [A[:, r * kw:(r + 1) * kw].contiguous().pin_memory() for r in range(W)]
+            bs = [B.clone().pin_memory() for _ in range(W)]
+            cs = [torch.empty((m, n), dtype=torch.bfloat16).pin_memory() for _ in range(W)]
+            bufs.append((shards, bs, cs))
+        torch.cuda.synchronize()
+        shape = _abi.AgShape(m, n, k, 0, 0, 0, _abi.TF_BF16)
+        for i, (shards, bs, cs) in enumerate(bufs):
+            sts = [x.cuda_stream for x in streams[i % 2]]
+            _abi.check(w.lib.tf_ag_gemm_host_async(
+                w.handle, _abi.TF_AG_PULL, C.byref(shape), _abi.ptr_array([x.data_ptr() for x in shards]),
+                _abi.ptr_array([x.data_ptr() for x in bs]), _abi.ptr_array([x.data_ptr() for x in cs]),
+                _abi.ptr_array(sts)))
+        torch.cuda.synchronize()
+        _abi.check(w.lib.tf_world_sync(w.handle))
+        for i, (_, _, cs) in enumerate(bufs):
+            for r in range(W):
+                got = cs[r].float().numpy()
+                assert np.array_equal(got.view(np.uint32), want[i][r].view(np.uint32)), (i, r)
