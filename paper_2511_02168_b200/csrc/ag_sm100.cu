@@ -1122,8 +1122,11 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   } else if (shp->CG == 2 && !std::getenv("TFB_NO_NARROW")) {
     int t2, n2, k2;
     TFB_CHECK(plan(shapes[2], t2, n2, k2));
-    // Narrow pair tiles only when the wide ones leave a quarter of the SMs idle.
-    if (unsigned(tiles * ks * 2) * 4 < grid_cap * 3 && t2 * k2 > tiles * ks) {
+    // Narrow pair tiles only when the wide ones leave a quarter of the SMs
+    // idle and the narrow ones fit one wave (M = 768: 96 narrow tiles on 74
+    // pairs ran 148 us vs 89 us for 48 wide tiles, tools/skinny_ab.py).
+    if (unsigned(tiles * ks * 2) * 4 < grid_cap * 3 && t2 * k2 > tiles * ks &&
+        unsigned(t2 * k2 * 2) <= grid_cap) {
       shp = &shapes[2];
       tiles = t2;
       num_n = n2;

@@ -25,7 +25,8 @@ def norm_err(c, ref):
     return float(np.abs(c - ref).max() / max(np.abs(ref).max(), 1e-30))
 
 
-@pytest.mark.parametrize("m,n,k", [(128, 256, 64), (256, 512, 512), (300, 264, 192), (1, 8, 64), (129, 1032, 1024)])
+@pytest.mark.parametrize("m,n,k", [(128, 256, 64), (256, 512, 512), (300, 264, 192), (1, 8, 64), (129, 1032, 1024),
+                                   (768, 8192, 256)])  # wide pair tiles: narrow ones would need two waves
 def test_single_rank_gemm(oracle, m, n, k):
     import torch
     p = bf16_problem(m * 7 + n, m, n, k, oracle)
