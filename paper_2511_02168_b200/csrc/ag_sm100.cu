@@ -1133,6 +1133,35 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
       ks = k2;
     }
   }
+  // Whole-K plans with a partial last round: compare rounds x tile time
+  // across the three tile shapes (tile times relative to a 256 x 512 pair
+  // tile, measured at K = N = 8192: 256 x 256 pairs 0.72, 128 x 256 CTAs
+  // 0.77).  M = 1152: 80 wide tiles on 74 pairs run two rounds (162 us),
+  // 288 single-CTA tiles two nearly full ones (125 us; cuBLAS 122).
+  if (shp->CG == 2 && ks == 1 && !(p.dbg & 8) && !std::getenv("TFB_NO_NARROW") && !std::getenv("TFB_FORCE_NARROW")) {
+    auto rounds = [](long items, long slots) { return double((items + slots - 1) / slots); };
+    const long pairs = long(grid_cap / 2);
+    double best = rounds(long(tiles), pairs) * (shp->NH == 2 ? 1.0 : 0.72);
+    const Shape* pick = shp;
+    int t0, n0, k0;
+    TFB_CHECK(plan(shapes[0], t0, n0, k0));
+    if (k0 == 1 && rounds(t0, long(grid_cap)) * 0.77 < best * 0.95) {
+      best = rounds(t0, long(grid_cap)) * 0.77;
+      pick = &shapes[0];
+    }
+    if (shp->NH == 2) {
+      int t2, n2, k2;
+      TFB_CHECK(plan(shapes[2], t2, n2, k2));
+      if (k2 == 1 && rounds(t2, pairs) * 0.72 < best * 0.95) {
+        best = rounds(t2, pairs) * 0.72;
+        pick = &shapes[2];
+      }
+    }
+    if (pick != shp) {
+      shp = pick;
+      TFB_CHECK(plan(*shp, tiles, num_n, ks));
+    }
+  }
   const int CG = shp->CG;
   p.num_n = num_n;
   p.mt_rot = (p.msharded && own >= 0) ? (own * p.mpr / CG) % ((p.num_m + CG - 1) / CG) : 0;
@@ -1174,7 +1203,13 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
     const int ncl = int(grid) / CG, T = p.num_tiles;
     const int fr = T / ncl, rem = T % ncl;
     if (fr >= 1 && rem > 0) {
-      int q = shp->NH == 2 ? 4 : 2;
+      // Off by default: a column slice ran as long as a whole tile at every
+      // shape measured (M = 1152 / 4096, K = N = 8192: 172 / 410 us with 4
+      // slices, 162 / 395 whole; config 2 within noise) -- the slice's
+      // k-block chain, not its MMA width, sets its time.  TFB_TAIL_Q = 2 / 4
+      // turns it on.
+      int q = 1;
+      if (const char* e = std::getenv("TFB_TAIL_Q")) q = std::max(1, std::atoi(e));
       while (q > 1 && rem * q > ncl) q /= 2;
       if (q > 1) {
         p.full_items = fr * ncl;
