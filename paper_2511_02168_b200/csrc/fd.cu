@@ -606,6 +606,7 @@ __device__ void fast_split(const FdParams& P, int lr, int g, int sp, float* wsro
     }
     P.trace[size_t(blockIdx.x) * kTraceSlots + 10] = lo;
     P.trace[size_t(blockIdx.x) * kTraceSlots + 11] = hi;
+    for (int w = 0; w < kFastWarps; ++w) P.trace[size_t(blockIdx.x) * kTraceSlots + 22 + w] = sm.wend[w];
   }
   if (sm.bad) {
     if (threadIdx.x == 0)

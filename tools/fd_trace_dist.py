@@ -60,3 +60,10 @@ with tf.World(1, [0], 512 << 20) as w:
             print(f"   last-warp-done->computed: first CTA on SM p50 {np.median(d1):.2f}  second {np.median(d2):.2f}")
         for sl, nm in ((22, "ck trace+bad"), (23, "ck weights"), (24, "ck barrier2")):
             print(f"   {nm:16s} cycles p10/50/90/max " + " ".join(f"{x:7.0f}" for x in np.percentile(t[:, sl], [10, 50, 90, 100])))
+        wt = rel[:, 22:30]
+        ok = (wt >= 0).all(axis=1)
+        if ok.any():
+            wt = wt[ok] - wt[ok].min(axis=1, keepdims=True)
+            print("   per-warp finish (us after the CTA's first warp), mean by warp: " +
+                  " ".join(f"{x:5.2f}" for x in wt.mean(axis=0)))
+            blk = t[ok, 15] if False else None
