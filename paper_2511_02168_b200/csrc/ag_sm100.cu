@@ -956,6 +956,104 @@ __global__ void __launch_bounds__(512) ag_push_kernel(const PushParams p) {
   }
 }
 
+// PUSH producer on the TMA engine: one warp per CTA, one elected thread.
+// Each claimed m-block of this rank's shard is staged box by box (64 x 256
+// bf16 = 32 KB, SWIZZLE_NONE) into a kPushStages-deep smem ring by TMA
+// loads, and every staged box is written to all W inboxes by TMA stores
+// (read once, stored W times -- the multicast-shaped part of push).  After
+// an m-block's stores complete (bulk wait_group 0), its W flags are raised
+// with system-scope release.  The SM does no per-element work, so a few
+// CTAs move what 16 register-copy CTAs did (tools/probe_push.py).
+constexpr int kPushStages = 4;
+constexpr int kPushMaxW = 8;
+struct PushMaps {
+  CUtensorMap src;                // this rank's shard: K-sharded [M][kw], M-sharded [mr][K]
+  CUtensorMap dst[kPushMaxW];     // every rank's inbox [M][K]
+};
+struct PushTmaParams {
+  uint64_t* ready[kPushMaxW];
+  unsigned long long* events[kPushMaxW];
+  int W, self, nmb;          // m-blocks this rank pushes
+  int msharded, mpr;
+  int box_c, box_r;          // box columns / rows
+  int cols;                  // shard columns (kw or K)
+  int M;
+  int local;                 // every destination inbox is on this CTA's device
+  int skip_self;             // own block read in place: only its flag is raised
+  unsigned int* ctr;         // [0] m-block counter, [1] done
+};
+
+__global__ void __launch_bounds__(32) ag_push_tma_kernel(const __grid_constant__ PushMaps maps,
+                                                         const __grid_constant__ PushTmaParams p) {
+  extern __shared__ __align__(1024) uint8_t push_smem[];
+  __shared__ __align__(8) uint64_t full[kPushStages];
+  if (threadIdx.x != 0) return;
+  const uint32_t box_bytes = uint32_t(p.box_c) * uint32_t(p.box_r) * 2u;
+  for (int s = 0; s < kPushStages; ++s) mbar_init(&full[s], 1);
+  fence_mbar_init();
+  tma_prefetch(&maps.src);
+  for (int d = 0; d < p.W; ++d) tma_prefetch(&maps.dst[d]);
+  const int ncb = p.cols / p.box_c, nrb = BM / p.box_r, nbox = ncb * nrb;
+  uint32_t issued = 0, consumed = 0;  // ring positions (box sequence numbers) of this CTA
+  for (;;) {
+    const int i = int(atomicAdd(&p.ctr[0], 1u));
+    if (i >= p.nmb) break;
+    const int mb = p.msharded ? p.self * p.mpr + i : i;   // global m-block (inbox rows)
+    const int r_src = p.msharded ? i * BM : mb * BM;      // rows in the shard map
+    const int c_dst = p.msharded ? 0 : p.self * p.cols;   // inbox column of the shard's column 0
+    auto box_at = [&](int j, int& c, int& r) {
+      c = (j % ncb) * p.box_c;
+      r = (j / ncb) * p.box_r;
+    };
+    // Prime S - 1 stages, then: wait box j, store it to every inbox, and
+    // load box j + S - 1 into the stage of box j - 1 (whose stores have read
+    // it: every group but the newest).
+    int next = 0;
+    auto load_next = [&]() {
+      const uint32_t st = issued % kPushStages;
+      int c, r;
+      box_at(next, c, r);
+      mbar_arrive_expect_tx(&full[st], box_bytes);
+      tma_load_2d(push_smem + st * box_bytes, &maps.src, &full[st], c, r_src + r);
+      ++issued;
+      ++next;
+    };
+    while (next < nbox && issued - consumed < uint32_t(kPushStages - 1)) load_next();
+    for (int j = 0; j < nbox; ++j) {
+      const uint32_t st = consumed % kPushStages;
+      mbar_wait(&full[st], (consumed / kPushStages) & 1u);
+      int c, r;
+      box_at(j, c, r);
+      for (int k = 1; k <= p.W - p.skip_self; ++k) {  // peers first, own inbox last
+        const int d = (p.self + k) % p.W;
+        tma_store_2d(&maps.dst[d], push_smem + st * box_bytes, c_dst + c, mb * BM + r);
+      }
+      bulk_commit();
+      ++consumed;
+      if (next < nbox) {
+        bulk_wait_read<1>();  // box j - 1's stores have read their stage
+        load_next();
+      }
+    }
+    bulk_wait_all();             // this m-block's stores are complete
+    fence_proxy_async_global();  // async-proxy writes before the generic release
+    if (p.local) __threadfence();  // every inbox on this device: gpu scope suffices
+    else __threadfence_system();
+    for (int k = 1; k <= p.W; ++k) {
+      const int d = (p.self + k) % p.W;
+      if (p.events[d]) p.events[d][(size_t(mb) * p.W + p.self) * 2] = globaltimer_ns();
+      if (p.local) red_release_gpu(p.ready[d] + size_t(mb) * p.W + p.self, 1);
+      else red_release_sys(p.ready[d] + size_t(mb) * p.W + p.self, 1);
+    }
+  }
+  __threadfence();
+  if (atomicAdd(&p.ctr[1], 1u) == gridDim.x - 1) {
+    p.ctr[0] = 0;
+    p.ctr[1] = 0;
+    __threadfence();
+  }
+}
+
 // ---- host ------------------------------------------------------------------------
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -990,7 +1088,8 @@ CUtensorMapL2promotion l2_promotion() {
 // 2-D bf16 map: `inner` contiguous elements per row, `outer` rows, row pitch
 // `pitch_elems`; box {box_inner, box_outer}; 128-byte swizzle.
 tf_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
-                   uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer, bool f32 = false) {
+                   uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer, bool f32 = false,
+                   bool swizzle = true) {
   EncodeFn enc = encode_fn();
   if (!enc) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {inner, outer};
@@ -999,7 +1098,8 @@ tf_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t ou
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                    const_cast<void*>(base), dims, strides, box,
-                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                    l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
@@ -1318,10 +1418,14 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
     if (gathered && gathered[r]) return static_cast<__nv_bfloat16*>(gathered[r]);
     return reinterpret_cast<__nv_bfloat16*>(w->ptr(r, inbox_off)) + size_t(parity) * m * k;
   };
+  // PUSH on the TMA producer (W <= 8): peers' inboxes only -- like pull, a
+  // rank's own block is read in place from its shard (unless the caller
+  // asked for the gathered operand in its own buffer).
+  const bool tma_push = variant == TF_AG_PUSH && W <= kPushMaxW && !std::getenv("TFB_PUSH_LSU");
   if (!lay.inbox_complete)
     for (int r = 0; r < W; ++r)
       for (int s = 0; s < W; ++s)
-        w->ag_src[r][s] = (variant == TF_AG_PULL && s == r && !(gathered && gathered[r]))
+        w->ag_src[r][s] = ((variant == TF_AG_PULL || tma_push) && s == r && !(gathered && gathered[r]))
                               ? World::AgBlock{a_shard[r], msh ? k : kw}  // read in place by the TMA producer
                               : World::AgBlock{inbox_of(r) + (msh ? size_t(s) * mr * k : size_t(s) * kw), k};
   auto ready_of = [&](int r) { return reinterpret_cast<uint64_t*>(w->ptr(r, rb.offset)); };
@@ -1426,7 +1530,20 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
   for (int r = 0; r < W; ++r)
     if (w->ranks[r].local) ++per_dev[w->ranks[r].device];
   // 16 producer CTAs per device, split among the ranks sharing it.
-  auto push_ctas_of = [&](int r) { return std::max(2u, 16u / per_dev[w->ranks[r].device]); };
+  // TMA producer (W <= 8): a few one-warp CTAs per device; the register-copy
+  // producer (TFB_PUSH_LSU, or W > 8): 16.
+  // Producer CTAs: TMA, 4 per rank (a TMA store engine moves ~62 GB/s per SM,
+  // tools/micro_tma_store.cu; a rank's GEMM consumes its A at well under
+  // 200 GB/s, so 4 keep ahead of it -- loopback W = 8 config 2: 8 / 16 / 24
+  // / 32 CTAs per device 5378 / 4062 / 3697 / 3580 us); register copy, 16 per
+  // device.  TFB_PUSH_CTAS: CTAs per device.
+  unsigned push_total = 0;
+  if (const char* e = std::getenv("TFB_PUSH_CTAS")) push_total = unsigned(std::max(1, std::atoi(e)));
+  auto push_ctas_of = [&](int r) {
+    const unsigned n = per_dev[w->ranks[r].device];
+    if (tma_push) return push_total ? std::max(1u, push_total / n) : 4u;
+    return std::max(2u, (push_total ? push_total : 16u) / n);
+  };
   for (int r = 0; r < W; ++r) {
     if (!w->ranks[r].local) continue;
     cudaSetDevice(w->ranks[r].device);
@@ -1451,7 +1568,41 @@ tf_status ag_bf16_run(World* w, tf_ag_variant variant, const tf_ag_shape& sh, vo
     pp.mpr = int(mr / BM);
     pp.ctr = ctr_of(r, 1);
     for (int d = 0; d < W; ++d) pp.events[d] = events_of(d);
-    ag_push_kernel<<<push_ctas_of(r), 512, 0, w->ranks[r].side>>>(pp);
+    if (tma_push) {
+      PushMaps maps{};
+      PushTmaParams tp{};
+      const size_t cols = msh ? k : kw;
+      tp.box_c = cols % 256 == 0 ? 256 : cols % 128 == 0 ? 128 : 64;
+      tp.box_r = std::min(BM, 16384 / tp.box_c);
+      tp.cols = int(cols);
+      TFB_CHECK(make_map(&maps.src, a_shard[r], cols, msh ? mr : m, cols, uint32_t(tp.box_c), uint32_t(tp.box_r),
+                         false, false));
+      for (int d = 0; d < W; ++d) {
+        TFB_CHECK(make_map(&maps.dst[d], inbox_of(d), k, m, k, uint32_t(tp.box_c), uint32_t(tp.box_r), false, false));
+        tp.ready[d] = ready_of(d);
+        tp.events[d] = events_of(d);
+      }
+      tp.W = W;
+      tp.self = r;
+      tp.nmb = msh ? int(mr / BM) : num_m;
+      tp.msharded = msh;
+      tp.mpr = int(mr / BM);
+      tp.M = int(m);
+      tp.local = 1;
+      for (int d = 0; d < W; ++d)
+        if (!w->ranks[d].local || w->ranks[d].device != w->ranks[r].device) tp.local = 0;
+      if (std::getenv("TFB_PUSH_SYS")) tp.local = 0;
+      tp.skip_self = !(gathered && gathered[r]);
+      tp.ctr = ctr_of(r, 1);
+      const int smem = kPushStages * tp.box_c * tp.box_r * 2;
+      static std::atomic<bool> push_attr[64];
+      if (!push_attr[w->ranks[r].device & 63].exchange(true))
+        TFB_CUDA(cudaFuncSetAttribute(ag_push_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kPushStages * 32768));
+      ag_push_tma_kernel<<<push_ctas_of(r), 32, smem, w->ranks[r].side>>>(maps, tp);
+    } else {
+      ag_push_kernel<<<push_ctas_of(r), 512, 0, w->ranks[r].side>>>(pp);
+    }
     TFB_CUDA(cudaGetLastError());
     ++w->launches;
   }

@@ -1,7 +1,6 @@
-"""Loopback AG+GEMM probe: W ranks on ONE GPU (each its own heap), config-2
-shapes (M=8192, K=8192, N=28672/W per rank).  Total FLOPs equal W=1's, so the
-time over the W=1 kernel is the cost of the fused exchange machinery (gather
-warps / push kernel, flags, gated TMA) -- with HBM standing in for NVLink."""
+"""Push-producer throughput probe (loopback W ranks on one GPU): config-2 A
+(M=8192, K=8192) with a tiny per-rank N, so the time is the exchange, not
+the GEMM.  python tools/probe_push.py [W ...]; env TFB_PUSH_CTAS."""
 import ctypes as C
 import os
 import sys
@@ -12,9 +11,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2511_02168_b200 as tf  # noqa: E402
 from paper_2511_02168_b200 import _abi  # noqa: E402
 
-M, K, NT = 8192, 8192, 28672
-for W in [int(x) for x in (sys.argv[1:] or ["1", "2", "4", "8"])]:
-    N, kw = NT // W, K // W
+M, K = 8192, 8192
+N = int(os.environ.get("N", "256"))
+for W in [int(x) for x in (sys.argv[1:] or ["2", "8"])]:
+    kw = K // W
     with tf.World(W, [0] * W, M * kw * 2 + 2 * 2 * M * K * 2 + (64 << 20)) as w:
         shards = w.alloc("ag.a", M * kw * 2)
         A = (torch.rand(M, K, device="cuda") * 2 - 1).bfloat16()
@@ -23,12 +23,8 @@ for W in [int(x) for x in (sys.argv[1:] or ["1", "2", "4", "8"])]:
             w.memcpy(shards[r], s.data_ptr(), s.numel() * 2)
         Bs = [(torch.rand(K, N, device="cuda") * 2 - 1).bfloat16() for _ in range(W)]
         Cs = [torch.empty(M, N, device="cuda", dtype=torch.bfloat16) for _ in range(W)]
-        torch.cuda.synchronize()
         shape = _abi.AgShape(M, N, K, 0, 0, 0, 1)
-        only = os.environ.get("VARS")
-        for name, var in (("pull", 1), ("push", 2), ("baseline", 0)):
-            if only and name not in only.split(","):
-                continue
+        for name, var in (("pull", 1), ("push", 2)):
             args = (w.handle, var, C.byref(shape), _abi.ptr_array(shards),
                     _abi.ptr_array([b.data_ptr() for b in Bs]), _abi.ptr_array([c.data_ptr() for c in Cs]),
                     None, None)
@@ -37,11 +33,15 @@ for W in [int(x) for x in (sys.argv[1:] or ["1", "2", "4", "8"])]:
             err = ((Cs[0][:256].float() - ref).abs().max() / ref.abs().max()).item()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
+            w.tax_reset()
             e0.record()
             for _ in range(5):
                 _abi.check(w.lib.tf_ag_gemm(*args))
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / 5
-            print(f"W={W} {name:8s} {ms*1e3:8.1f} us  {2*M*NT*K/ms/1e9:7.1f} TFLOP/s (all ranks)  err {err:.2e}",
+            moved = W * M * K * 2  # every rank's inbox receives all of A
+            print(f"W={W} N={N} {name:5s} {ms*1e3:8.1f} us  exchange {moved/ms/1e6:7.1f} GB/s into inboxes  err {err:.2e}",
                   flush=True)
+            if os.environ.get("TAXES"):
+                print("   rank0 taxes:", w.taxes(0), flush=True)
