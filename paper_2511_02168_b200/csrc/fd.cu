@@ -94,6 +94,8 @@ struct FdParams {
   unsigned int* ctr;          // [0] compute, [1] fold, [2] done
   unsigned int* sfc;          // [nlocal] split-fold sub-item counters
   int hc;                     // heads per split-fold sub-item
+  int fold_once;              // every CTA's first split-fold claim covers all sub-items:
+                              // a CTA folds at most one and skips the re-claim
   int interleave;             // fast split: the CTA's warps interleave 16-key tiles
   uint64_t local_dst;         // bit dst: dst's inbox/flags live on this launch's device
   int push;                   // push rank partials to every inbox (+ signal)
@@ -1265,6 +1267,12 @@ __device__ __forceinline__ void fd_post_phases_body(const FdParams& P, unsigned 
   auto stamp = [&](int i) {
     if (tr && threadIdx.x == 0) tr[i] = globaltimer_ns();
   };
+  // direct + fold_once: a folding CTA counts itself out (ctr[2]) as soon as
+  // its group's splits have landed -- its last read of any per-launch
+  // counter -- and reads the ticket only after its fold, so the exit count's
+  // round trip overlaps the fold instead of following it.
+  unsigned exit_ticket = 0;  // thread 0: old ctr[2] + 1 (0: not counted yet)
+  bool counted = false;
   // Split-fold phase: sub-items (group, hc heads) of every local rank this
   // CTA computed for, each waiting for its group's S splits.  Every compute
   // item has been claimed by a CTA that never blocks before publishing it,
@@ -1278,9 +1286,10 @@ __device__ __forceinline__ void fd_post_phases_body(const FdParams& P, unsigned 
     const int nhc = P.gs / P.hc;
     const unsigned nsub = unsigned(G) * nhc;
     int lr = 0;
+    bool folded = false;
     for (;;) {
       while (lr < P.nlocal && !((ranks_mask >> lr) & 1u)) ++lr;
-      if (lr >= P.nlocal) break;
+      if (lr >= P.nlocal || (folded && P.fold_once)) break;  // fold_once: no claim round trip on the way out
       __syncthreads();
       if (threadIdx.x == 0) s_item = atomicAdd(&P.sfc[lr], 1u);
       __syncthreads();
@@ -1291,6 +1300,7 @@ __device__ __forceinline__ void fd_post_phases_body(const FdParams& P, unsigned 
         continue;
       }
       const int hb = item % nhc, g = item / nhc;
+      folded = true;
       stamp(13);
       if (threadIdx.x == 0) {
         // Intra-rank completion counter: a local spin, not a fabric signal
@@ -1321,6 +1331,10 @@ __device__ __forceinline__ void fd_post_phases_body(const FdParams& P, unsigned 
       if (s_last == 2) continue;
       if (!s_last) break;  // an error elsewhere (e.g. NumericError) ends the launch
       stamp(9);
+      if (P.direct && P.fold_once) {
+        if (threadIdx.x == 0) exit_ticket = atomicAdd(&P.ctr[2], 1u) + 1u;
+        counted = true;
+      }
       if (P.d == 128) fold_heads128(P, lr, g, hb * P.hc, P.hc, s_wm, s_fL, s_fO);
       else if (P.d <= 128) fold_heads<4, 8>(P, lr, g, hb * P.hc, P.hc, s_wm, s_fL, s_fO);
       else fold_heads<8, 4>(P, lr, g, hb * P.hc, P.hc, s_wm, s_fL, s_fO);
@@ -1422,8 +1436,12 @@ __device__ __forceinline__ void fd_post_phases_body(const FdParams& P, unsigned 
   // epoch-valued count would fall behind when schedules are mixed.
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    s_last = atomicAdd(&P.ctr[2], 1u) == gridDim.x - 1;
+    if (counted) {
+      s_last = exit_ticket == gridDim.x;
+    } else {
+      __threadfence();
+      s_last = atomicAdd(&P.ctr[2], 1u) == gridDim.x - 1;
+    }
   }
   __syncthreads();
   if (s_last) {
@@ -2528,6 +2546,8 @@ static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape
             attr[hilo][kv.first & 63].store(true);
           }
           const unsigned grid = std::max(1u, std::min(Q.nitems, unsigned(w->sm_count)));
+          Q.fold_once = Q.nlocal == 1 && Q.nitems >= grid && unsigned(G) * unsigned(Q.gs / Q.hc) <= grid &&
+                        !std::getenv("TFB_FD_REFOLD");
           cudaLaunchConfig_t lc{};
           cudaLaunchAttribute la[1];
           lc.gridDim = dim3(grid);
@@ -2562,6 +2582,10 @@ static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kFastThreads, 0);
         const unsigned grid =
             std::max(1u, std::min(items, unsigned(std::max(per_sm, 1) * w->sm_count)));
+        // Every CTA computes an item (items >= grid), so every CTA enters the
+        // split fold and the first claims cover all nsub sub-items.
+        Q.fold_once = Q.nlocal == 1 && items >= grid && unsigned(G) * unsigned(Q.gs / Q.hc) <= grid &&
+                      !std::getenv("TFB_FD_REFOLD");
         cudaLaunchConfig_t lc{};
         cudaLaunchAttribute la[1];
         lc.gridDim = dim3(grid);
