@@ -277,7 +277,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                          const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC,
                          const __grid_constant__ CUtensorMap tmB4, const AgTcParams p) {
-  pdl_begin();
+  pdl_launch();
+  if (p.dbg & 65536) pdl_wait();  // A/B knob: wait at entry (round-2 placement)
   using K_ = Cfg<CG, NH_>;
   constexpr int STAGES = K_::STAGES, NH = K_::NH, CPH = K_::CPH;
   extern __shared__ uint8_t smem_raw[];
@@ -360,6 +361,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // the predecessor's writes (A, B, flags, C, counters) are visible from here on
   // Profiling (TFB_DEBUG & 4096): %globaltimer phase stamps of CTA 0, printed at exit.
   __shared__ unsigned long long s_ts[12];
   __shared__ unsigned long long s_kp[24], s_km[24];  // TFB_DEBUG 8192: producer / MMA per-k-block stamps
