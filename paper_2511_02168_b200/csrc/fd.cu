@@ -1615,6 +1615,14 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(sm100::smem_u32(bar)), "l"(pol)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2, int c3, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3, %4, %5}], [%6], %7;" ::"r"(sm100::smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(sm100::smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    sm100::smem_u32(dst)),
@@ -1665,6 +1673,12 @@ __device__ void stream_producer(const FdParams& P, const FdMaps& M, StreamSmem& 
       while (globaltimer_ns() - t0 < P.r[lr].skew_ns) __nanosleep(1000);
       skewed |= 1u << lr;
     }
+    // Paged KV (page_size >= 64, so a 64-key stage never crosses a page):
+    // the stage's page comes from the batch's block table; the next slot's
+    // entry is loaded when a slot is entered, so the table read is off the
+    // issue chain except at an item's first stage.
+    const int* tbl = P.paged && !end ? P.r[lr].pages + size_t(b) * P.pps : nullptr;
+    int cslot = -1, cpg = 0, nslot = -1, npg = 0;
     for (unsigned key = e.z;; key += kStageKeys) {
       if (!end && key >= e.w) break;
       const int st = int(seq % kStreamStages);
@@ -1681,8 +1695,33 @@ __device__ void stream_producer(const FdParams& P, const FdMaps& M, StreamSmem& 
       }
       const bool first = key == e.z;
       sm100::mbar_arrive_expect_tx(&sm.full[st], kStageKV + (first ? 2048u : 0u));
-      tma_load_3d(sm.kv[st], &M.k[lr], &sm.full[st], 0, int(row0 + key), 0, pol);
-      tma_load_3d(sm.kv[st] + kStageKV / 2, &M.v[lr], &sm.full[st], 0, int(row0 + key), 0, pol);
+      if (tbl) {
+        const int slot = int(key >> P.page_shift);
+        if (slot != cslot) {
+          cpg = slot == nslot ? npg : __ldg(tbl + slot);
+          cslot = slot;
+          nslot = slot + 1;
+          npg = nslot < P.pps ? __ldg(tbl + nslot) : 0;
+          if (unsigned(cpg) >= unsigned(P.num_pages)) {
+            raise_err(P.err, TF_ERR_SHAPE, kPage, P.r[lr].rank, -1, b, slot, uint64_t(P.num_pages),
+                      uint64_t(unsigned(cpg)), 0);
+            cpg = 0;
+          }
+        }
+        const int in_page = int(key & ((1u << P.page_shift) - 1u));
+        if (P.hnd) {  // [pages][Hkv][page][d]: one row range per (page, kv head)
+          const int row = ((cpg * P.Hkv + kvh) << P.page_shift) + in_page;
+          tma_load_3d(sm.kv[st], &M.k[lr], &sm.full[st], 0, row, 0, pol);
+          tma_load_3d(sm.kv[st] + kStageKV / 2, &M.v[lr], &sm.full[st], 0, row, 0, pol);
+        } else {  // [pages][page][Hkv][d]: key rows Hkv * 256 B apart
+          const int krow = (cpg << P.page_shift) + in_page;
+          tma_load_4d(sm.kv[st], &M.k[lr], &sm.full[st], 0, krow, kvh, 0, pol);
+          tma_load_4d(sm.kv[st] + kStageKV / 2, &M.v[lr], &sm.full[st], 0, krow, kvh, 0, pol);
+        }
+      } else {
+        tma_load_3d(sm.kv[st], &M.k[lr], &sm.full[st], 0, int(row0 + key), 0, pol);
+        tma_load_3d(sm.kv[st] + kStageKV / 2, &M.v[lr], &sm.full[st], 0, int(row0 + key), 0, pol);
+      }
       if (first) {
         bulk_load(sm.q[st], static_cast<const __nv_bfloat16*>(P.r[lr].q) + (size_t(b) * P.Hq + kvh * 8) * 128, 2048,
                   &sm.full[st]);
@@ -2108,6 +2147,24 @@ static tf_status fd_kv_map(CUtensorMap* m, const void* base, size_t rows) {
   return TF_OK;
 }
 
+// Paged NHD pool [pages][page][Hkv][d] as [key rows][Hkv][2 halves][64 d]
+// with the key dimension second, so a box lands in smem exactly like the
+// contiguous map's [2 halves][64 keys][64 d].
+static tf_status fd_kv_map_nhd(CUtensorMap* m, const void* base, size_t key_rows, int hkv) {
+  FdEncodeFn enc = fd_encode_fn();
+  if (!enc) return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {64, key_rows, cuuint64_t(hkv), 2};
+  cuuint64_t strides[3] = {cuuint64_t(hkv) * 256, 256, 128};
+  cuuint32_t box[4] = {64, uint32_t(kStageKeys), 1, 2};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(TF_ERR_CUDA, "cuTensorMapEncodeTiled (paged NHD K/V) failed (" + std::to_string(int(r)) + ")");
+  return TF_OK;
+}
+
 // Item table of fd_stream_kernel: a fixed function of the shape and the
 // grid, so every run cuts the same splits (bitwise-reproducible partials
 // whatever CTA computes them).  Guided sizes: each item takes
@@ -2266,7 +2323,14 @@ static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape
   const bool fast = fast_ok(sh);
   // TMA-fed kernel (fd_stream_kernel) with a guided item table, else the
   // register-streaming kernel with S equal splits per group.
-  const bool stream = !paged && fd_stream_ok(sh, w, q, k_shard, v_shard);  // paged: register kernel
+  // Paged KV streams through the TMA kernel when a 64-key stage stays in one
+  // page (page_size >= 64) and the pool's rows fit int32 coordinates;
+  // smaller pages use the register kernel's per-tile lookups.
+  const bool paged_stream_ok =
+      !paged || (paged->page_size >= int(kStageKeys) &&
+                 size_t(paged->num_pages) * size_t(paged->page_size) * size_t(sh.kv_heads) < (size_t(1) << 31) &&
+                 !std::getenv("TFB_FD_PAGED_REGISTER"));
+  const bool stream = paged_stream_ok && fd_stream_ok(sh, w, q, k_shard, v_shard);
   // The plan is a function of (G, len, grid, knobs): built and uploaded
   // once per geometry; later calls only need its size and split count.
   FdPlan plan;
@@ -2533,9 +2597,16 @@ static tf_status fd_async(tf_world* tw, tf_fd_variant variant, const tf_fd_shape
           FdMaps maps{};
           for (int i = 0; i < Q.nlocal; ++i) {
             const int r = rs[c0 + i];
-            const size_t rows = size_t(sh.batch) * sh.kv_heads * len;
-            TFB_CHECK(fd_kv_map(&maps.k[i], k_shard[r], rows));
-            TFB_CHECK(fd_kv_map(&maps.v[i], v_shard[r], rows));
+            if (paged && paged->layout == TF_PAGED_NHD) {
+              const size_t krows = size_t(paged->num_pages) * size_t(paged->page_size);
+              TFB_CHECK(fd_kv_map_nhd(&maps.k[i], k_shard[r], krows, sh.kv_heads));
+              TFB_CHECK(fd_kv_map_nhd(&maps.v[i], v_shard[r], krows, sh.kv_heads));
+            } else {
+              const size_t rows = paged ? size_t(paged->num_pages) * size_t(paged->page_size) * sh.kv_heads
+                                        : size_t(sh.batch) * sh.kv_heads * len;
+              TFB_CHECK(fd_kv_map(&maps.k[i], k_shard[r], rows));
+              TFB_CHECK(fd_kv_map(&maps.v[i], v_shard[r], rows));
+            }
           }
           const void* kfn = hilo ? reinterpret_cast<const void*>(fd_stream_kernel<true>)
                                  : reinterpret_cast<const void*>(fd_stream_kernel<false>);

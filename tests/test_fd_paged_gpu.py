@@ -91,3 +91,26 @@ def test_paged_layout_validation():
     p = tf.fd.make_problem(2, 2, 16, 256)
     with pytest.raises(tf.ConfigError, match="power of two"):
         tf.fd.run_fused(p, tf.WorldConfig(world_size=1), paged=tf.fd.PagedLayout(page_size=24))
+
+
+@pytest.mark.parametrize("W", [1, 2])
+@pytest.mark.parametrize("page_size", [64, 256])
+@pytest.mark.parametrize("hnd", [False, True])
+def test_paged_stream_kernel_equals_contiguous(monkeypatch, W, page_size, hnd):
+    # TFB_FD_STREAM=1: the TMA-fed stream kernel for both runs (pages >= 64
+    # keys: one TMA box per 64-key stage, HND as a 3-D map over the pool,
+    # NHD as a 4-D one with the key rows Hkv * 256 B apart)
+    monkeypatch.setenv("TFB_FD_STREAM", "1")
+    p = gqa_problem(9, batch=3, kv_len=W * 1000, heads=16, kv_heads=2)
+    lay = tf.fd.PagedLayout(page_size=page_size, spare_pages=5, seed=11, hnd=hnd)
+    for variant in (V.kFused, V.kBsp):
+        cfg = tf.WorldConfig(world_size=W)
+        base = tf.fd.run_fd(p, variant, cfg, dtype=_abi.TF_BF16, out_dtype=_abi.TF_BF16)
+        pg = tf.fd.run_fd(p, variant, cfg, dtype=_abi.TF_BF16, out_dtype=_abi.TF_BF16, paged=lay)
+        for r in range(W):
+            assert same(pg.out[r], base.out[r]), (variant, W, page_size, hnd, r)
+        assert not np.isnan(pg.out[0]).any()
+    # ... and a bad table entry is still a ShapeError from the stream kernel
+    with pytest.raises(tf.ShapeError, match="outside the pool"):
+        tf.fd.run_fused(p, tf.WorldConfig(world_size=1), dtype=_abi.TF_BF16, out_dtype=_abi.TF_BF16,
+                        paged=tf.fd.PagedLayout(page_size=page_size, hnd=hnd), bad_page=True)
