@@ -94,6 +94,7 @@ struct AgTcParams {
   uint64_t watchdog_ns;
   DevErr* err;
   int board;
+  int xchg_lsu;  // split-K L2 exchange: outgoing slices stored by every thread (else one TMA bulk store each)
   int dbg;  // TFB_DEBUG knobs: 1 skip C stores, 2 skip MMAs, 8 force CG=1, 16 skip the split-K reduce,
            // 32 poll-wait the epilogue, 64 skip the epilogue, 256 skip A loads, 512 skip B loads,
            // 4096 print CTA 0's phase stamps (profiling aids)
@@ -141,6 +142,19 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 // shared::cluster address of `p` (a local smem object) in CTA `rank`.
+// Explicit shared-window accesses for the split-K dump and sum: through a
+// generic pointer (the 1 KB-aligned dynamic smem base loses its state
+// space) they compiled to generic LD.E / ST.E.
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ float4 lds128f(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a)
+               : "memory");
+  return v;
+}
 __device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
@@ -268,6 +282,67 @@ __device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr) {
                  : "memory");
   else
     tmem_dealloc(taddr, TMEM_COLS);
+}
+
+// Split-K sum (see the kernel): CTA ks owns rows [ks*rows_per, +rows_per)
+// of the tile's 128; sibling s2's partial of them sits in R's slice s2
+// (L2 route) or in sibling s2's own R (DSMEM route, cluster rank
+// prank + CG * s2).  Task (row, g): 16-byte chunks g and g + 32 of the
+// row (columns 4g..4g+3, 128+4g..), so a quarter-warp reads 8 consecutive
+// chunks -- conflict-free under the XOR swizzle.  Ascending s2 order.
+struct SumArgs {
+  uint32_t R;  // this CTA's R (shared window)
+  int ks, rows_per, row_base, col_base, prank, CG;
+};
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+template <int S, bool L2>
+__device__ __forceinline__ void splitk_sum(const SumArgs& a, const AgTcParams& p) {
+  const int tasks = a.rows_per * 32;
+  uint32_t src[S];
+#pragma unroll
+  for (int s2 = 0; s2 < S; ++s2) src[s2] = L2 ? 0u : mapa_u32(a.R, uint32_t(a.prank + a.CG * s2));
+  for (int e = threadIdx.x; e < tasks; e += NUM_THREADS) {
+    const int rl = a.ks * a.rows_per + e / 32, g = e % 32;
+    const int grow = a.row_base + rl, gcol = a.col_base + g * 4;
+    const uint32_t off0 = uint32_t(rl * 1024 + ((g ^ (rl & 7)) * 16));
+    const uint32_t off1 = uint32_t(rl * 1024 + (((g + 32) ^ (rl & 7)) * 16));
+    float4 x[S], y[S];
+#pragma unroll
+    for (int s2 = 0; s2 < S; ++s2) {
+      if (L2) {  // sibling s2's copy sits in slice position s2 of R
+        const uint32_t b = a.R + uint32_t((s2 - a.ks) * a.rows_per * 1024);
+        x[s2] = lds128f(b + off0);
+        y[s2] = lds128f(b + off1);
+      } else if (s2 == a.ks) {
+        x[s2] = lds128f(a.R + off0);
+        y[s2] = lds128f(a.R + off1);
+      } else {  // sibling s2's R: same offset in its window
+        const uint32_t rb = src[s2];
+        asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(x[s2].x), "=f"(x[s2].y), "=f"(x[s2].z), "=f"(x[s2].w) : "r"(rb + off0));
+        asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(y[s2].x), "=f"(y[s2].y), "=f"(y[s2].z), "=f"(y[s2].w) : "r"(rb + off1));
+      }
+    }
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int s2 = 0; s2 < S; ++s2) {
+      acc[0] += x[s2].x; acc[1] += x[s2].y; acc[2] += x[s2].z; acc[3] += x[s2].w;
+      acc[4] += y[s2].x; acc[5] += y[s2].y; acc[6] += y[s2].z; acc[7] += y[s2].w;
+    }
+    if (grow < p.M && !(p.dbg & 1)) {
+      __nv_bfloat16* crow = p.C + size_t(grow) * p.ldc;
+      if (gcol < p.N)
+        *reinterpret_cast<uint2*>(crow + gcol) = make_uint2(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]));
+      if (gcol + 128 < p.N)
+        *reinterpret_cast<uint2*>(crow + gcol + 128) =
+            make_uint2(pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+    }
+  }
 }
 
 template <int CG, int NH_>
@@ -632,7 +707,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           pk.y = pack_bf16x2(__uint_as_float(src[2]), __uint_as_float(src[3]));
           pk.z = pack_bf16x2(__uint_as_float(src[4]), __uint_as_float(src[5]));
           pk.w = pack_bf16x2(__uint_as_float(src[6]), __uint_as_float(src[7]));
-          *reinterpret_cast<uint4*>(buf + lane * 128 + ((j ^ (lane & 7)) * 16)) = pk;
+          sts128(smem_u32(buf) + uint32_t(lane * 128 + ((j ^ (lane & 7)) * 16)), pk);
         }
         fence_proxy_async_shared();
         __syncwarp();
@@ -758,8 +833,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int c = cc * 8 + j;  // 16-byte chunk of the 256-column row
-            *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(R) + row * 1024 + ((c ^ (row & 7)) * 16)) =
-                make_uint4(r0[4 * j], r0[4 * j + 1], r0[4 * j + 2], r0[4 * j + 3]);
+            sts128(smem_u32(R) + uint32_t(row * 1024 + ((c ^ (row & 7)) * 16)),
+                   make_uint4(r0[4 * j], r0[4 * j + 1], r0[4 * j + 2], r0[4 * j + 3]));
           }
         }
       }
@@ -776,7 +851,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint8_t* wsme = p.ws + (size_t(blockIdx.x) * NH + h) * (size_t(BM) * 1024);
         fence_proxy_async_shared();
         named_bar(2, NUM_THREADS);
-        if (threadIdx.x == 0) {
+        if (p.xchg_lsu) {
+          // Every thread copies 16-byte words of the outgoing slices (raw
+          // bytes, layout kept); the cluster barrier's release orders them
+          // before the siblings' loads -- no TMA-store drain on the chain.
+          for (int j = 0; j < S; ++j) {
+            if (j == ks) continue;
+            const uint4* from = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(R) + j * slice);
+            uint4* to = reinterpret_cast<uint4*>(wsme + j * slice);
+            for (int v = threadIdx.x; v < int(slice / 16); v += NUM_THREADS) __stcg(to + v, from[v]);
+          }
+          if (threadIdx.x == 0) mbar_arrive_expect_tx(rbar, slice * uint32_t(S - 1));
+        } else if (threadIdx.x == 0) {
           for (int j = 0; j < S; ++j) {
             if (j == ks) continue;
             asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(wsme + j * slice),
@@ -808,50 +894,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         cluster_sync();
       }
       if (tsd && threadIdx.x == 0 && h == 0) s_ts[4] = globaltimer_ns();  // partials exchanged
-      uint32_t src[8];
-#pragma unroll
-      for (int s2 = 0; s2 < 8; ++s2)
-        if (s2 < S) src[s2] = mapa(R, prank + uint32_t(CG * s2));
-      const int tasks = (p.dbg & 16) ? 0 : rows_per * 32;  // 8-column groups per row: 32
-      for (int e = threadIdx.x; e < tasks; e += NUM_THREADS) {
-        const int rl = ks * rows_per + e / 32, g = e % 32;
-        const int grow = row_base + rl, gcol = nb * K_::BN_TILE + h * 256 + g * 8;
-        const uint32_t off0 = uint32_t(rl * 1024 + (((2 * g) ^ (rl & 7)) * 16));
-        const uint32_t off1 = uint32_t(rl * 1024 + (((2 * g + 1) ^ (rl & 7)) * 16));
-        // All 2*S remote loads in flight first, then the ascending sum.
-        float4 x[8], y[8];
-#pragma unroll
-        for (int s2 = 0; s2 < 8; ++s2) {
-          if (s2 < S && p.ws) {  // sibling s2's copy sits in slice position s2 of R
-            const uint8_t* b = reinterpret_cast<const uint8_t*>(R) + (s2 - ks) * rows_per * 1024;
-            x[s2] = *reinterpret_cast<const float4*>(b + off0);
-            y[s2] = *reinterpret_cast<const float4*>(b + off1);
-          } else if (s2 == ks) {  // this CTA's own copy: a local smem load
-            x[s2] = *reinterpret_cast<const float4*>(reinterpret_cast<const uint8_t*>(R) + off0);
-            y[s2] = *reinterpret_cast<const float4*>(reinterpret_cast<const uint8_t*>(R) + off1);
-          } else if (s2 < S) {
-            asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-                         : "=f"(x[s2].x), "=f"(x[s2].y), "=f"(x[s2].z), "=f"(x[s2].w) : "r"(src[s2] + off0));
-            asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-                         : "=f"(y[s2].x), "=f"(y[s2].y), "=f"(y[s2].z), "=f"(y[s2].w) : "r"(src[s2] + off1));
-          }
-        }
-        float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-        for (int s2 = 0; s2 < 8; ++s2) {
-          if (s2 < S) {
-            a[0] += x[s2].x; a[1] += x[s2].y; a[2] += x[s2].z; a[3] += x[s2].w;
-            a[4] += y[s2].x; a[5] += y[s2].y; a[6] += y[s2].z; a[7] += y[s2].w;
-          }
-        }
-        if (grow < p.M && gcol < p.N && !(p.dbg & 1)) {
-          uint4 o;
-          o.x = pack_bf16x2(a[0], a[1]);
-          o.y = pack_bf16x2(a[2], a[3]);
-          o.z = pack_bf16x2(a[4], a[5]);
-          o.w = pack_bf16x2(a[6], a[7]);
-          *reinterpret_cast<uint4*>(p.C + size_t(grow) * p.ldc + gcol) = o;
-        }
+      // The owned rows' ascending S-way sum and bf16 C stores, specialised
+      // on S and the exchange route: the generic loop's per-sibling branches
+      // made it instruction-bound at 10 warps (~650 cycles per 320 tasks,
+      // 2.6 us of the M = 256 tail; clock64 per warp, TFB_DEBUG 4096).
+      if (!(p.dbg & 16)) {
+        const SumArgs sa{smem_u32(R), ks, rows_per, row_base, nb * K_::BN_TILE + h * 256, int(prank), CG};
+        const bool l2 = p.ws != nullptr;
+        if (S == 2) l2 ? splitk_sum<2, true>(sa, p) : splitk_sum<2, false>(sa, p);
+        else if (S == 4) l2 ? splitk_sum<4, true>(sa, p) : splitk_sum<4, false>(sa, p);
+        else l2 ? splitk_sum<8, true>(sa, p) : splitk_sum<8, false>(sa, p);
       }
       if (tsd && threadIdx.x == 0) s_ts[5 + h] = globaltimer_ns();  // half h summed + stored
       if (p.ws) named_bar(2, NUM_THREADS);  // R fully read before the next half's dump
@@ -1148,6 +1200,7 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   if (const char* e = std::getenv("TFB_DEBUG")) p.dbg = std::atoi(e);
   if (const char* e = std::getenv("TFB_L2HINT")) p.l2hint = std::atoi(e);
   p.one_producer = std::getenv("TFB_ONE_PRODUCER") ? 1 : 0;
+  p.xchg_lsu = std::getenv("TFB_SPLITK_LSU") ? 1 : 0;
   const int dev = w->ranks[r].device;
   cudaSetDevice(dev);
   // Kernel shapes: CTA pairs (cta_group::2) with 256 x 512 tiles whenever
