@@ -851,6 +851,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint8_t* wsme = p.ws + (size_t(blockIdx.x) * NH + h) * (size_t(BM) * 1024);
         fence_proxy_async_shared();
         named_bar(2, NUM_THREADS);
+        if (tsd && threadIdx.x == 0 && h == 0) s_ts[8] = globaltimer_ns();  // partial dumped
         if (p.xchg_lsu) {
           // Every thread copies 16-byte words of the outgoing slices (raw
           // bytes, layout kept); the cluster barrier's release orders them
@@ -871,10 +872,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           bulk_commit();
           bulk_wait_all();
+          if (tsd && h == 0) s_ts[9] = globaltimer_ns();  // slices in L2
           asm volatile("fence.proxy.async.global;" ::: "memory");
           mbar_arrive_expect_tx(rbar, slice * uint32_t(S - 1));
         }
         cluster_sync();
+        if (tsd && threadIdx.x == 0 && h == 0) s_ts[10] = globaltimer_ns();  // cluster synced
         if (threadIdx.x == 0) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
           const int cta0 = int(blockIdx.x) - int(crank);  // cluster's first CTA
@@ -925,9 +928,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   if (tsd && threadIdx.x == 0) {
     auto rel = [&](int i) { return s_ts[i] ? (long long)(s_ts[i] - s_ts[0]) : -1ll; };
-    printf("[ag cta0 CG=%d NH=%d S=%d] first-stage %lld last-commit %lld tfull %lld exchanged %lld "
-           "sum0 %lld sum1 %lld epilogue %lld exit %lld ns\n", CG, NH, p.ksplit, rel(1), rel(2), rel(3), rel(4),
-           rel(5), rel(6), rel(7), (long long)(globaltimer_ns() - s_ts[0]));
+    printf("[ag cta0 CG=%d NH=%d S=%d] first-stage %lld last-commit %lld tfull %lld dumped %lld inl2 %lld "
+           "synced %lld exchanged %lld sum0 %lld sum1 %lld epilogue %lld exit %lld ns\n", CG, NH, p.ksplit, rel(1),
+           rel(2), rel(3), rel(8), rel(9), rel(10), rel(4), rel(5), rel(6), rel(7),
+           (long long)(globaltimer_ns() - s_ts[0]));
   }
   if (warp == 1) {
     __syncwarp();
@@ -1342,11 +1346,12 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   grid = std::max(grid, unsigned(CG));
   if (p.ksplit > 1) grid = pair_tiles * CG;  // exactly one item per CTA (the reduction aliases its smem)
   p.ws = nullptr;
-  // Split-K partials cross through L2 (bulk copies) for one-half tiles:
-  // measured 35.7 vs 37.7 us at M = 128 (tools/ab_gemm.py, TFB_SPLITK_DSMEM
-  // A/B); two-half tiles pay the copy-then-barrier latency chain twice and
-  // lose ~2 us at M = 512, so they keep the DSMEM path.
-  if (p.ksplit > 1 && (shp->NH == 1 || std::getenv("TFB_SPLITK_L2")) && !std::getenv("TFB_SPLITK_DSMEM")) {
+  // Split-K partials are summed straight from the siblings' smem (DSMEM)
+  // since the sum loop was specialised on S (M = 128 / 256: 30.0 / 37.2 us
+  // vs 32.5 / 38.1 through L2 bulk copies, tools/skinny_ab.py; before it the
+  // branchy generic loop made the L2 route the faster one).  The L2
+  // exchange (TFB_SPLITK_L2) stays as an A/B path -- bitwise equal.
+  if (p.ksplit > 1 && std::getenv("TFB_SPLITK_L2") && !std::getenv("TFB_SPLITK_DSMEM")) {
     void* ws = nullptr;
     TFB_CHECK(ensure_scratch(w, r, 2, size_t(grid) * shp->NH * BM * 1024, &ws));
     p.ws = static_cast<uint8_t*>(ws);

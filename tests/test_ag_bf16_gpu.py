@@ -124,22 +124,27 @@ def test_push_loopback_ranks_share_the_sms(oracle):
 
 
 @pytest.mark.parametrize("m,n,k", [(1024, 7168, 512),   # <2,2> pair tiles, N % 512 != 0 (last tile half OOB)
-                                   (128, 8192, 2048),   # <1,1> + split-K (L2 exchange)
-                                   (256, 2304, 1024)])  # <2,1> or <2,2> + split-K (DSMEM exchange)
+                                   (128, 8192, 2048),   # <1,1> + split-K
+                                   (256, 2304, 1024)])  # <2,1> or <2,2> + split-K
 def test_b_box_and_splitk_exchange_bitwise(oracle, monkeypatch, m, n, k):
     """The 4-D B box (a CTA's whole B stage in one TMA box) stages the same
     bytes as the per-chunk 2-D boxes, and the L2 split-K exchange sums the
     same partials in the same order as the DSMEM one: C is bitwise equal
-    across TFB_NO_B4 / TFB_SPLITK_DSMEM, and within the bf16 bar."""
+    across TFB_NO_B4 / TFB_SPLITK_L2 (/ TFB_SPLITK_LSU), and within the bf16 bar."""
     import torch
     p = bf16_problem(m + n + k, m, n, k, oracle)
     base = tf.ag.run_pull(p, tf.WorldConfig(world_size=1), dtype=1).c[0]
     monkeypatch.setenv("TFB_NO_B4", "1")
     no_b4 = tf.ag.run_pull(p, tf.WorldConfig(world_size=1), dtype=1).c[0]
     monkeypatch.delenv("TFB_NO_B4")
-    monkeypatch.setenv("TFB_SPLITK_DSMEM", "1")
-    dsmem = tf.ag.run_pull(p, tf.WorldConfig(world_size=1), dtype=1).c[0]
+    monkeypatch.setenv("TFB_SPLITK_L2", "1")  # default: DSMEM exchange; this: the L2 bulk-copy one
+    via_l2 = tf.ag.run_pull(p, tf.WorldConfig(world_size=1), dtype=1).c[0]
+    monkeypatch.delenv("TFB_SPLITK_L2")
+    monkeypatch.setenv("TFB_SPLITK_LSU", "1")
+    monkeypatch.setenv("TFB_SPLITK_L2", "1")  # L2 exchange, slices stored by every thread
+    via_l2_lsu = tf.ag.run_pull(p, tf.WorldConfig(world_size=1), dtype=1).c[0]
     assert np.array_equal(base, no_b4)
-    assert np.array_equal(base, dsmem)
+    assert np.array_equal(base, via_l2)
+    assert np.array_equal(base, via_l2_lsu)
     ref = (torch.from_numpy(p.a).double() @ torch.from_numpy(p.b).double()).float().numpy()
     assert norm_err(base, ref) <= TOL
