@@ -63,13 +63,16 @@ constexpr int GATHER_T = NUM_THREADS - 192;  // gather threads (PULL)
 constexpr int TMEM_COLS = 512;
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 
-template <int CG, int NH_>
+template <int CG, int NH_, int BK_ = 64>
 struct Cfg {
   static constexpr int NH = NH_;                        // 256-column MMA halves per tile
   static constexpr int BN_TILE = 256 * NH;              // tile width
   static constexpr int ACC_BUFS = NH == 2 ? 1 : 2;      // accumulators in 512 TMEM columns
+  static constexpr int BK = BK_;                        // k-block depth (64, or 128 for narrow pair tiles)
+  static constexpr int A_BYTES = BM * BK_ * 2;          // 16 / 32 KB: BK / 64 A boxes of 64 columns
   // Narrow pair tiles (32 KB stages) fit six in flight: the skinny main loop is load-latency bound.
-  static constexpr int STAGES = (CG == 2 && NH_ == 1) ? 6 : 4;
+  // With 128-deep k-blocks (64 KB stages) three: the same bytes in flight, half the ring rounds.
+  static constexpr int STAGES = (CG == 2 && NH_ == 1) ? (BK_ == 128 ? 3 : 6) : 4;
   static constexpr int CPH = 4 / CG;                    // 64-column B chunks per half per CTA
   static constexpr int B_BYTES = NH * CPH * BK * 128;   // 32 KB
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES; // 48 KB
@@ -345,7 +348,7 @@ __device__ __forceinline__ void splitk_sum(const SumArgs& a, const AgTcParams& p
   }
 }
 
-template <int CG, int NH_>
+template <int CG, int NH_, int BK_ = 64>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     ag_gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA_own,
                          const __grid_constant__ CUtensorMap tmA_inbox,
@@ -354,8 +357,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                          const __grid_constant__ CUtensorMap tmB4, const AgTcParams p) {
   pdl_launch();
   if (p.dbg & 65536) pdl_wait();  // A/B knob: wait at entry (round-2 placement)
-  using K_ = Cfg<CG, NH_>;
+  using K_ = Cfg<CG, NH_, BK_>;
   constexpr int STAGES = K_::STAGES, NH = K_::NH, CPH = K_::CPH;
+  constexpr int BK = K_::BK, A_BYTES = K_::A_BYTES;  // shadow the 64-deep globals
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
@@ -508,8 +512,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           else mbar_arrive_cluster(bar);
           if (!skip_a) {
             uint8_t* a_dst = smA + stage * A_BYTES;
-            if (from_own) tma_load<CG>(a_dst, &tmA_own, bar, kb * BK - a_col_own, m0 - a_row_own, pol_a);
-            else tma_load<CG>(a_dst, &tmA_inbox, bar, kb * BK, m0, pol_a);
+#pragma unroll
+            for (int ab = 0; ab < BK / 64; ++ab) {  // 64-column boxes (SW128's 128-byte rows)
+              if (from_own)
+                tma_load<CG>(a_dst + ab * (BM * 128), &tmA_own, bar, kb * BK + ab * 64 - a_col_own, m0 - a_row_own,
+                             pol_a);
+              else tma_load<CG>(a_dst + ab * (BM * 128), &tmA_inbox, bar, kb * BK + ab * 64, m0, pol_a);
+            }
           }
           uint8_t* b_dst = smB + stage * K_::B_BYTES;
           if (skip_b) {
@@ -571,8 +580,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint64_t b_st = bdesc0 + uint64_t(uint32_t(stg * K_::B_BYTES) >> 4);
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k) {
-          // A: K-major SW128, 8-row groups 1024 B apart; +32 B per K=16.
-          const uint64_t ad = a_st + uint64_t((k * 32) >> 4);
+          // A: K-major SW128, 8-row groups 1024 B apart; +32 B per K=16
+          // inside a 64-column box, boxes BM * 128 B apart.
+          const uint64_t ad = a_st + uint64_t(((k >> 2) * (BM * 128) + (k & 3) * 32) >> 4);
           // B: MN-major SW128, 64-column chunks 8 KB apart (LBO), 8-row K
           // groups 1 KB apart (SBO); +16 rows (2 KB) per K=16.  Whole tiles
           // take the unrolled constant-descriptor path: the single issuing
@@ -1216,10 +1226,11 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
     size_t smem;
     int id;
   };
-  const Shape shapes[3] = {
+  const Shape shapes[4] = {
       {1, 1, ag_gemm_sm100_kernel<1, 1>, Cfg<1, 1>::SMEM, 0},
       {2, 2, ag_gemm_sm100_kernel<2, 2>, Cfg<2, 2>::SMEM, 1},
       {2, 1, ag_gemm_sm100_kernel<2, 1>, Cfg<2, 1>::SMEM, 2},
+      {2, 1, ag_gemm_sm100_kernel<2, 1, 128>, Cfg<2, 1, 128>::SMEM, 3},  // narrow, 128-deep k-blocks
   };
   // Skinny M: too few tiles to occupy the SMs -> split K across a cluster
   // of S CTAs (pairs) per tile, reduced in-kernel through DSMEM in
@@ -1244,7 +1255,7 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
       // Per (shape, split, device) occupancy cache; atomics so concurrent
       // worlds on other host threads never race on it (a stale read only
       // recomputes the same value).
-      static std::atomic<int> max_active[3][9][16];
+      static std::atomic<int> max_active[4][9][16];
       std::atomic<int>& slot = max_active[shp.id][ks][dev & 15];
       int ma = slot.load(std::memory_order_relaxed);
       if (ma == 0) {
@@ -1321,6 +1332,26 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
       TFB_CHECK(plan(*shp, tiles, num_n, ks));
     }
   }
+  // Narrow pair tiles take 128-deep k-blocks when every owner band is a
+  // whole number of them: their k-block is paced by a ~560-cycle producer /
+  // MMA ring round, not by its 4 MMAs (TFB_DEBUG 8192 cadence), so half the
+  // rounds per FLOP (profiles/r2_skinny_analysis.md).  TFB_BK64 keeps 64.
+  int bk = 64;
+  if (shp->id == 2 && (p.msharded ? sh.k % 128 == 0 : kw % 128 == 0) && !std::getenv("TFB_BK64")) {
+    const int kb64 = p.kb_total, kbw64 = p.kbw;
+    p.kb_total = int(sh.k / 128);
+    p.kbw = int(kw / 128);
+    int t3, n3, k3;
+    TFB_CHECK(plan(shapes[3], t3, n3, k3));
+    if (t3 == tiles && k3 == ks) {
+      shp = &shapes[3];
+      bk = 128;
+      TFB_CHECK(make_map(&mB, b, sh.n, sh.k, ldb, 64, 128));
+    } else {  // the deeper k-block would change the split: keep 64
+      p.kb_total = kb64;
+      p.kbw = kbw64;
+    }
+  }
   const int CG = shp->CG;
   p.num_n = num_n;
   p.mt_rot = (p.msharded && own >= 0) ? (own * p.mpr / CG) % ((p.num_m + CG - 1) / CG) : 0;
@@ -1330,12 +1361,12 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
   p.q_tail = 1;
   p.total_items = tiles * ks;
   if (std::getenv("TFB_KSPLIT_VERBOSE"))
-    std::fprintf(stderr, "[ag] m=%zu n=%zu k=%zu CG=%d NH=%d tiles=%d ksplit=%d\n", sh.m, sh.n, sh.k, CG,
-                 shp->NH, tiles, ks);
+    std::fprintf(stderr, "[ag] m=%zu n=%zu k=%zu CG=%d NH=%d BK=%d tiles=%d ksplit=%d\n", sh.m, sh.n, sh.k, CG,
+                 shp->NH, bk, tiles, ks);
   p.ldc = int(ldc);
   auto kern = shp->kern;
   const size_t smem = shp->smem;
-  static std::atomic<bool> attr_set[3][64];  // idempotent attribute, set once per (shape, device)
+  static std::atomic<bool> attr_set[4][64];  // idempotent attribute, set once per (shape, device)
   if (!attr_set[shp->id][dev & 63].load(std::memory_order_acquire)) {
     TFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr_set[shp->id][dev & 63].store(true, std::memory_order_release);
@@ -1405,7 +1436,7 @@ static tf_status launch_gemm(World* w, int r, const tf_ag_shape& sh, const void*
     EncodeFn enc = encode_fn();
     cuuint64_t dims[4] = {64, sh.k, 4, sh.n / 256};
     cuuint64_t strides[3] = {ldb * 2, 128, 512};
-    cuuint32_t box[4] = {64, uint32_t(BK), uint32_t(4 / CG), uint32_t(shp->NH)};
+    cuuint32_t box[4] = {64, uint32_t(bk), uint32_t(4 / CG), uint32_t(shp->NH)};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     if (enc && enc(&mB4, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(b), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
@@ -1689,6 +1720,7 @@ void ag_sm100_preload() {  // see ag_exact_preload
   cudaFuncGetAttributes(&a, ag_gemm_sm100_kernel<1, 1>);
   cudaFuncGetAttributes(&a, ag_gemm_sm100_kernel<2, 2>);
   cudaFuncGetAttributes(&a, ag_gemm_sm100_kernel<2, 1>);
+  cudaFuncGetAttributes(&a, ag_gemm_sm100_kernel<2, 1, 128>);
   cudaFuncGetAttributes(&a, ag_push_kernel);
 }
 

@@ -125,12 +125,16 @@ def test_push_loopback_ranks_share_the_sms(oracle):
 
 @pytest.mark.parametrize("m,n,k", [(1024, 7168, 512),   # <2,2> pair tiles, N % 512 != 0 (last tile half OOB)
                                    (128, 8192, 2048),   # <1,1> + split-K
-                                   (256, 2304, 1024)])  # <2,1> or <2,2> + split-K
+                                   (256, 2304, 1024),   # <2,1> or <2,2> + split-K
+                                   (256, 8192, 2048),   # <2,1> narrow pair tiles, 128-deep k-blocks, split-K
+                                   (512, 4096, 384)])   # narrow, K = 384: 128-deep k-blocks, whole K
 def test_b_box_and_splitk_exchange_bitwise(oracle, monkeypatch, m, n, k):
     """The 4-D B box (a CTA's whole B stage in one TMA box) stages the same
     bytes as the per-chunk 2-D boxes, and the L2 split-K exchange sums the
     same partials in the same order as the DSMEM one: C is bitwise equal
-    across TFB_NO_B4 / TFB_SPLITK_L2 (/ TFB_SPLITK_LSU), and within the bf16 bar."""
+    across TFB_NO_B4 / TFB_SPLITK_L2 (/ TFB_SPLITK_LSU) / TFB_BK64 (narrow pair
+    tiles on 64- instead of 128-deep k-blocks: the same k order per element),
+    and within the bf16 bar."""
     import torch
     p = bf16_problem(m + n + k, m, n, k, oracle)
     base = tf.ag.run_pull(p, tf.WorldConfig(world_size=1), dtype=1).c[0]
@@ -143,6 +147,11 @@ def test_b_box_and_splitk_exchange_bitwise(oracle, monkeypatch, m, n, k):
     monkeypatch.setenv("TFB_SPLITK_LSU", "1")
     monkeypatch.setenv("TFB_SPLITK_L2", "1")  # L2 exchange, slices stored by every thread
     via_l2_lsu = tf.ag.run_pull(p, tf.WorldConfig(world_size=1), dtype=1).c[0]
+    monkeypatch.delenv("TFB_SPLITK_LSU")
+    monkeypatch.delenv("TFB_SPLITK_L2")
+    monkeypatch.setenv("TFB_BK64", "1")  # narrow pair tiles: 64-deep instead of 128-deep k-blocks
+    bk64 = tf.ag.run_pull(p, tf.WorldConfig(world_size=1), dtype=1).c[0]
+    assert np.array_equal(base, bk64)
     assert np.array_equal(base, no_b4)
     assert np.array_equal(base, via_l2)
     assert np.array_equal(base, via_l2_lsu)
