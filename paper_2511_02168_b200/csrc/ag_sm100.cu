@@ -919,8 +919,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         else l2 ? splitk_sum<8, true>(sa, p) : splitk_sum<8, false>(sa, p);
       }
       if (tsd && threadIdx.x == 0) s_ts[5 + h] = globaltimer_ns();  // half h summed + stored
-      if (p.ws) named_bar(2, NUM_THREADS);  // R fully read before the next half's dump
-      else cluster_sync();  // siblings done reading R before it is rewritten / released
+      // R fully read (siblings included) before the next half's dump; after
+      // the last half the kernel's closing cluster barrier does it.
+      if (h + 1 < NH) {
+        if (p.ws) named_bar(2, NUM_THREADS);
+        else cluster_sync();
+      }
     }
   }
 
