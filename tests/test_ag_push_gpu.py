@@ -34,7 +34,8 @@ def same(a, b):
 @pytest.mark.parametrize("w,m,n,k", [(2, 300, 256, 2 * 64),     # 64-column boxes, ragged M
                                      (2, 256, 512, 2 * 128),    # 128-column boxes
                                      (4, 384, 256, 4 * 512),    # 256-column boxes, 2 per row
-                                     (8, 130, 264, 8 * 192)])   # 64-column boxes, W = 8, ragged M / N
+                                     (8, 130, 264, 8 * 192),    # 64-column boxes, W = 8, ragged M / N
+                                     (2, 300, 256, 2 * 512)])   # 64-row boxes: the last one wholly past M
 def test_tma_and_register_producers_agree(oracle, monkeypatch, w, m, n, k):
     import torch
     p = bf16_problem(w * 100 + m, m, n, k, oracle)
